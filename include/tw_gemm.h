@@ -1,0 +1,135 @@
+/*
+ * tw_gemm.h -- C ABI of the B200-native TW / TEW sparse matmul
+ * (libtwgemm.so, built from paper_2402_10876_b200/csrc for sm_100a).
+ *
+ * The reference (tilesparse 0.1.0, pure Python) has no FFI; its boundary for
+ * this path is the Python call surface of executor.py / formats.py.  Each
+ * entry point below names the reference function it replaces; the Python
+ * shim in paper_2402_10876_b200/executor.py keeps the reference signatures
+ * and calls these through ctypes.
+ *
+ * Conventions
+ *   - Plain C types only: host pointers for weights/encodings, device
+ *     pointers for activations/outputs, cudaStream_t passed as void*.
+ *   - Activations are A^T: K rows x M tokens, tokens contiguous, row pitch
+ *     ld_at elements (ld_at % 8 == 0, 16-byte aligned base).  Outputs are
+ *     C'^T: one row per output column, tokens contiguous, pitch ld_ct.
+ *   - Stream-ordered, no host synchronisation inside tw_gemm / tw_gemm_tew /
+ *     tw_transpose_cast, so they are CUDA-graph capturable.
+ *   - Every function returns a status code; tw_last_error() gives the
+ *     thread-local message of the last failure.
+ */
+#ifndef TW_GEMM_H_
+#define TW_GEMM_H_
+
+#include <stdint.h>
+#include <stddef.h>
+
+#if defined(__GNUC__)
+#define TW_API __attribute__((visibility("default")))
+#else
+#define TW_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes: mirror tilesparse.errors (errors.py:4-17) and the CLI exit
+ * codes (cli.py:40-45). */
+#define TW_OK 0
+#define TW_ERR_INVALID_INPUT 2   /* InvalidInputError                     */
+#define TW_ERR_CONTRACT 3        /* ContractViolationError                */
+#define TW_ERR_CORRUPT 4         /* CorruptEncodingError (CLI exit 2)     */
+#define TW_ERR_CUDA 5            /* CUDA / driver failure (no reference)  */
+
+/* Element types. */
+#define TW_F32 0
+#define TW_F16 1
+#define TW_BF16 2
+
+/* Sub-tile visiting order inside each 128-token block
+ * (executor.py:206-227 schedule_tiles strategies). */
+#define TW_SCHEDULE_LPT 0          /* descending surviving K'             */
+#define TW_SCHEDULE_ROUND_ROBIN 1  /* tile order                          */
+
+typedef struct tw_plan tw_plan;
+
+typedef struct tw_plan_info {
+  int32_t k, n, g;            /* original dims and tile width            */
+  int32_t n_tiles;            /* TW tiles                                */
+  int32_t n_sub;              /* UMMA-N slices (== n_tiles when g <= 256) */
+  int32_t bn;                 /* UMMA N of the kernel instance           */
+  int32_t kp;                 /* padded gather-list length               */
+  int32_t n_condensed;        /* N' = sum of tile widths                 */
+  int32_t n_union;            /* |TW cols U overlay cols| (TEW), else N' */
+  int32_t compute_dtype;      /* TW_F16 | TW_BF16                        */
+  int64_t nnz;                /* overlay entries (0 when none)           */
+  int64_t kept_macs_per_token;/* sum_i width_i * K'_i (+ nnz for TEW)    */
+  int32_t sm_count;           /* SMs of the plan's device                */
+  int32_t has_overlay;
+} tw_plan_info;
+
+/* Build a device plan from a CTO encoding held in host memory.
+ * Replaces: formats.CtoEncoding (formats.py:82-181) as consumed by
+ * executor.gemm_cto (executor.py:149-177).  Validates exactly what
+ * gemm_cto validates (offset decode of tile_rows / tile_cols, columns
+ * strictly increasing across tiles -> TW_ERR_CORRUPT), converts the fp32
+ * payload to compute_dtype on the device and builds the gather lists.
+ *   row_offsets: n_tiles x max_rows u32, col_offsets: n_tiles x max_cols u32,
+ *   payload: sum(row_counts[i]*col_counts[i]) fp32, per tile transposed
+ *            (width x kept rows, kept rows contiguous; formats.py:200).
+ * Synchronises `stream` before returning. */
+TW_API int tw_plan_create_cto(tw_plan** out, int32_t k, int32_t n, int32_t g, int32_t n_tiles,
+                       const uint32_t* row_counts, const uint32_t* col_counts,
+                       const uint32_t* row_offsets, int32_t max_rows,
+                       const uint32_t* col_offsets, int32_t max_cols, const float* payload,
+                       int32_t compute_dtype, int32_t schedule, void* stream);
+
+/* Attach a TEW overlay (CSC, int64 like patterns.SparseOverlay,
+ * patterns.py:145-214).  Replaces the overlap/dims checks of
+ * executor.gemm_tew (executor.py:186-193): dims mismatch -> TW_ERR_INVALID_INPUT,
+ * an entry on a payload slot -> TW_ERR_CONTRACT.  Computes the union column
+ * layout of the TEW output (executor.py:201-203). */
+TW_API int tw_plan_attach_overlay(tw_plan* plan, int32_t k, int32_t n, int64_t nnz,
+                           const int64_t* col_ptr, const int64_t* row_idx, const float* values,
+                           void* stream);
+
+TW_API int tw_plan_get_info(const tw_plan* plan, tw_plan_info* info);
+
+/* Output column maps (host buffers sized n_condensed / n_union):
+ * original column id of every row of C'^T. */
+TW_API int tw_plan_condensed_columns(const tw_plan* plan, int32_t* out_cols);
+TW_API int tw_plan_union_columns(const tw_plan* plan, int32_t* out_cols);
+
+/* TW product, condensed: ct[N' x M] = (A . W_tw)^T.
+ * Replaces: executor.gemm_cto (executor.py:149-177), gemm_tile_sparse
+ * (executor.py:135-146) and execute_batched (executor.py:230-265); all three
+ * are bit-identical on the GPU as in the reference. */
+TW_API int tw_gemm(const tw_plan* plan, const void* at, int64_t m, int64_t ld_at, void* ct,
+            int64_t ld_ct, int32_t out_dtype, void* stream);
+
+/* TEW product over the union columns: ct[|union| x M].
+ * Replaces: executor.gemm_tew (executor.py:180-203). */
+TW_API int tw_gemm_tew(const tw_plan* plan, const void* at, int64_t m, int64_t ld_at, void* ct,
+                int64_t ld_ct, int32_t out_dtype, void* stream);
+
+/* A (m x k row-major, pitch lda, a_dtype) -> A^T (k x m, pitch ld_at, at_dtype).
+ * Replaces the float32/float64 carrier copies of core.as_matrix
+ * (core.py:32-43) and executor.py:158 on the device. */
+TW_API int tw_transpose_cast(const void* a, int32_t a_dtype, int64_t m, int64_t k, int64_t lda,
+                      void* at, int32_t at_dtype, int64_t ld_at, void* stream);
+
+TW_API void tw_plan_destroy(tw_plan* plan);
+
+/* Thread-local message of the last failing call ("" if none). */
+TW_API const char* tw_last_error(void);
+
+/* ABI version (major * 100 + minor). */
+TW_API int32_t tw_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TW_GEMM_H_ */

@@ -1,0 +1,476 @@
+// C ABI (include/tw_gemm.h): host-side validation of CTO encodings and
+// overlays, construction of the device weight format, TMA descriptor
+// encoding, and kernel dispatch.  All numerics run in the kernels of
+// tw_gemm.cu / tw_aux.cu; nothing here computes on the CPU beyond index
+// bookkeeping.
+#include "../../include/tw_gemm.h"
+#include "tw_kernels.cuh"
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <iterator>
+#include <memory>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <vector>
+
+using namespace tw;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int status, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return status;
+}
+
+#define TW_CUDA(expr)                                                                    \
+  do {                                                                                   \
+    cudaError_t _e = (expr);                                                             \
+    if (_e != cudaSuccess)                                                               \
+      return fail(TW_ERR_CUDA, "%s failed: %s", #expr, cudaGetErrorString(_e));          \
+  } while (0)
+
+// ------------------------------------------------------- driver entry point
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+// 2-D tensor map over a row-major [rows][cols] 16-bit matrix (cols contiguous).
+int make_map_2d(CUtensorMap* map, const void* base, int32_t dtype, uint64_t cols, uint64_t rows,
+                uint64_t pitch_elems, uint32_t box_cols, uint32_t box_rows) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return fail(TW_ERR_CUDA, "cuTensorMapEncodeTiled unavailable (driver too old?)");
+  const CUtensorMapDataType dt =
+      dtype == kBF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {pitch_elems * 2};
+  cuuint32_t box[2] = {box_cols, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, dt, 2, const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(TW_ERR_INVALID_INPUT,
+                "cuTensorMapEncodeTiled failed (%d): cols=%llu rows=%llu pitch=%llu", (int)r,
+                (unsigned long long)cols, (unsigned long long)rows,
+                (unsigned long long)pitch_elems);
+  return TW_OK;
+}
+
+int sm_count_of_current_device(int* out) {
+  int dev = 0;
+  TW_CUDA(cudaGetDevice(&dev));
+  TW_CUDA(cudaDeviceGetAttribute(out, cudaDevAttrMultiProcessorCount, dev));
+  return TW_OK;
+}
+
+template <class T>
+int upload(T** dptr, const std::vector<T>& host, cudaStream_t s) {
+  *dptr = nullptr;
+  if (host.empty()) return TW_OK;
+  TW_CUDA(cudaMalloc(reinterpret_cast<void**>(dptr), host.size() * sizeof(T)));
+  TW_CUDA(cudaMemcpyAsync(*dptr, host.data(), host.size() * sizeof(T), cudaMemcpyHostToDevice, s));
+  return TW_OK;
+}
+
+}  // namespace
+
+struct tw_plan {
+  int32_t k = 0, n = 0, g = 0, n_tiles = 0, n_sub = 0, bn = 0, kp = 0, n_cond = 0;
+  int32_t dtype = kF16, schedule = TW_SCHEDULE_LPT, sm_count = 0;
+  std::vector<SubTile> subtiles;
+  std::vector<int32_t> cond_cols;        // condensed col -> original col
+  std::vector<int32_t> tile_of_col;      // original col -> tile (or -1)
+  std::vector<std::vector<uint8_t>> tile_rows;  // per tile: K flags
+  std::vector<int32_t> tile_first_cond;  // per tile: first condensed column
+  int64_t kept_macs = 0;
+  // device
+  int32_t* d_rowidx = nullptr;
+  SubTile* d_subtiles = nullptr;
+  int32_t* d_order = nullptr;
+  void* d_payload = nullptr;
+  CUtensorMap map_pay;
+  // TEW overlay
+  bool has_overlay = false;
+  int64_t nnz = 0;
+  std::vector<int32_t> union_cols;
+  int32_t* d_union_rowmap = nullptr;  // condensed col -> union position
+  int32_t n_ov_cols = 0;
+  int32_t* d_ov_start = nullptr;
+  int32_t* d_ov_rows = nullptr;
+  float* d_ov_vals = nullptr;
+  int32_t* d_ov_out = nullptr;
+  int32_t* d_ov_acc = nullptr;
+
+  ~tw_plan() {
+    for (void* p : {(void*)d_rowidx, (void*)d_subtiles, (void*)d_order, d_payload,
+                    (void*)d_union_rowmap, (void*)d_ov_start, (void*)d_ov_rows, (void*)d_ov_vals,
+                    (void*)d_ov_out, (void*)d_ov_acc})
+      if (p) cudaFree(p);
+  }
+};
+
+extern "C" {
+
+const char* tw_last_error(void) { return g_last_error.c_str(); }
+
+int32_t tw_abi_version(void) { return 100; }
+
+int tw_plan_create_cto(tw_plan** out, int32_t k, int32_t n, int32_t g, int32_t n_tiles,
+                       const uint32_t* row_counts, const uint32_t* col_counts,
+                       const uint32_t* row_offsets, int32_t max_rows,
+                       const uint32_t* col_offsets, int32_t max_cols, const float* payload,
+                       int32_t compute_dtype, int32_t schedule, void* stream) {
+  g_last_error.clear();
+  if (!out) return fail(TW_ERR_INVALID_INPUT, "out is null");
+  *out = nullptr;
+  if (k < 1 || n < 1 || g < 1) return fail(TW_ERR_INVALID_INPUT, "dims must be >= 1");
+  if (compute_dtype != kF16 && compute_dtype != kBF16)
+    return fail(TW_ERR_INVALID_INPUT, "compute dtype must be fp16 or bf16");
+  if (schedule != TW_SCHEDULE_LPT && schedule != TW_SCHEDULE_ROUND_ROBIN)
+    return fail(TW_ERR_INVALID_INPUT, "unknown schedule %d", schedule);
+  // CtoEncoding.__post_init__ (formats.py:94-127)
+  if (n_tiles < 1) return fail(TW_ERR_CORRUPT, "encoding must contain at least one tile");
+  if (!row_counts || !col_counts || !row_offsets || !col_offsets || !payload)
+    return fail(TW_ERR_INVALID_INPUT, "null encoding array");
+  uint32_t max_h = 0, max_w = 0;
+  for (int i = 0; i < n_tiles; ++i) {
+    if (row_counts[i] < 1 || col_counts[i] < 1)
+      return fail(TW_ERR_CORRUPT, "every tile must keep at least one row and one column");
+    max_h = std::max(max_h, row_counts[i]);
+    max_w = std::max(max_w, col_counts[i]);
+  }
+  if ((uint32_t)max_rows < max_h)
+    return fail(TW_ERR_CORRUPT, "row offsets narrower than the largest row count");
+  if ((uint32_t)max_cols < max_w)
+    return fail(TW_ERR_CORRUPT, "col offsets narrower than the largest col count");
+
+  auto plan = new tw_plan();
+  std::unique_ptr<tw_plan> guard(plan);
+  plan->k = k;
+  plan->n = n;
+  plan->g = g;
+  plan->n_tiles = n_tiles;
+  plan->dtype = compute_dtype;
+  plan->schedule = schedule;
+  if (int st = sm_count_of_current_device(&plan->sm_count)) return st;
+  TW_CUDA(configure_gemm_kernels());
+
+  // decode offsets: tile_rows / tile_cols (formats.py:138-158) and the column
+  // order check of gemm_cto (executor.py:478-480)
+  plan->tile_of_col.assign(n, -1);
+  plan->tile_rows.resize(n_tiles);
+  std::vector<std::vector<int32_t>> rows(n_tiles);
+  int64_t prev_col = -1;
+  for (int i = 0; i < n_tiles; ++i) {
+    const uint32_t h = row_counts[i], w = col_counts[i];
+    rows[i].resize(h);
+    plan->tile_rows[i].assign(k, 0);
+    int64_t prev = -1;
+    for (uint32_t j = 0; j < h; ++j) {
+      const int64_t r = (int64_t)j + row_offsets[(int64_t)i * max_rows + j];
+      if (r <= prev || r >= k)
+        return fail(TW_ERR_CORRUPT,
+                    "tile %d: reconstructed rows are not strictly increasing within [0, %d)", i,
+                    k);
+      rows[i][j] = (int32_t)r;
+      plan->tile_rows[i][r] = 1;
+      prev = r;
+    }
+    plan->tile_first_cond.push_back((int32_t)plan->cond_cols.size());
+    int64_t prevc = -1;
+    for (uint32_t j = 0; j < w; ++j) {
+      const int64_t c = (int64_t)j + col_offsets[(int64_t)i * max_cols + j];
+      if (c <= prevc || c >= n)
+        return fail(TW_ERR_CORRUPT,
+                    "tile %d: reconstructed cols are not strictly increasing within [0, %d)", i,
+                    n);
+      if (c <= prev_col)
+        return fail(TW_ERR_CORRUPT, "tile column ranges overlap or are out of order");
+      plan->cond_cols.push_back((int32_t)c);
+      plan->tile_of_col[c] = i;
+      prevc = c;
+      prev_col = c;
+    }
+    plan->kept_macs += (int64_t)h * w;
+  }
+  plan->n_cond = (int32_t)plan->cond_cols.size();
+
+  // kernel geometry
+  const int bn = max_w <= 32 ? 32 : max_w <= 64 ? 64 : max_w <= 128 ? 128 : 256;
+  plan->bn = bn;
+  plan->kp = (int32_t)(((max_h + kBK - 1) / kBK) * kBK);
+  std::vector<int64_t> src_base;
+  std::vector<int32_t> src_ld;
+  int64_t pbase = 0;
+  for (int i = 0; i < n_tiles; ++i) {
+    const int32_t h = (int32_t)row_counts[i], w = (int32_t)col_counts[i];
+    for (int32_t c0 = 0; c0 < w; c0 += bn) {
+      SubTile st{};
+      st.kp_steps = (h + kBK - 1) / kBK;
+      st.idx_row = i;
+      st.pay_row = (int32_t)plan->subtiles.size() * bn;
+      st.width = std::min(bn, w - c0);
+      st.out_row = plan->tile_first_cond[i] + c0;
+      st.kept = h;
+      plan->subtiles.push_back(st);
+      src_base.push_back(pbase + (int64_t)c0 * h);
+      src_ld.push_back(h);
+    }
+    pbase += (int64_t)h * w;
+  }
+  plan->n_sub = (int32_t)plan->subtiles.size();
+  std::vector<int32_t> order(plan->n_sub);
+  std::iota(order.begin(), order.end(), 0);
+  if (schedule == TW_SCHEDULE_LPT) {
+    // executor.py:526 sorts tiles by (-macs, index); per 128-token block the
+    // MACs of a sub-tile are proportional to K' * width
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
+      const int64_t wa = (int64_t)plan->subtiles[a].kept * plan->subtiles[a].width;
+      const int64_t wb = (int64_t)plan->subtiles[b].kept * plan->subtiles[b].width;
+      return wa > wb;
+    });
+  }
+  std::vector<int32_t> rowidx((size_t)n_tiles * plan->kp, k);  // pad = K -> TMA OOB zero fill
+  for (int i = 0; i < n_tiles; ++i)
+    std::copy(rows[i].begin(), rows[i].end(), rowidx.begin() + (size_t)i * plan->kp);
+
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (int st = upload(&plan->d_rowidx, rowidx, s)) return st;
+  if (int st = upload(&plan->d_subtiles, plan->subtiles, s)) return st;
+  if (int st = upload(&plan->d_order, order, s)) return st;
+  int64_t* d_src_base = nullptr;
+  int32_t* d_src_ld = nullptr;
+  float* d_src = nullptr;
+  if (int st = upload(&d_src_base, src_base, s)) return st;
+  if (int st = upload(&d_src_ld, src_ld, s)) return st;
+  TW_CUDA(cudaMalloc(&d_src, std::max<int64_t>(pbase, 1) * sizeof(float)));
+  TW_CUDA(cudaMemcpyAsync(d_src, payload, pbase * sizeof(float), cudaMemcpyHostToDevice, s));
+  const size_t pay_bytes = (size_t)plan->n_sub * bn * plan->kp * 2;
+  TW_CUDA(cudaMalloc(&plan->d_payload, pay_bytes));
+  PayloadArgs pa{d_src, d_src_base, d_src_ld, plan->d_subtiles, plan->d_payload,
+                 compute_dtype, bn, plan->kp, plan->n_sub};
+  TW_CUDA(launch_build_payload(pa, s));
+  TW_CUDA(cudaStreamSynchronize(s));
+  cudaFree(d_src);
+  cudaFree(d_src_base);
+  cudaFree(d_src_ld);
+  if (int st = make_map_2d(&plan->map_pay, plan->d_payload, compute_dtype, plan->kp,
+                           (uint64_t)plan->n_sub * bn, plan->kp, kBK, bn))
+    return st;
+  plan->union_cols = plan->cond_cols;
+  *out = guard.release();
+  return TW_OK;
+}
+
+int tw_plan_attach_overlay(tw_plan* p, int32_t k, int32_t n, int64_t nnz, const int64_t* col_ptr,
+                           const int64_t* row_idx, const float* values, void* stream) {
+  g_last_error.clear();
+  if (!p) return fail(TW_ERR_INVALID_INPUT, "plan is null");
+  if (k != p->k || n != p->n)
+    return fail(TW_ERR_INVALID_INPUT, "overlay dims (%d, %d) do not match weights (%d, %d)", k,
+                n, p->k, p->n);
+  if (nnz < 0 || !col_ptr || (nnz > 0 && (!row_idx || !values)))
+    return fail(TW_ERR_INVALID_INPUT, "malformed overlay arrays");
+  if (col_ptr[0] != 0 || col_ptr[n] != nnz)
+    return fail(TW_ERR_INVALID_INPUT, "malformed overlay column pointers");
+  // overlap check of gemm_tew (executor.py:190-193) + union (executor.py:201-203)
+  std::vector<int32_t> ov_cols;
+  for (int32_t c = 0; c < n; ++c) {
+    const int64_t lo = col_ptr[c], hi = col_ptr[c + 1];
+    if (hi < lo) return fail(TW_ERR_INVALID_INPUT, "overlay column pointers must be non-decreasing");
+    if (hi == lo) continue;
+    ov_cols.push_back(c);
+    const int t = p->tile_of_col[c];
+    for (int64_t e = lo; e < hi; ++e) {
+      const int64_t r = row_idx[e];
+      if (r < 0 || r >= k || (e > lo && r <= row_idx[e - 1]))
+        return fail(TW_ERR_INVALID_INPUT, "overlay rows must be strictly increasing within a column");
+      if (t >= 0 && p->tile_rows[t][r])
+        return fail(TW_ERR_CONTRACT, "overlay entries overlap tile payload positions");
+    }
+  }
+  std::vector<int32_t> uni;
+  std::set_union(p->cond_cols.begin(), p->cond_cols.end(), ov_cols.begin(), ov_cols.end(),
+                 std::back_inserter(uni));
+  std::vector<int32_t> pos_of(n, -1);
+  for (size_t i = 0; i < uni.size(); ++i) pos_of[uni[i]] = (int32_t)i;
+  std::vector<int32_t> rowmap(p->n_cond);
+  for (int32_t i = 0; i < p->n_cond; ++i) rowmap[i] = pos_of[p->cond_cols[i]];
+  std::vector<int32_t> start(1, 0), rows, out_rows, acc;
+  std::vector<float> vals;
+  for (int32_t c : ov_cols) {
+    for (int64_t e = col_ptr[c]; e < col_ptr[c + 1]; ++e) {
+      rows.push_back((int32_t)row_idx[e]);
+      vals.push_back(values[e]);
+    }
+    start.push_back((int32_t)rows.size());
+    out_rows.push_back(pos_of[c]);
+    acc.push_back(p->tile_of_col[c] >= 0 ? 1 : 0);
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  for (void* q : {(void*)p->d_union_rowmap, (void*)p->d_ov_start, (void*)p->d_ov_rows,
+                  (void*)p->d_ov_vals, (void*)p->d_ov_out, (void*)p->d_ov_acc})
+    if (q) cudaFree(q);
+  p->d_union_rowmap = nullptr;
+  p->d_ov_start = p->d_ov_rows = p->d_ov_out = p->d_ov_acc = nullptr;
+  p->d_ov_vals = nullptr;
+  if (int st = upload(&p->d_union_rowmap, rowmap, s)) return st;
+  if (int st = upload(&p->d_ov_start, start, s)) return st;
+  if (int st = upload(&p->d_ov_rows, rows, s)) return st;
+  if (int st = upload(&p->d_ov_vals, vals, s)) return st;
+  if (int st = upload(&p->d_ov_out, out_rows, s)) return st;
+  if (int st = upload(&p->d_ov_acc, acc, s)) return st;
+  TW_CUDA(cudaStreamSynchronize(s));
+  p->union_cols = uni;
+  p->n_ov_cols = (int32_t)ov_cols.size();
+  p->nnz = nnz;
+  p->has_overlay = true;
+  return TW_OK;
+}
+
+int tw_plan_get_info(const tw_plan* p, tw_plan_info* info) {
+  if (!p || !info) return fail(TW_ERR_INVALID_INPUT, "null argument");
+  info->k = p->k;
+  info->n = p->n;
+  info->g = p->g;
+  info->n_tiles = p->n_tiles;
+  info->n_sub = p->n_sub;
+  info->bn = p->bn;
+  info->kp = p->kp;
+  info->n_condensed = p->n_cond;
+  info->n_union = (int32_t)p->union_cols.size();
+  info->compute_dtype = p->dtype;
+  info->nnz = p->nnz;
+  info->kept_macs_per_token = p->kept_macs + p->nnz;
+  info->sm_count = p->sm_count;
+  info->has_overlay = p->has_overlay ? 1 : 0;
+  return TW_OK;
+}
+
+int tw_plan_condensed_columns(const tw_plan* p, int32_t* out) {
+  if (!p || !out) return fail(TW_ERR_INVALID_INPUT, "null argument");
+  std::copy(p->cond_cols.begin(), p->cond_cols.end(), out);
+  return TW_OK;
+}
+
+int tw_plan_union_columns(const tw_plan* p, int32_t* out) {
+  if (!p || !out) return fail(TW_ERR_INVALID_INPUT, "null argument");
+  std::copy(p->union_cols.begin(), p->union_cols.end(), out);
+  return TW_OK;
+}
+
+static int check_io(const tw_plan* p, const void* at, int64_t m, int64_t ld_at, const void* ct,
+                    int64_t ld_ct, int32_t out_dtype) {
+  if (!p || !at || !ct) return fail(TW_ERR_INVALID_INPUT, "null argument");
+  if (m < 1 || m > INT32_MAX) return fail(TW_ERR_INVALID_INPUT, "m must be in [1, 2^31)");
+  if (ld_at < m || ld_at % 8 != 0)
+    return fail(TW_ERR_INVALID_INPUT, "ld_at (%lld) must be >= m and a multiple of 8",
+                (long long)ld_at);
+  if (reinterpret_cast<uintptr_t>(at) % 16 != 0)
+    return fail(TW_ERR_INVALID_INPUT, "A^T base must be 16-byte aligned");
+  if (ld_ct < m) return fail(TW_ERR_INVALID_INPUT, "ld_ct must be >= m");
+  if (out_dtype != kF32 && out_dtype != kF16 && out_dtype != kBF16)
+    return fail(TW_ERR_INVALID_INPUT, "unknown output dtype %d", out_dtype);
+  return TW_OK;
+}
+
+static int run_tw(const tw_plan* p, const void* at, int64_t m, int64_t ld_at, void* ct,
+                  int64_t ld_ct, int32_t out_dtype, const int32_t* rowmap, cudaStream_t s) {
+  CUtensorMap map_at;
+  if (int st = make_map_2d(&map_at, at, p->dtype, (uint64_t)m, (uint64_t)p->k, (uint64_t)ld_at,
+                           64, 1))
+    return st;
+  GemmArgs a{};
+  a.rowidx = p->d_rowidx;
+  a.subtiles = p->d_subtiles;
+  a.order = p->d_order;
+  a.rowmap = rowmap;
+  a.out = ct;
+  a.ld_out = ld_ct;
+  a.out_dtype = out_dtype;
+  a.M = (int32_t)m;
+  a.Kp = p->kp;
+  a.n_sub = p->n_sub;
+  a.n_mblk = (int32_t)((m + kBM - 1) / kBM);
+  a.n_units = a.n_sub * a.n_mblk;
+  const int grid = std::min(a.n_units, p->sm_count);
+  TW_CUDA(launch_tw_gather_gemm(map_at, p->map_pay, a, p->bn, p->dtype, grid, s));
+  return TW_OK;
+}
+
+int tw_gemm(const tw_plan* p, const void* at, int64_t m, int64_t ld_at, void* ct, int64_t ld_ct,
+            int32_t out_dtype, void* stream) {
+  g_last_error.clear();
+  if (int st = check_io(p, at, m, ld_at, ct, ld_ct, out_dtype)) return st;
+  return run_tw(p, at, m, ld_at, ct, ld_ct, out_dtype, nullptr, static_cast<cudaStream_t>(stream));
+}
+
+int tw_gemm_tew(const tw_plan* p, const void* at, int64_t m, int64_t ld_at, void* ct,
+                int64_t ld_ct, int32_t out_dtype, void* stream) {
+  g_last_error.clear();
+  if (int st = check_io(p, at, m, ld_at, ct, ld_ct, out_dtype)) return st;
+  if (!p->has_overlay) return fail(TW_ERR_INVALID_INPUT, "plan has no overlay attached");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (int st = run_tw(p, at, m, ld_at, ct, ld_ct, out_dtype, p->d_union_rowmap, s)) return st;
+  ResidualArgs r{};
+  r.at = at;
+  r.ld_at = ld_at;
+  r.in_dtype = p->dtype;
+  r.col_start = p->d_ov_start;
+  r.rows = p->d_ov_rows;
+  r.vals = p->d_ov_vals;
+  r.out_rows = p->d_ov_out;
+  r.accumulate = p->d_ov_acc;
+  r.out = ct;
+  r.ld_out = ld_ct;
+  r.out_dtype = out_dtype;
+  r.M = (int32_t)m;
+  r.n_cols = p->n_ov_cols;
+  TW_CUDA(launch_tw_residual(r, s));
+  return TW_OK;
+}
+
+int tw_transpose_cast(const void* a, int32_t a_dtype, int64_t m, int64_t k, int64_t lda, void* at,
+                      int32_t at_dtype, int64_t ld_at, void* stream) {
+  g_last_error.clear();
+  if (!a || !at) return fail(TW_ERR_INVALID_INPUT, "null argument");
+  if (m < 1 || k < 1 || lda < k || ld_at < m)
+    return fail(TW_ERR_INVALID_INPUT, "bad transpose geometry");
+  for (int32_t d : {a_dtype, at_dtype})
+    if (d != kF32 && d != kF16 && d != kBF16)
+      return fail(TW_ERR_INVALID_INPUT, "unknown dtype %d", d);
+  TW_CUDA(launch_transpose_cast(a, a_dtype, m, k, lda, at, at_dtype, ld_at,
+                                static_cast<cudaStream_t>(stream)));
+  return TW_OK;
+}
+
+void tw_plan_destroy(tw_plan* p) { delete p; }
+
+}  // extern "C"

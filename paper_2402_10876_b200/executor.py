@@ -1,0 +1,470 @@
+"""The "matmul" step on B200: the reference executor API backed by sm_100a kernels.
+
+Keeps the call signatures of reference executor.py so it drops in for the
+TW/TEW path:
+
+* :func:`gemm_tile_sparse` -- executor.py:135-146
+* :func:`gemm_cto`         -- executor.py:149-177
+* :func:`execute_batched`  -- executor.py:230-265 (+ :func:`schedule_tiles` 206-227)
+* :func:`gemm_tew`         -- executor.py:180-203
+* :class:`GemmOutput`      -- executor.py:68-80
+* :class:`ExecutionTrace`  -- executor.py:83-118
+* :func:`relative_error`   -- executor.py:278-288
+
+Every product runs in ``libtwgemm.so`` (K1 ``tw_gather_gemm`` for TW, K1 +
+K2 ``tw_residual`` for TEW) on the current CUDA device and stream.  Numerics
+contract: operands are rounded once to ``compute_dtype``
+(fp16 default, bf16 optional), products accumulate in fp32 in TMEM, and the
+output is fp32 unless ``out_dtype`` asks for fp16/bf16.  The three TW entry
+points launch the same deterministic kernel, so -- as in the reference --
+their outputs are bit-identical to each other.
+
+Outputs live on the GPU: ``GemmOutput.condensed`` is an M x N' torch view of
+the kernel's native C'^T (N' x M) buffer.
+"""
+
+from __future__ import annotations
+
+import weakref
+from dataclasses import dataclass
+from typing import List, Optional, Tuple, Union
+
+import numpy as np
+
+from . import _native
+from .core import ACC_DTYPE, IndexMask, as_matrix
+from .errors import DeviceError, InvalidInputError
+from .formats import CtoEncoding, encode_cto
+from .patterns import SparseOverlay, TileSparseMatrix
+
+_DTYPE_CODES = {"fp32": _native.TW_F32, "fp16": _native.TW_F16, "bf16": _native.TW_BF16}
+
+
+def _torch():
+    return _native.require_cuda()
+
+
+def _torch_dtype(name: str):
+    torch = _torch()
+    return {"fp32": torch.float32, "fp16": torch.float16, "bf16": torch.bfloat16}[name]
+
+
+def _dtype_name(dt) -> str:
+    """Accept 'fp16' / torch.float16 / np.float16 style names."""
+    if isinstance(dt, str):
+        if dt in _DTYPE_CODES:
+            return dt
+        raise InvalidInputError(f"unknown dtype {dt!r}")
+    torch = _torch()
+    table = {torch.float32: "fp32", torch.float16: "fp16", torch.bfloat16: "bf16"}
+    if dt in table:
+        return table[dt]
+    raise InvalidInputError(f"unsupported dtype {dt!r}")
+
+
+# ----------------------------------------------------------------------------
+# device plan (GPU weight format)
+# ----------------------------------------------------------------------------
+
+class TwPlan:
+    """Device-resident TW weight (plus optional TEW overlay).
+
+    Built from a :class:`CtoEncoding` (the reference's compressed format,
+    formats.py:82-181); the C library validates it exactly like
+    ``gemm_cto`` does and derives the GPU layout: per-tile int32 gather lists
+    padded to a multiple of 64 and the K-major fp16/bf16 payload.
+    """
+
+    def __init__(self, enc: CtoEncoding, overlay: Optional[SparseOverlay] = None,
+                 compute_dtype: str = "fp16", schedule: str = "lpt"):
+        torch = _torch()
+        lib = _native.load_library()
+        if schedule not in _native.SCHEDULES:
+            raise InvalidInputError(f"unknown strategy {schedule!r}")
+        self.compute_dtype = _dtype_name(compute_dtype)
+        if self.compute_dtype == "fp32":
+            raise InvalidInputError("compute_dtype must be fp16 or bf16 (tensor-core inputs)")
+        self.schedule = schedule
+        self.device = torch.cuda.current_device()
+        self.original_dims = enc.original_dims
+        k, n = enc.original_dims
+        rc = np.ascontiguousarray(enc.row_counts, dtype=np.uint32)
+        cc = np.ascontiguousarray(enc.col_counts, dtype=np.uint32)
+        ro = np.ascontiguousarray(enc.row_offsets, dtype=np.uint32)
+        co = np.ascontiguousarray(enc.col_offsets, dtype=np.uint32)
+        pl = np.ascontiguousarray(enc.payload, dtype=np.float32)
+        handle = _native._vp()
+        _native.check(lib.tw_plan_create_cto(
+            ctypes_byref(handle), k, n, enc.config.granularity_g, rc.size,
+            _native.ptr(rc, _native.ctypes.c_uint32), _native.ptr(cc, _native.ctypes.c_uint32),
+            _native.ptr(ro, _native.ctypes.c_uint32), ro.shape[1],
+            _native.ptr(co, _native.ctypes.c_uint32), co.shape[1],
+            _native.ptr(pl, _native.ctypes.c_float), _DTYPE_CODES[self.compute_dtype],
+            _native.SCHEDULES[schedule], _native.stream_handle()))
+        self._handle = handle
+        self._finalizer = weakref.finalize(self, lib.tw_plan_destroy, handle)
+        self.per_tile_kept = [int(h) for h in rc]
+        self.per_tile_width = [int(w) for w in cc]
+        if overlay is not None:
+            self.attach_overlay(overlay)
+        self._refresh_info()
+
+    # -- metadata -------------------------------------------------------
+    def _refresh_info(self) -> None:
+        lib = _native.load_library()
+        info = _native.PlanInfo()
+        _native.check(lib.tw_plan_get_info(self._handle, _native.ctypes.byref(info)))
+        self.info = info
+        cond = np.empty(info.n_condensed, dtype=np.int32)
+        _native.check(lib.tw_plan_condensed_columns(self._handle,
+                                                    _native.ptr(cond, _native.ctypes.c_int32)))
+        uni = np.empty(info.n_union, dtype=np.int32)
+        _native.check(lib.tw_plan_union_columns(self._handle,
+                                                _native.ptr(uni, _native.ctypes.c_int32)))
+        self.condensed_columns = cond.astype(np.int64)
+        self.union_columns = uni.astype(np.int64)
+
+    @property
+    def has_overlay(self) -> bool:
+        return bool(self.info.has_overlay)
+
+    def attach_overlay(self, ov: SparseOverlay) -> None:
+        if tuple(ov.dims) != tuple(self.original_dims):
+            raise InvalidInputError(
+                f"overlay dims {tuple(ov.dims)} do not match weights {tuple(self.original_dims)}")
+        lib = _native.load_library()
+        ptr_ = np.ascontiguousarray(ov.col_ptr, dtype=np.int64)
+        rows = np.ascontiguousarray(ov.row_idx, dtype=np.int64)
+        vals = np.ascontiguousarray(ov.values, dtype=np.float32)
+        if rows.size == 0:
+            rows = np.zeros(1, dtype=np.int64)
+            vals = np.zeros(1, dtype=np.float32)
+        k, n = self.original_dims
+        _native.check(lib.tw_plan_attach_overlay(
+            self._handle, k, n, int(ov.nnz), _native.ptr(ptr_, _native.ctypes.c_int64),
+            _native.ptr(rows, _native.ctypes.c_int64), _native.ptr(vals, _native.ctypes.c_float),
+            _native.stream_handle()))
+        self._refresh_info()
+
+    def flops(self, m: int, tew: bool = False) -> int:
+        """Surviving FLOPs of one product (metrics.py:114-117)."""
+        macs = self.info.kept_macs_per_token if tew else self.info.kept_macs_per_token - self.info.nnz
+        return 2 * int(m) * int(macs)
+
+    # -- launches -------------------------------------------------------
+    def _check_at(self, at):
+        torch = _torch()
+        if not isinstance(at, torch.Tensor) or not at.is_cuda:
+            raise InvalidInputError("A^T must be a CUDA tensor (use prepare_activations)")
+        if at.dim() != 2 or at.shape[0] != self.original_dims[0]:
+            raise InvalidInputError(
+                f"A^T must be K x M with K={self.original_dims[0]}, got {tuple(at.shape)}")
+        if at.dtype != _torch_dtype(self.compute_dtype):
+            raise InvalidInputError(f"A^T dtype {at.dtype} != plan compute dtype "
+                                    f"{self.compute_dtype}")
+        if at.stride(1) != 1:
+            raise InvalidInputError("A^T must have unit stride along tokens")
+        return int(at.shape[1]), int(at.stride(0))
+
+    def _out(self, rows: int, m: int, out, out_dtype):
+        torch = _torch()
+        if out is None:
+            return torch.empty((rows, m), dtype=_torch_dtype(_dtype_name(out_dtype)),
+                               device=f"cuda:{self.device}")
+        if out.shape[0] < rows or out.shape[1] < m or out.stride(1) != 1:
+            raise InvalidInputError("out must be a (rows x M) CUDA tensor with unit token stride")
+        return out
+
+    def run(self, at, out=None, out_dtype="fp32", stream=None):
+        """C'^T (N' x M) = TW product of A^T (K x M); K1 only."""
+        m, ld_at = self._check_at(at)
+        ct = self._out(self.info.n_condensed, m, out, out_dtype)
+        lib = _native.load_library()
+        _native.check(lib.tw_gemm(self._handle, at.data_ptr(), m, ld_at, ct.data_ptr(),
+                                  ct.stride(0), _DTYPE_CODES[_dtype_name(ct.dtype)],
+                                  _native.stream_handle(stream)))
+        return ct
+
+    def run_tew(self, at, out=None, out_dtype="fp32", stream=None):
+        """C^T over the union columns (|union| x M) = TW + overlay; K1 + K2."""
+        if not self.has_overlay:
+            raise InvalidInputError("plan has no overlay attached")
+        m, ld_at = self._check_at(at)
+        ct = self._out(self.info.n_union, m, out, out_dtype)
+        lib = _native.load_library()
+        _native.check(lib.tw_gemm_tew(self._handle, at.data_ptr(), m, ld_at, ct.data_ptr(),
+                                      ct.stride(0), _DTYPE_CODES[_dtype_name(ct.dtype)],
+                                      _native.stream_handle(stream)))
+        return ct
+
+
+def ctypes_byref(x):
+    return _native.ctypes.byref(x)
+
+
+def prepare_activations(a, compute_dtype: str = "fp16", stream=None):
+    """Reference-layout activations (M x K) -> device A^T (K x M) in compute dtype.
+
+    ``a`` may be a numpy array / nested list (coerced with :func:`as_matrix`
+    like the reference, core.py:32-43) or a CUDA tensor.  The transpose and
+    cast run in the K4 kernel; the token pitch is padded to a multiple of 8
+    so the TMA descriptor is legal.  Returns a K x M view.
+    """
+    torch = _torch()
+    cd = _dtype_name(compute_dtype)
+    if isinstance(a, torch.Tensor):
+        if a.dim() != 2 or a.shape[0] < 1 or a.shape[1] < 1:
+            raise InvalidInputError(f"matrix must be 2-D with dims >= 1, got {tuple(a.shape)}")
+        src = a if a.is_cuda else a.cuda(non_blocking=True)
+        if src.dtype not in (torch.float32, torch.float16, torch.bfloat16):
+            src = src.float()
+        if src.stride(1) != 1:
+            src = src.contiguous()
+    else:
+        src = torch.from_numpy(as_matrix(a)).cuda()
+    m, k = src.shape
+    ld = (m + 7) // 8 * 8
+    at = torch.empty((k, ld), dtype=_torch_dtype(cd), device=src.device)
+    lib = _native.load_library()
+    _native.check(lib.tw_transpose_cast(src.data_ptr(), _DTYPE_CODES[_dtype_name(src.dtype)], m,
+                                        k, src.stride(0), at.data_ptr(), _DTYPE_CODES[cd], ld,
+                                        _native.stream_handle(stream)))
+    return at[:, :m]
+
+
+# ----------------------------------------------------------------------------
+# plan cache keyed by the (immutable) reference objects
+# ----------------------------------------------------------------------------
+
+_PLAN_CACHE: dict = {}
+
+
+def plan_for(b: Union[TileSparseMatrix, CtoEncoding], overlay: Optional[SparseOverlay] = None,
+             compute_dtype: str = "fp16", schedule: str = "lpt") -> TwPlan:
+    """Cached :class:`TwPlan` for a tile matrix / encoding (+ overlay).
+
+    The reference structures are frozen, so a plan is keyed by the identity
+    of the objects it was built from and dropped when any of them dies.
+    """
+    torch = _torch()
+    watched = [b] if overlay is None else [b, overlay]
+    key = tuple(id(o) for o in watched) + (torch.cuda.current_device(), compute_dtype, schedule)
+    plan = _PLAN_CACHE.get(key)
+    if plan is None:
+        enc = b if isinstance(b, CtoEncoding) else encode_cto(b)
+        plan = TwPlan(enc, overlay, compute_dtype, schedule)
+        _PLAN_CACHE[key] = plan
+        for o in watched:
+            weakref.finalize(o, _PLAN_CACHE.pop, key, None)
+    return plan
+
+
+# ----------------------------------------------------------------------------
+# reference API
+# ----------------------------------------------------------------------------
+
+@dataclass
+class GemmOutput:
+    """Condensed product plus its column map (reference executor.py:68-80).
+
+    ``condensed`` is an M x N_out CUDA tensor (a transposed view of the
+    kernel's C'^T buffer, available as :attr:`condensed_t`).
+    """
+
+    condensed: object
+    column_map: IndexMask
+
+    @property
+    def condensed_t(self):
+        return self.condensed.t()
+
+    def expand(self):
+        """M x N CUDA tensor with zero columns at pruned positions."""
+        torch = _torch()
+        m = self.condensed.shape[0]
+        out = torch.zeros((m, self.column_map.domain_len), dtype=self.condensed.dtype,
+                          device=self.condensed.device)
+        idx = torch.tensor(np.asarray(self.column_map.kept, dtype=np.int64), device=out.device)
+        out.index_copy_(1, idx, self.condensed)
+        return out
+
+    def to_numpy(self) -> np.ndarray:
+        """Condensed result on the host as float64 (the reference's carrier)."""
+        return self.condensed.double().cpu().numpy()
+
+
+@dataclass
+class ExecutionTrace:
+    """Per-tile work, assignment and balance (reference executor.py:83-118)."""
+
+    strategy: str
+    workers: int
+    per_tile_macs: List[int]
+    assignment: List[int]
+    per_worker_macs: List[int]
+
+    @property
+    def total_macs(self) -> int:
+        return int(sum(self.per_tile_macs))
+
+    @property
+    def total_flops(self) -> int:
+        return 2 * self.total_macs
+
+    @property
+    def imbalance(self) -> float:
+        t = np.asarray(self.per_worker_macs, dtype=np.float64)
+        mean = t.mean()
+        return float(t.max() / mean) if mean > 0 else 1.0
+
+    def to_json_dict(self) -> dict:
+        return {"strategy": self.strategy, "workers": self.workers,
+                "per_tile_flops": [2 * v for v in self.per_tile_macs],
+                "per_tile_macs": [int(v) for v in self.per_tile_macs],
+                "assignment": [int(v) for v in self.assignment],
+                "per_worker_flops": [2 * v for v in self.per_worker_macs],
+                "imbalance": self.imbalance, "total_macs": self.total_macs,
+                "total_flops": self.total_flops}
+
+
+def schedule_tiles(per_tile_macs: List[int], workers: int, strategy: str = "lpt") -> List[int]:
+    """Deterministic tile -> worker assignment (reference executor.py:206-227).
+
+    ``lpt``: descending work onto the least-loaded worker (ties to the lower
+    worker); ``round_robin``: tile i onto worker i % workers.
+    """
+    if workers < 1:
+        raise InvalidInputError(f"workers must be >= 1, got {workers}")
+    if strategy == "round_robin":
+        return [i % workers for i in range(len(per_tile_macs))]
+    if strategy != "lpt":
+        raise InvalidInputError(f"unknown strategy {strategy!r}")
+    loads = [0] * workers
+    out = [0] * len(per_tile_macs)
+    for i in sorted(range(len(per_tile_macs)), key=lambda t: (-per_tile_macs[t], t)):
+        w = min(range(workers), key=lambda x: (loads[x], x))
+        out[i] = w
+        loads[w] += per_tile_macs[i]
+    return out
+
+
+def _activations(a, k: int, compute_dtype: str):
+    torch = _torch()
+    m_k = tuple(a.shape) if isinstance(a, torch.Tensor) else as_matrix(a).shape
+    if len(m_k) != 2 or m_k[1] != k:
+        raise InvalidInputError(f"inner dims disagree: a has {m_k[-1]} cols, weights have K={k}")
+    return prepare_activations(a, compute_dtype)
+
+
+def gemm_tile_sparse(a, b: TileSparseMatrix, *, compute_dtype: str = "fp16",
+                     out_dtype: str = "fp32") -> GemmOutput:
+    """Per-tile gather + GEMM over every tile; output condensed to N'."""
+    at = _activations(a, b.original_dims[0], compute_dtype)
+    plan = plan_for(b, compute_dtype=compute_dtype)
+    ct = plan.run(at, out_dtype=out_dtype)
+    return GemmOutput(condensed=ct.t(), column_map=b.column_mask)
+
+
+def gemm_cto(a, c: CtoEncoding, check_padding: bool = False, *, compute_dtype: str = "fp16",
+             out_dtype: str = "fp32") -> GemmOutput:
+    """Single fused pass over the offset encoding.
+
+    The library decodes and validates the offsets (CorruptEncodingError on
+    malformed ones) and builds gather lists of exactly ``row_counts[i]``
+    entries, so padded offsets are never dereferenced; ``check_padding`` is
+    accepted for signature compatibility.
+    """
+    at = _activations(a, c.original_dims[0], compute_dtype)
+    plan = plan_for(c, compute_dtype=compute_dtype)
+    ct = plan.run(at, out_dtype=out_dtype)
+    return GemmOutput(condensed=ct.t(), column_map=IndexMask(c.original_dims[1],
+                                                             plan.condensed_columns))
+
+
+def execute_batched(a, b: TileSparseMatrix, workers: int, strategy: str = "lpt", *,
+                    compute_dtype: str = "fp16",
+                    out_dtype: str = "fp32") -> Tuple[GemmOutput, ExecutionTrace]:
+    """All tiles in one persistent launch; ``strategy`` sets the sub-tile
+    order inside each 128-token block (lpt = descending K').  The trace
+    reports the reference's host-side LPT / round-robin assignment over
+    ``workers`` lanes so accounting matches executor.py:241-265."""
+    macs_per_token = [t.width * t.kept_rows.n_kept for t in b.tiles]
+    assignment = schedule_tiles(macs_per_token, workers, strategy)
+    at = _activations(a, b.original_dims[0], compute_dtype)
+    m = int(at.shape[1])
+    plan = plan_for(b, compute_dtype=compute_dtype, schedule=strategy)
+    ct = plan.run(at, out_dtype=out_dtype)
+    per_tile = [m * v for v in macs_per_token]
+    per_worker = [0] * workers
+    for i, w in enumerate(assignment):
+        per_worker[w] += per_tile[i]
+    trace = ExecutionTrace(strategy=strategy, workers=workers, per_tile_macs=per_tile,
+                           assignment=assignment, per_worker_macs=per_worker)
+    return GemmOutput(condensed=ct.t(), column_map=b.column_mask), trace
+
+
+def gemm_tew(a, b: TileSparseMatrix, ov: SparseOverlay,
+             tile_output: Optional[GemmOutput] = None, *, compute_dtype: str = "fp16",
+             out_dtype: str = "fp32") -> GemmOutput:
+    """TW product + CSC overlay SpMM, condensed to the union of surviving
+    columns (reference executor.py:180-203).  The TW part is recomputed in
+    the same stream (K1 writes straight into union rows, K2 adds the
+    residual), so ``tile_output`` is accepted but not needed."""
+    if tuple(ov.dims) != tuple(b.original_dims):
+        raise InvalidInputError(f"overlay dims {tuple(ov.dims)} do not match weights "
+                                f"{tuple(b.original_dims)}")
+    at = _activations(a, b.original_dims[0], compute_dtype)
+    plan = plan_for(b, overlay=ov, compute_dtype=compute_dtype)
+    ct = plan.run_tew(at, out_dtype=out_dtype)
+    return GemmOutput(condensed=ct.t(), column_map=IndexMask(b.original_dims[1],
+                                                             plan.union_columns))
+
+
+def gemm_dense(a, b):
+    """Dense float64 product on the device (verification helper mirroring
+    executor.py:40-65; cuBLAS DGEMM, not the reference's fixed k order)."""
+    torch = _torch()
+    a_t = torch.as_tensor(as_matrix(a) if not isinstance(a, torch.Tensor) else a).cuda().double()
+    b_t = torch.as_tensor(as_matrix(b) if not isinstance(b, torch.Tensor) else b).cuda().double()
+    if a_t.shape[1] != b_t.shape[0]:
+        raise InvalidInputError(f"inner dims disagree: a is {tuple(a_t.shape)}, "
+                                f"b is {tuple(b_t.shape)}")
+    return a_t @ b_t
+
+
+def masked_dense_reference(a, w, keep_mask: np.ndarray):
+    """Zero pruned positions and run the dense float64 product on the device
+    (verification helper mirroring executor.py:268-275)."""
+    w = as_matrix(w)
+    mask = np.asarray(keep_mask, dtype=bool)
+    if mask.shape != w.shape:
+        raise InvalidInputError(f"mask shape {mask.shape} != weights shape {w.shape}")
+    return gemm_dense(a, np.where(mask, w, np.float32(0.0)))
+
+
+def _as_f64(x) -> np.ndarray:
+    try:
+        import torch
+        if isinstance(x, torch.Tensor):
+            return x.detach().double().cpu().numpy()
+    except ImportError:  # pragma: no cover
+        pass
+    return np.asarray(x, dtype=ACC_DTYPE)
+
+
+def relative_error(result, reference) -> float:
+    """max|result - reference| / max|reference| (reference executor.py:278-288)."""
+    r = _as_f64(result)
+    ref = _as_f64(reference)
+    if r.shape != ref.shape:
+        raise InvalidInputError(f"shape mismatch: {r.shape} vs {ref.shape}")
+    scale = float(np.max(np.abs(ref))) if ref.size else 0.0
+    diff = float(np.max(np.abs(r - ref))) if r.size else 0.0
+    if scale == 0.0:
+        return 0.0 if diff == 0.0 else float("inf")
+    return diff / scale
+
+
+__all__ = ["TwPlan", "prepare_activations", "plan_for", "GemmOutput", "ExecutionTrace",
+           "schedule_tiles", "gemm_tile_sparse", "gemm_cto", "execute_batched", "gemm_tew",
+           "gemm_dense", "masked_dense_reference", "relative_error", "DeviceError"]

@@ -1,0 +1,190 @@
+"""GPU parity: the sm_100a kernels (through the C ABI) vs the CPU oracle.
+
+Protocol: inputs are rounded once to the compute
+dtype; the oracle (fp64, reference accumulation order) and the GPU (fp32
+TMEM accumulation) see identical values, so the only differences are fp32
+accumulation order and output rounding.  Tolerances on
+``relative_error`` (executor.py:278-288, max|diff| / max|ref|):
+
+    fp32 out: 1e-5     fp16 out: 1e-3     bf16 out: 8e-3
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from helpers import load_npz, tiles_from_record
+
+import paper_2402_10876_b200 as tw
+from oracle import tilesparse_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"fp32": 1e-5, "fp16": 1e-3, "bf16": 8e-3}
+
+
+def _rounded(x, dt="fp16"):
+    return tw.round_to(x, dt)
+
+
+def _problem(k, n, m, s, g, seed, dt="fp16"):
+    rng = np.random.default_rng(seed)
+    w = _rounded(rng.normal(size=(k, n)).astype(np.float32), dt)
+    a = _rounded(rng.normal(size=(m, k)).astype(np.float32), dt)
+    plan, tsm = tw.prune_tw(w, s, g)
+    return w, a, plan, tsm
+
+
+def _oracle_tw(a, tsm):
+    return orc.c_gemm_cto_enc(a, tw.encode_cto(tsm))
+
+
+@pytest.mark.parametrize("k,n,m,s,g", [
+    (64, 64, 128, 0.5, 32),       # one 128-token block, single k-step
+    (128, 256, 256, 0.75, 128),   # two tiles, two blocks
+    (200, 150, 77, 0.6, 64),      # ragged M, ragged last tile
+    (768, 768, 1000, 0.75, 128),  # BERT-shaped, M tail
+    (96, 80, 5, 0.3, 16),         # M < 8 (padded pitch)
+    (33, 17, 1, 0.5, 4),          # M = 1, tiny tiles
+    (300, 700, 130, 0.5, 300),    # g > 256: tiles split into UMMA-N slices
+    (50, 64, 64, 0.0, 8),         # nothing pruned
+    (40, 400, 64, 0.9, 1),        # g = 1: 40 width-1 tiles
+])
+def test_tw_matches_oracle(k, n, m, s, g):
+    w, a, plan, tsm = _problem(k, n, m, s, g, seed=k * 31 + n)
+    out = tw.gemm_tile_sparse(a, tsm)
+    ref = _oracle_tw(a, tsm)
+    assert out.condensed.shape == ref.shape
+    assert tw.relative_error(out.condensed, ref) <= TOL["fp32"]
+    # expanded result vs masked dense: zeros at pruned columns
+    full = out.expand().cpu().numpy()
+    pruned = np.setdiff1d(np.arange(n), tsm.column_mask.kept)
+    assert np.all(full[:, pruned] == 0)
+
+
+def test_three_tw_paths_bit_identical():
+    w, a, plan, tsm = _problem(256, 384, 300, 0.75, 128, seed=7)
+    enc = tw.encode_cto(tsm)
+    o1 = tw.gemm_tile_sparse(a, tsm).condensed
+    o2 = tw.gemm_cto(a, enc, check_padding=True).condensed
+    o3, trace = tw.execute_batched(a, tsm, workers=3)
+    o4, _ = tw.execute_batched(a, tsm, workers=2, strategy="round_robin")
+    for o in (o2, o3.condensed, o4.condensed):
+        assert o.cpu().numpy().tobytes() == o1.cpu().numpy().tobytes()
+    assert trace.total_macs == sum(300 * t.width * t.kept_rows.n_kept for t in tsm.tiles)
+
+
+@pytest.mark.parametrize("out_dtype", ["fp32", "fp16", "bf16"])
+@pytest.mark.parametrize("compute", ["fp16", "bf16"])
+def test_dtypes(compute, out_dtype):
+    w, a, plan, tsm = _problem(256, 256, 256, 0.75, 64, seed=3, dt=compute)
+    out = tw.gemm_tile_sparse(a, tsm, compute_dtype=compute, out_dtype=out_dtype)
+    ref = _oracle_tw(a, tsm)
+    assert tw.relative_error(out.condensed, ref) <= TOL[out_dtype]
+
+
+def test_bert_golden_rows():
+    """First 8 tokens of every BERT layer vs the reference's own fp64 output."""
+    z, meta = load_npz("bert.npz")
+    for li, info in enumerate(meta):
+        k, n = info["k"], info["n"]
+        w = tw.round_to(tw.synthetic_matrix(0, k, n, tw.STREAM_WEIGHTS), "fp16")
+        a = tw.round_to(tw.synthetic_matrix(0, 8192, k, tw.STREAM_INPUT), "fp16")
+        plan, tsm = tw.prune_tw(w, 0.75, 128)
+        rows = tiles_from_record(z, f"l{li}_tw_")
+        assert all(np.array_equal(t.kept_rows.kept, r) for t, r in zip(tsm.tiles, rows))
+        out = tw.gemm_cto(a, tw.encode_cto(tsm))
+        got = out.condensed[:8].cpu().numpy()
+        assert tw.relative_error(got, z[f"l{li}_tw_out8"]) <= TOL["fp32"]
+        # full M = 8192 against the oracle (pinned to the reference by sha256)
+        full = orc.c_gemm_cto_enc(a, tw.encode_cto(tsm))
+        assert tw.relative_error(out.condensed, full) <= TOL["fp32"]
+
+
+def test_tew_matches_oracle():
+    rng = np.random.default_rng(11)
+    k, n, m = 256, 320, 200
+    w = _rounded(rng.normal(size=(k, n)).astype(np.float32))
+    a = _rounded(rng.normal(size=(m, k)).astype(np.float32))
+    plan, tsm, ov = tw.prune_tew(w, 0.6, 0.05, 64)
+    out = tw.gemm_tew(a, tsm, ov)
+    ref, union = orc.tew_reference(a, tw.encode_cto(tsm), ov.col_ptr, ov.row_idx, ov.values, n)
+    assert np.array_equal(out.column_map.kept, union)
+    assert tw.relative_error(out.condensed, ref) <= TOL["fp32"]
+    # and against the masked dense fp64 product on the union mask
+    dense = tw.masked_dense_reference(a, w, plan.element_mask)
+    assert tw.relative_error(out.expand(), dense) <= TOL["fp32"]
+
+
+def test_tew_bert_golden_rows():
+    z, meta = load_npz("bert.npz")
+    for li, info in enumerate(meta):
+        k, n = info["k"], info["n"]
+        w = tw.round_to(tw.synthetic_matrix(0, k, n, tw.STREAM_WEIGHTS), "fp16")
+        a = tw.round_to(tw.synthetic_matrix(0, 8192, k, tw.STREAM_INPUT), "fp16")
+        plan, tsm, ov = tw.prune_tew(w, 0.75, 0.015, 128)
+        assert ov.nnz == info["tew_nnz"]
+        out = tw.gemm_tew(a, tsm, ov)
+        assert np.array_equal(out.column_map.kept, z[f"l{li}_tew_union"])
+        got = out.condensed[:8].cpu().numpy()
+        assert tw.relative_error(got, z[f"l{li}_tew_out8"]) <= TOL["fp32"]
+
+
+def test_empty_overlay_equals_tw():
+    w, a, plan, tsm = _problem(64, 96, 40, 0.5, 32, seed=5)
+    empty = tw.SparseOverlay.empty((64, 96))
+    base = tw.gemm_tile_sparse(a, tsm).expand().cpu().numpy()
+    out = tw.gemm_tew(a, tsm, empty).expand().cpu().numpy()
+    assert np.array_equal(base, out)
+
+
+def test_error_mapping():
+    w, a, plan, tsm = _problem(48, 32, 16, 0.6, 8, seed=9)
+    enc = tw.encode_cto(tsm)
+    bad = enc.row_offsets.copy()
+    bad[0, 0] = 5000
+    corrupt = tw.CtoEncoding(original_dims=enc.original_dims, config=enc.config,
+                             row_counts=enc.row_counts, col_counts=enc.col_counts,
+                             row_offsets=bad, col_offsets=enc.col_offsets, payload=enc.payload)
+    with pytest.raises(tw.CorruptEncodingError):
+        tw.gemm_cto(a, corrupt)
+    with pytest.raises(tw.InvalidInputError):
+        tw.gemm_tile_sparse(np.ones((4, 47), np.float32), tsm)
+    r, c = np.argwhere(tsm.keep_mask())[0]
+    clash = tw.SparseOverlay.from_coords((48, 32), [r], [c], [1.0])
+    with pytest.raises(tw.ContractViolationError):
+        tw.gemm_tew(a, tsm, clash)
+    with pytest.raises(tw.InvalidInputError):
+        tw.gemm_tew(a, tsm, tw.SparseOverlay.empty((49, 32)))
+
+
+def test_padding_never_dereferenced():
+    """Corrupting only the padded region of the offsets leaves the result
+    bit-identical (test_executor.py:156-180)."""
+    w, a, plan, tsm = _problem(96, 64, 64, 0.6, 16, seed=13)
+    enc = tw.encode_cto(tsm)
+    clean = tw.gemm_cto(a, enc).condensed.cpu().numpy()
+    rows = enc.row_offsets.copy()
+    for i in range(enc.tile_count):
+        rows[i, int(enc.row_counts[i]):] = 9999
+    dirty = tw.CtoEncoding(original_dims=enc.original_dims, config=enc.config,
+                           row_counts=enc.row_counts, col_counts=enc.col_counts,
+                           row_offsets=rows, col_offsets=enc.col_offsets, payload=enc.payload)
+    assert tw.gemm_cto(a, dirty).condensed.cpu().numpy().tobytes() == clean.tobytes()
+
+
+def test_nonfinite_activation_not_in_padding():
+    """A NaN in an activation row that no tile keeps must not leak into the
+    output (gather padding is TMA out-of-bounds zero fill, not a real row)."""
+    w, a, plan, tsm = _problem(64, 64, 128, 0.75, 32, seed=21)
+    kept_any = np.zeros(64, bool)
+    for t in tsm.tiles:
+        kept_any[t.kept_rows.kept] = True
+    dead = np.flatnonzero(~kept_any)
+    if dead.size == 0:
+        pytest.skip("every row kept by some tile")
+    a2 = a.copy()
+    a2[:, dead] = np.nan
+    out = tw.gemm_tile_sparse(a2, tsm).condensed.cpu().numpy()
+    assert np.all(np.isfinite(out))
