@@ -1,0 +1,502 @@
+"""Benchmark of the B200 TW sparse matmul (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config bert|bert_tew|cfg1]
+                    [--impl ours|reference]
+
+One *step* = one pass of the hot path over one batch: the TW product of the
+three BERT-base linear layers (768x768, 768x3072, 3072x768) at 75% TW
+sparsity, G=128, M = 128 x 64 = 8192 tokens, fp16 operands, fp32
+accumulation, fp16 output (configs[1]).  ``--config bert_tew`` is configs[2]
+(TW 0.75 + 1.5% element overlay); ``--config cfg1`` is configs[0].
+
+value        effective TFLOP/s = surviving FLOPs (metrics.report.sparse_flops,
+             metrics.py:114-117) of all ranks / max-over-ranks device time,
+             inputs resident in HBM; 4 rotating buffer sets (> 2 x L2) so
+             every step streams cold activations, weights and outputs.  Each
+             step is one CUDA-graph replay of the three layer launches (the
+             dense cuBLAS arm is graph-captured the same way).
+e2e          same metric through the public API (prepare_activations +
+             TwPlan.run) from pinned HOST fp16 activations, with the H2D
+             copies, the A->A^T transpose kernel, the GEMM and the D2H copy
+             of the fp16 result inside the timed region.
+cublas       dense torch.matmul (cuBLAS) at the same shapes and layout.
+roofline     K1 (tw_gather_gemm) launches timed per layer with CUDA events;
+             achieved = algorithmic bytes / launch time vs the
+             measured HBM peak (the step is HBM-bound: AI 188 < ridge 240).
+cpu_baseline the reference algorithm (oracle port of execute_batched,
+             executor.py:230-265) on host cores, bounded M-slice sample.
+
+N > 1 (torchrun): weak scaling, every rank runs its own 8192-token batch
+(M-split data parallelism, no collective on the data path).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "TW-GEMM speedup vs dense cuBLAS at 75% sparsity; effective TFLOP/s"
+BERT_LAYERS = [(768, 768), (768, 3072), (3072, 768)]
+CONFIGS = {
+    "bert": {"layers": BERT_LAYERS, "m": 8192, "s": 0.75, "g": 128, "delta": 0.0,
+             "workload": "BERT-base linear layers 768x768, 768x3072, 3072x768; TW 75% G=128; "
+                         "M=128x64 tokens; fp16 (configs[1])"},
+    "bert_tew": {"layers": BERT_LAYERS, "m": 8192, "s": 0.75, "g": 128, "delta": 0.015,
+                 "workload": "BERT-base TEW: TW 75% + 1.5% element overlay, G=128, "
+                             "M=8192 (configs[2])"},
+    "cfg1": {"layers": [(1024, 1024)], "m": 128, "s": 0.75, "g": 128, "delta": 0.0,
+             "workload": "single 1024x1024 weight, TW 75% G=128, M=128 (configs[0])"},
+}
+N_ROTATE = 4
+
+
+def peaks() -> dict:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return {"hbm": float(d["hbm_gbs"]), "tc": float(d["bf16_tflops"]),
+                "tc_sustained": float(d.get("bf16_tflops_sustained", d["bf16_tflops"])),
+                "source": "measured (MEASURED_PEAKS.json)"}
+    return {"hbm": 6650.0, "tc": 1590.0, "tc_sustained": 1400.0,
+            "source": "fallback (B200_PROFILING.md)"}
+
+
+# ----------------------------------------------------------------------------
+# clocks sampler
+# ----------------------------------------------------------------------------
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[4:8]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------
+# problem construction (host prune/compress, identical on every rank)
+# ----------------------------------------------------------------------------
+
+def build_layers(cfg: dict):
+    import paper_2402_10876_b200 as tw
+
+    layers = []
+    for li, (k, n) in enumerate(cfg["layers"]):
+        w = tw.round_to(tw.synthetic_matrix(0, k, n, tw.STREAM_WEIGHTS), "fp16")
+        if cfg["delta"] > 0:
+            plan, tsm, ov = tw.prune_tew(w, cfg["s"], cfg["delta"], cfg["g"])
+        else:
+            plan, tsm = tw.prune_tw(w, cfg["s"], cfg["g"])
+            ov = None
+        enc = tw.encode_cto(tsm)
+        n_out = tsm.n_condensed
+        if ov is not None:
+            ov_cols = np.flatnonzero(np.diff(ov.col_ptr))
+            n_out = int(np.union1d(tsm.column_mask.kept, ov_cols).size)
+        layers.append({"k": k, "n": n, "w": w, "plan": plan, "tsm": tsm, "enc": enc, "ov": ov,
+                       "flops": tw.sparse_flops(tsm, cfg["m"], ov),
+                       "bytes": tw.algorithmic_bytes(tsm, cfg["m"], overlay=ov, n_out=n_out)})
+    return layers
+
+
+def activations(cfg: dict, k: int, li: int, rank: int):
+    import paper_2402_10876_b200 as tw
+
+    # stream 1 = input stream of the reference CLI; each rank its own batch
+    return tw.round_to(tw.synthetic_matrix(rank, cfg["m"], k, tw.STREAM_INPUT), "fp16")
+
+
+# ----------------------------------------------------------------------------
+# reference arm / CPU baseline: the reference algorithm on host cores
+# ----------------------------------------------------------------------------
+
+def cpu_reference_rate(cfg: dict, layers, m_sample: int, reps: int = 1):
+    """Time the oracle port of execute_batched (+ gemm_tew overlay) on an
+    M-slice; returns (TFLOP/s, seconds, flops, workers)."""
+    from oracle import tilesparse_oracle as orc
+
+    workers = os.cpu_count() or 1
+    total_s, total_f = 0.0, 0
+    for _ in range(reps):
+        for li, L in enumerate(layers):
+            a = activations(cfg, L["k"], li, 0)[:m_sample]
+            tiles = [(t.kept_rows.kept, t.payload) for t in L["tsm"].tiles]
+            t0 = time.perf_counter()
+            out = orc.execute_batched(a, tiles, workers, "lpt")
+            if L["ov"] is not None and L["ov"].nnz:
+                full = np.zeros((a.shape[0], L["n"]))
+                full[:, L["tsm"].column_mask.kept] = out
+                orc.gemm_tew_add(a, full, L["ov"].col_ptr, L["ov"].row_idx, L["ov"].values)
+            total_s += time.perf_counter() - t0
+            nnz = L["ov"].nnz if L["ov"] is not None else 0
+            total_f += 2 * m_sample * (sum(t.width * t.kept_rows.n_kept for t in L["tsm"].tiles)
+                                       + nnz)
+    return total_f / total_s / 1e12, total_s, total_f, workers
+
+
+def run_reference_arm(args, cfg, rank: int, world: int) -> None:
+    if rank != 0:
+        return
+    layers = build_layers(cfg)
+    m_sample = min(cfg["m"], 512)
+    for _ in range(args.warmup):
+        cpu_reference_rate(cfg, layers, m_sample)
+    rate, secs, flops, workers = cpu_reference_rate(cfg, layers, m_sample, reps=args.steps)
+    sample = (f"{m_sample} of {cfg['m']} tokens per step through every layer "
+              f"(oracle port of execute_batched, lpt, {workers} workers)")
+    line = {
+        "metric": METRIC, "value": rate, "unit": "TFLOP/s", "impl": "reference",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": secs / args.steps * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (Philox seed 0, fp16-rounded)",
+        "config": {"workload": cfg["workload"], "parallelism": "cpu", "m_sample": m_sample},
+        "cpu_baseline": {"value": rate, "unit": "TFLOP/s", "cores": workers, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": rate, "unit": "TFLOP/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+# ----------------------------------------------------------------------------
+# our arm
+# ----------------------------------------------------------------------------
+
+def capture_graph(fn):
+    """CUDA graph of fn() (eager warm-up first, captured on a side stream)."""
+    import torch
+
+    g = torch.cuda.CUDAGraph()
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        fn()
+        with torch.cuda.graph(g, stream=side):
+            fn()
+    torch.cuda.current_stream().wait_stream(side)
+    torch.cuda.synchronize()
+    return g
+
+
+def run_ours(args, cfg, rank: int, world: int) -> None:
+    import torch
+    import torch.distributed as dist
+
+    import paper_2402_10876_b200 as tw
+
+    dev = torch.device("cuda", torch.cuda.current_device())
+    layers = build_layers(cfg)
+    m = cfg["m"]
+    tew = cfg["delta"] > 0
+
+    # R rotating sets of (plan, A^T, C^T) per layer: total footprint > 2 x L2
+    sets = []
+    for r in range(N_ROTATE):
+        layer_set = []
+        for li, L in enumerate(layers):
+            plan = tw.TwPlan(L["enc"], L["ov"], compute_dtype="fp16")
+            a = activations(cfg, L["k"], li, rank)
+            at = tw.prepare_activations(torch.from_numpy(a).to(dev))
+            rows = plan.info.n_union if tew else plan.info.n_condensed
+            ct = torch.empty((rows, m), dtype=torch.float16, device=dev)
+            layer_set.append((plan, at, ct))
+        sets.append(layer_set)
+    torch.cuda.synchronize()
+
+    def run_set(r: int):
+        for plan, at, ct in sets[r]:
+            if tew:
+                plan.run_tew(at, out=ct)
+            else:
+                plan.run(at, out=ct)
+
+    # one CUDA graph per rotating set: a step is one graph replay (3 launches)
+    graphs = [capture_graph(lambda r=r: run_set(r)) for r in range(N_ROTATE)]
+
+    def step(i: int):
+        graphs[i % N_ROTATE].replay()
+
+    flops_step = sum(L["flops"] for L in layers)
+    stream = torch.cuda.current_stream()
+
+    # ---- timed region: K steps, barrier + sync on both sides, max over ranks
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        # soak so the clock sampler sees the GPU under this load (>= ~1 s)
+        t_soak = time.time()
+        i = 0
+        while time.time() - t_soak < 1.0:
+            step(i)
+            i += 1
+            if i % 64 == 0:
+                torch.cuda.synchronize()
+        for i in range(args.warmup):
+            step(i)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        for i in range(args.steps):
+            step(i)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = ev0.elapsed_time(ev1)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    ms_step = ms_max / args.steps
+    value = world * flops_step / (ms_step * 1e-3) / 1e12
+
+    # ---- per-launch K1 timing (roofline): graph of REPS launches per layer
+    per_layer = []
+    reps = 32
+    for li, L in enumerate(layers):
+        def layer_launches(li=li):
+            for i in range(reps):
+                plan, at, ct = sets[i % N_ROTATE][li]
+                if tew:
+                    plan.run_tew(at, out=ct)
+                else:
+                    plan.run(at, out=ct)
+        g = capture_graph(layer_launches)
+        times = []
+        for _ in range(5):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            g.replay()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1) * 1e3 / reps)
+        us = statistics.median(times)
+        per_layer.append({"shape": f"{L['k']}x{L['n']}", "us": us, "flops": L["flops"],
+                          "bytes": L["bytes"],
+                          "tflops": L["flops"] / (us * 1e-6) / 1e12,
+                          "gbs": L["bytes"] / (us * 1e-6) / 1e9})
+        del g
+
+    # ---- dense cuBLAS at the same shapes / layout (C^T = W^T . A^T)
+    dense = []
+    for r in range(N_ROTATE):
+        row = []
+        for li, L in enumerate(layers):
+            wt = torch.from_numpy(np.ascontiguousarray(L["w"].T)).to(dev, torch.float16)
+            row.append((wt, sets[r][li][1],
+                        torch.empty((L["n"], m), dtype=torch.float16, device=dev)))
+        dense.append(row)
+
+    def dense_set(r: int):
+        for wt, at, out in dense[r]:
+            torch.matmul(wt, at, out=out)
+
+    dense_graphs = [capture_graph(lambda r=r: dense_set(r)) for r in range(N_ROTATE)]
+
+    def dense_step(i: int):
+        dense_graphs[i % N_ROTATE].replay()
+
+    for i in range(args.warmup):
+        dense_step(i)
+    torch.cuda.synchronize()
+    d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    d0.record(stream)
+    for i in range(args.steps):
+        dense_step(i)
+    d1.record(stream)
+    torch.cuda.synchronize()
+    dense_ms = d0.elapsed_time(d1) / args.steps
+    td = torch.tensor([dense_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(td, op=dist.ReduceOp.MAX)
+    dense_ms = float(td.item())
+    dense_flops = sum(2 * m * L["k"] * L["n"] for L in layers)
+    del dense, dense_graphs
+
+    # ---- e2e through the public API from pinned host memory
+    host_a = [torch.from_numpy(activations(cfg, L["k"], li, rank)).to(torch.float16)
+              .pin_memory() for li, L in enumerate(layers)]
+    host_c = [torch.empty((s[2].shape[1], s[2].shape[0]), dtype=torch.float16).pin_memory()
+              for s in sets[0]]
+    dev_a = [torch.empty(h.shape, dtype=torch.float16, device=dev) for h in host_a]
+    h2d = sum(h.numel() * h.element_size() for h in host_a)
+    d2h = sum(h.numel() * h.element_size() for h in host_c)
+
+    def e2e_step(i: int):
+        for li, (plan, _, ct) in enumerate(sets[i % N_ROTATE]):
+            dev_a[li].copy_(host_a[li], non_blocking=True)
+            at = tw.prepare_activations(dev_a[li])
+            if tew:
+                plan.run_tew(at, out=ct)
+            else:
+                plan.run(at, out=ct)
+            host_c[li].copy_(ct.t(), non_blocking=True)
+
+    for i in range(args.warmup):
+        e2e_step(i)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for i in range(args.steps):
+        e2e_step(i)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    te = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_ms = float(te.item()) / args.steps
+    e2e_value = world * flops_step / (e2e_ms * 1e-3) / 1e12
+
+    if rank != 0:
+        return
+
+    pk = peaks()
+    tot_bytes = sum(p["bytes"] for p in per_layer)
+    tot_us = sum(p["us"] for p in per_layer)
+    achieved_gbs = tot_bytes / (tot_us * 1e-6) / 1e9
+    ai = flops_step / tot_bytes
+    ridge = pk["tc"] * 1e12 / (pk["hbm"] * 1e9)
+    traffic = None
+    tfile = ROOT / "profiles" / "ncu_traffic.json"
+    if tfile.exists():
+        try:
+            traffic = json.loads(tfile.read_text()).get(args.config)
+        except (ValueError, OSError):
+            traffic = None
+    if ai < ridge:
+        roofline = {"bound": "hbm", "achieved": achieved_gbs, "peak": pk["hbm"], "unit": "GB/s",
+                    "frac": achieved_gbs / pk["hbm"], "traffic": traffic}
+    else:
+        tf = flops_step / (tot_us * 1e-6) / 1e12
+        roofline = {"bound": "tensor", "achieved": tf, "peak": pk["tc"], "unit": "TFLOP/s",
+                    "frac": tf / pk["tc"], "traffic": traffic}
+    roofline.update({"kernel": "tw_gather_gemm" + ("+tw_residual" if tew else ""),
+                     "peak_source": pk["source"], "arithmetic_intensity": ai,
+                     "layers": per_layer})
+
+    # CPU baseline: the reference algorithm on this host, bounded sample
+    m_sample = min(m, 1024)
+    cpu_rate, cpu_s, _, workers = cpu_reference_rate(cfg, layers, m_sample)
+    clocks = clk.summary()
+    line = {
+        "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp16",
+        "data": "synthetic (Philox seed=rank, fp16-rounded; weights seed 0)",
+        "config": {"workload": cfg["workload"], "m_tokens_per_gpu": m,
+                   "sparsity": cfg["s"], "g": cfg["g"], "delta": cfg["delta"],
+                   "parallelism": f"dp{world} (M-split, no collective)",
+                   "l2": f"{N_ROTATE} rotating buffer sets (weights, A^T, C^T) > 2x L2"},
+        "speedup_vs_cublas": dense_ms / ms_step,
+        "cublas": {"ms_per_step": dense_ms,
+                   "tflops_dense": world * dense_flops / (dense_ms * 1e-3) / 1e12},
+        "frac_of_dense_peak": value / world / pk["tc"],
+        "e2e": {"value": e2e_value, "unit": "TFLOP/s", "ms_per_step": e2e_ms,
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "path": "pinned host fp16 A -> H2D -> tw_transpose_cast -> tw_gemm -> D2H fp16"},
+        "roofline": roofline,
+        "cpu_baseline": {"value": cpu_rate, "unit": "TFLOP/s", "cores": workers, "kind": "port",
+                         "sample": f"{m_sample} of {m} tokens through every layer "
+                                   f"({cpu_s:.1f} s, oracle port of execute_batched lpt)"},
+        "gpu_launches": args.steps * len(layers) * (2 if tew else 1),
+        "launch": "CUDA graph per step (one graph per rotating buffer set)",
+        "clocks": clocks,
+    }
+    print(json.dumps(line))
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="bert", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    cfg = CONFIGS[args.config]
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        run_reference_arm(args, cfg, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    try:
+        run_ours(args, cfg, rank, world)
+    finally:
+        if world > 1:
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

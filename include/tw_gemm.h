@@ -122,6 +122,11 @@ TW_API int tw_transpose_cast(const void* a, int32_t a_dtype, int64_t m, int64_t 
 
 TW_API void tw_plan_destroy(tw_plan* plan);
 
+/* Diagnostics only: device buffer of (grid x 4096) int64 that K1 fills with
+ * clock64() timestamps per pipeline stage (nullptr disables).  Not for
+ * production use; see scripts/ktrace.py. */
+TW_API void tw_debug_set_trace(void* dev_buffer);
+
 /* Thread-local message of the last failing call ("" if none). */
 TW_API const char* tw_last_error(void);
 

@@ -47,6 +47,7 @@ SIGNATURES = {
     "tw_gemm_tew": (_c_int, [_vp, _vp, _i64, _i64, _vp, _i64, _i32, _vp]),
     "tw_transpose_cast": (_c_int, [_vp, _i32, _i64, _i64, _i64, _vp, _i32, _i64, _vp]),
     "tw_plan_destroy": (None, [_vp]),
+    "tw_debug_set_trace": (None, [_vp]),
     "tw_last_error": (ctypes.c_char_p, []),
     "tw_abi_version": (_i32, []),
 }

@@ -14,6 +14,7 @@
 #include <memory>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <string>
@@ -24,6 +25,7 @@ using namespace tw;
 namespace {
 
 thread_local std::string g_last_error;
+long long* g_trace = nullptr;  // diagnostics: per-CTA clock64 trace buffer
 
 int fail(int status, const char* fmt, ...) {
   char buf[512];
@@ -61,19 +63,23 @@ EncodeTiledFn encode_fn() {
   return fn;
 }
 
-// 2-D tensor map over a row-major [rows][cols] 16-bit matrix (cols contiguous).
+// 2-D tensor map over a row-major [rows][cols] matrix (cols contiguous).
 int make_map_2d(CUtensorMap* map, const void* base, int32_t dtype, uint64_t cols, uint64_t rows,
-                uint64_t pitch_elems, uint32_t box_cols, uint32_t box_rows) {
+                uint64_t pitch_elems, uint32_t box_cols, uint32_t box_rows,
+                bool swizzle128 = true) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) return fail(TW_ERR_CUDA, "cuTensorMapEncodeTiled unavailable (driver too old?)");
-  const CUtensorMapDataType dt =
-      dtype == kBF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+  const CUtensorMapDataType dt = dtype == kBF16  ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+                                 : dtype == kF32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                                 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+  const uint64_t esz = dtype == kF32 ? 4 : 2;
   cuuint64_t dims[2] = {cols, rows};
-  cuuint64_t strides[1] = {pitch_elems * 2};
+  cuuint64_t strides[1] = {pitch_elems * esz};
   cuuint32_t box[2] = {box_cols, box_rows};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = fn(map, dt, 2, const_cast<void*>(base), dims, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
     return fail(TW_ERR_INVALID_INPUT,
@@ -81,6 +87,11 @@ int make_map_2d(CUtensorMap* map, const void* base, int32_t dtype, uint64_t cols
                 (unsigned long long)cols, (unsigned long long)rows,
                 (unsigned long long)pitch_elems);
   return TW_OK;
+}
+
+int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return (v && *v) ? atoi(v) : dflt;
 }
 
 int sm_count_of_current_device(int* out) {
@@ -113,8 +124,10 @@ struct tw_plan {
   // device
   int32_t* d_rowidx = nullptr;
   SubTile* d_subtiles = nullptr;
-  int32_t* d_order = nullptr;
   void* d_payload = nullptr;
+  int32_t spm = 0;
+  float* d_ws = nullptr;
+  int32_t* d_ws_flags = nullptr;
   CUtensorMap map_pay;
   // TEW overlay
   bool has_overlay = false;
@@ -129,7 +142,7 @@ struct tw_plan {
   int32_t* d_ov_acc = nullptr;
 
   ~tw_plan() {
-    for (void* p : {(void*)d_rowidx, (void*)d_subtiles, (void*)d_order, d_payload,
+    for (void* p : {(void*)d_rowidx, (void*)d_subtiles, (void*)d_ws, (void*)d_ws_flags, d_payload,
                     (void*)d_union_rowmap, (void*)d_ov_start, (void*)d_ov_rows, (void*)d_ov_vals,
                     (void*)d_ov_out, (void*)d_ov_acc})
       if (p) cudaFree(p);
@@ -235,7 +248,7 @@ int tw_plan_create_cto(tw_plan** out, int32_t k, int32_t n, int32_t g, int32_t n
       SubTile st{};
       st.kp_steps = (h + kBK - 1) / kBK;
       st.idx_row = i;
-      st.pay_row = (int32_t)plan->subtiles.size() * bn;
+      st.pay_row = 0;  // assigned after ordering
       st.width = std::min(bn, w - c0);
       st.out_row = plan->tile_first_cond[i] + c0;
       st.kept = h;
@@ -246,6 +259,7 @@ int tw_plan_create_cto(tw_plan** out, int32_t k, int32_t n, int32_t g, int32_t n
     pbase += (int64_t)h * w;
   }
   plan->n_sub = (int32_t)plan->subtiles.size();
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
   std::vector<int32_t> order(plan->n_sub);
   std::iota(order.begin(), order.end(), 0);
   if (schedule == TW_SCHEDULE_LPT) {
@@ -257,14 +271,35 @@ int tw_plan_create_cto(tw_plan** out, int32_t k, int32_t n, int32_t g, int32_t n
       return wa > wb;
     });
   }
+  {
+    // the device table is stored in visiting order with stage offsets
+    std::vector<SubTile> ordered(plan->n_sub);
+    std::vector<int64_t> base2(plan->n_sub);
+    std::vector<int32_t> ld2(plan->n_sub);
+    int32_t off = 0;
+    for (int i = 0; i < plan->n_sub; ++i) {
+      ordered[i] = plan->subtiles[order[i]];
+      ordered[i].stage_off = off;
+      off += ordered[i].kp_steps;
+      base2[i] = src_base[order[i]];
+      ld2[i] = src_ld[order[i]];
+    }
+    plan->subtiles.swap(ordered);
+    src_base.swap(base2);
+    src_ld.swap(ld2);
+    plan->spm = off;
+    for (int i = 0; i < plan->n_sub; ++i) plan->subtiles[i].pay_row = i * bn;
+  }
+  // stream-K workspace: one [BN][128] fp32 partial + flag per CTA
+  TW_CUDA(cudaMalloc(&plan->d_ws, (size_t)plan->sm_count * bn * kBM * sizeof(float)));
+  TW_CUDA(cudaMalloc(&plan->d_ws_flags, (size_t)plan->sm_count * sizeof(int32_t)));
+  TW_CUDA(cudaMemsetAsync(plan->d_ws_flags, 0, (size_t)plan->sm_count * sizeof(int32_t), s));
   std::vector<int32_t> rowidx((size_t)n_tiles * plan->kp, k);  // pad = K -> TMA OOB zero fill
   for (int i = 0; i < n_tiles; ++i)
     std::copy(rows[i].begin(), rows[i].end(), rowidx.begin() + (size_t)i * plan->kp);
 
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (int st = upload(&plan->d_rowidx, rowidx, s)) return st;
   if (int st = upload(&plan->d_subtiles, plan->subtiles, s)) return st;
-  if (int st = upload(&plan->d_order, order, s)) return st;
   int64_t* d_src_base = nullptr;
   int32_t* d_src_ld = nullptr;
   float* d_src = nullptr;
@@ -402,7 +437,8 @@ static int check_io(const tw_plan* p, const void* at, int64_t m, int64_t ld_at, 
 }
 
 static int run_tw(const tw_plan* p, const void* at, int64_t m, int64_t ld_at, void* ct,
-                  int64_t ld_ct, int32_t out_dtype, const int32_t* rowmap, cudaStream_t s) {
+                  int64_t ld_ct, int32_t out_dtype, const int32_t* rowmap, int64_t out_rows,
+                  cudaStream_t s) {
   CUtensorMap map_at;
   if (int st = make_map_2d(&map_at, at, p->dtype, (uint64_t)m, (uint64_t)p->k, (uint64_t)ld_at,
                            64, 1))
@@ -410,7 +446,6 @@ static int run_tw(const tw_plan* p, const void* at, int64_t m, int64_t ld_at, vo
   GemmArgs a{};
   a.rowidx = p->d_rowidx;
   a.subtiles = p->d_subtiles;
-  a.order = p->d_order;
   a.rowmap = rowmap;
   a.out = ct;
   a.ld_out = ld_ct;
@@ -420,8 +455,40 @@ static int run_tw(const tw_plan* p, const void* at, int64_t m, int64_t ld_at, vo
   a.n_sub = p->n_sub;
   a.n_mblk = (int32_t)((m + kBM - 1) / kBM);
   a.n_units = a.n_sub * a.n_mblk;
-  const int grid = std::min(a.n_units, p->sm_count);
-  TW_CUDA(launch_tw_gather_gemm(map_at, p->map_pay, a, p->bn, p->dtype, grid, s));
+  a.K = p->k;
+  a.flags = env_int("TW_DEBUG_FLAGS", 0);
+  a.trace = g_trace;
+  const int esz = out_dtype == kF32 ? 4 : 2;
+  a.vec_ok = ((ld_ct * esz) % 16 == 0 && reinterpret_cast<uintptr_t>(ct) % 16 == 0) ? 1 : 0;
+  const int mode = env_int("TW_GATHER", kGatherCpAsync);
+  // condensed output: whole 32-column chunks leave through TMA 2-D stores
+  CUtensorMap map_out;
+  std::memset(&map_out, 0, sizeof(map_out));
+  a.use_tma_store = 0;
+  if (a.vec_ok && rowmap == nullptr && !env_int("TW_NO_TMA_STORE", 0)) {
+    if (make_map_2d(&map_out, ct, out_dtype, (uint64_t)m, (uint64_t)out_rows, (uint64_t)ld_ct,
+                    32, 32, /*swizzle128=*/false) == TW_OK)
+      a.use_tma_store = 1;
+    g_last_error.clear();
+  }
+  // Work split: whole units when they fit in one wave, else stream-K with
+  // equal stage ranges (each range must hold the longest unit so a unit is
+  // split at most once).
+  int grid = std::min(a.n_units, p->sm_count);
+  a.spm = p->spm;
+  a.split = 0;
+  a.ws = p->d_ws;
+  a.ws_flags = p->d_ws_flags;
+  if (a.n_units > p->sm_count && env_int("TW_STREAMK", 0)) {
+    const int64_t total = (int64_t)a.n_mblk * p->spm;
+    int max_kp = 1;
+    for (const SubTile& st : p->subtiles) max_kp = std::max(max_kp, (int)st.kp_steps);
+    grid = (int)std::min<int64_t>(p->sm_count, total / max_kp);
+    grid = std::max(grid, 1);
+    a.split = 1;
+  }
+  TW_CUDA(launch_tw_gather_gemm(map_at, p->map_pay, map_out, a, at, ld_at, p->bn, p->dtype, mode,
+                                grid, s));
   return TW_OK;
 }
 
@@ -429,7 +496,8 @@ int tw_gemm(const tw_plan* p, const void* at, int64_t m, int64_t ld_at, void* ct
             int32_t out_dtype, void* stream) {
   g_last_error.clear();
   if (int st = check_io(p, at, m, ld_at, ct, ld_ct, out_dtype)) return st;
-  return run_tw(p, at, m, ld_at, ct, ld_ct, out_dtype, nullptr, static_cast<cudaStream_t>(stream));
+  return run_tw(p, at, m, ld_at, ct, ld_ct, out_dtype, nullptr, p->n_cond,
+                static_cast<cudaStream_t>(stream));
 }
 
 int tw_gemm_tew(const tw_plan* p, const void* at, int64_t m, int64_t ld_at, void* ct,
@@ -438,7 +506,9 @@ int tw_gemm_tew(const tw_plan* p, const void* at, int64_t m, int64_t ld_at, void
   if (int st = check_io(p, at, m, ld_at, ct, ld_ct, out_dtype)) return st;
   if (!p->has_overlay) return fail(TW_ERR_INVALID_INPUT, "plan has no overlay attached");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (int st = run_tw(p, at, m, ld_at, ct, ld_ct, out_dtype, p->d_union_rowmap, s)) return st;
+  if (int st = run_tw(p, at, m, ld_at, ct, ld_ct, out_dtype, p->d_union_rowmap,
+                      (int64_t)p->union_cols.size(), s))
+    return st;
   ResidualArgs r{};
   r.at = at;
   r.ld_at = ld_at;
@@ -472,5 +542,7 @@ int tw_transpose_cast(const void* a, int32_t a_dtype, int64_t m, int64_t k, int6
 }
 
 void tw_plan_destroy(tw_plan* p) { delete p; }
+
+void tw_debug_set_trace(void* dev_buffer) { g_trace = static_cast<long long*>(dev_buffer); }
 
 }  // extern "C"

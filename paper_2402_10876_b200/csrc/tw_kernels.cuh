@@ -21,13 +21,13 @@ struct SubTile {
   int32_t width;     // live output columns of this slice (<= BN)
   int32_t out_row;   // first condensed output column == row of C'^T
   int32_t kept;      // K'_i (kept rows), for accounting
-  int32_t pad0, pad1;
+  int32_t stage_off; // first stage of this sub-tile inside one 128-token block
+  int32_t pad1;
 };
 
 struct GemmArgs {
   const int32_t* rowidx;    // [n_tiles][Kp] original K-row ids; padding = K (TMA OOB -> zeros)
-  const SubTile* subtiles;  // [n_sub]
-  const int32_t* order;     // [n_sub] sub-tile visiting order inside one m-block (LPT)
+  const SubTile* subtiles;  // [n_sub] in visiting order inside one m-block (LPT)
   const int32_t* rowmap;    // [n_cond] condensed col -> output row; nullptr = identity
   void* out;                // C'^T, rows = output columns, M contiguous
   int64_t ld_out;           // elements between output rows
@@ -37,13 +37,33 @@ struct GemmArgs {
   int32_t n_sub;
   int32_t n_mblk;
   int32_t n_units;          // n_sub * n_mblk
+  int32_t flags;            // diagnostics (kFlag*); 0 in production
+  int32_t K;                // original rows of A^T (gather sentinel)
+  const void* at;           // A^T base (cp.async gather path)
+  int64_t ld_at;            // A^T row pitch in elements
+  int32_t spm;              // stages per 128-token block (sum of kp_steps)
+  int32_t split;            // 1 = stream-K ranges, 0 = whole units strided by gridDim.x
+  float* ws;                // stream-K partials, gridDim.x x [BN][128] fp32
+  int32_t* ws_flags;        // gridDim.x publish flags (0 between launches)
+  int32_t vec_ok;           // output rows 16-byte aligned: vector stores allowed
+  int32_t use_tma_store;    // map_out is valid (condensed output via TMA 2-D stores)
+  long long* trace;         // optional per-CTA clock64 trace (4096 entries per CTA)
 };
+
+// Diagnostic switches (profiling only; results are wrong when set).
+constexpr int32_t kFlagSkipA = 1;       // do not load the gathered activations
+constexpr int32_t kFlagSkipStore = 2;   // do not write the output
+constexpr int32_t kFlagSkipMma = 4;     // do not issue tcgen05.mma
+
+// How the activation rows are gathered into shared memory.
+enum GatherMode : int32_t { kGatherTma4 = 0, kGatherCpAsync = 1 };
 
 // K1: persistent warp-specialised gather GEMM (tcgen05 + TMA gather4).
 // bn in {32, 64, 128, 256}; in_dtype kF16 or kBF16.
 cudaError_t launch_tw_gather_gemm(const CUtensorMap& map_at, const CUtensorMap& map_pay,
-                                  const GemmArgs& args, int bn, int in_dtype, int grid,
-                                  cudaStream_t stream);
+                                  const CUtensorMap& map_out, const GemmArgs& args,
+                                  const void* at, int64_t ld_at, int bn, int in_dtype,
+                                  int gather_mode, int grid, cudaStream_t stream);
 
 // Raise the dynamic shared-memory limit of every K1 instance (call once per
 // device before launching or capturing).

@@ -1,0 +1,73 @@
+"""Per-stage clock64 timeline of K1 (diagnostics; GPU box).
+
+    python scripts/ktrace.py [--layer 0|1|2] [--mode 1] [--flags 0]
+"""
+import argparse
+import os
+import sys
+from pathlib import Path
+
+import numpy as np
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import paper_2402_10876_b200 as tw  # noqa: E402
+from paper_2402_10876_b200 import _native  # noqa: E402
+
+LAYERS = [(768, 768), (768, 3072), (3072, 768)]
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--layer", type=int, default=0)
+    ap.add_argument("--mode", default="1")
+    ap.add_argument("--flags", default="0")
+    ap.add_argument("--m", type=int, default=8192)
+    args = ap.parse_args()
+    os.environ["TW_GATHER"] = args.mode
+    os.environ["TW_DEBUG_FLAGS"] = args.flags
+    k, n = LAYERS[args.layer]
+    w = tw.round_to(tw.synthetic_matrix(0, k, n, 0), "fp16")
+    _, tsm = tw.prune_tw(w, 0.75, 128)
+    plan = tw.TwPlan(tw.encode_cto(tsm))
+    a = tw.round_to(tw.synthetic_matrix(0, args.m, k, 1), "fp16")
+    at = tw.prepare_activations(torch.from_numpy(a).cuda())
+    out = torch.empty((tsm.n_condensed, args.m), dtype=torch.float16, device="cuda")
+    for _ in range(3):
+        plan.run(at, out=out)
+    buf = torch.zeros((148, 4096), dtype=torch.int64, device="cuda")
+    lib = _native.load_library()
+    lib.tw_debug_set_trace(buf.data_ptr())
+    torch.cuda.synchronize()
+    plan.run(at, out=out)
+    torch.cuda.synchronize()
+    lib.tw_debug_set_trace(None)
+    t = buf.cpu().numpy()
+    print(f"layer {k}x{n} mode={args.mode} flags={args.flags}")
+    full_ts, epi = [], []
+    ends = []
+    for c in range(148):
+        t0 = t[c, 3072]
+        if t0 == 0:
+            continue
+        ful = t[c, 1024:2048]
+        ns = int(np.count_nonzero(ful))
+        e = t[c, 2048:2048 + 512].reshape(-1, 2)
+        e = e[e[:, 0] > 0]
+        if ns:
+            full_ts.append(ful[ns - 1] - t0)
+        if len(e):
+            ends.append(e[-1, 1] - t0)
+            epi.extend((e[:, 1] - e[:, 0]).tolist())
+        if c < 4 or c in (74, 147):
+            f = ful[:ns] - t0
+            print(f" cta {c}: stages {ns}, full at {f[:3].tolist()}..{f[-2:].tolist()}, "
+                  "epi " + ", ".join(f"[{a0 - t0}, {a1 - t0}]" for a0, a1 in e))
+    q = lambda v: np.percentile(v, [10, 50, 90, 100]).astype(int).tolist() if len(v) else []
+    print(" last-full p10/50/90/max", q(full_ts))
+    print(" cta end (last epilogue) p10/50/90/max", q(ends))
+    print(" epilogue per segment p10/50/90/max", q(epi))
+
+
+if __name__ == "__main__":
+    main()

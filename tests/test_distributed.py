@@ -1,0 +1,92 @@
+"""Multi-rank partition logic on CPU (gloo, world_size 2).
+
+The GPU path runs the sm_100a kernel per rank and NCCL for the gather; here
+each rank computes its shard with the CPU oracle so the partition, the
+contiguous C'^T row ownership and the all-gather assembly are checked
+without a GPU.
+"""
+
+from __future__ import annotations
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+import paper_2402_10876_b200 as tw
+from paper_2402_10876_b200 import distributed as D
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _problem():
+    rng = np.random.default_rng(42)
+    w = rng.normal(size=(96, 200)).astype(np.float32)
+    a = rng.normal(size=(50, 96)).astype(np.float32)
+    _, tsm = tw.prune_tw(w, 0.5, 16)
+    return a, tw.encode_cto(tsm)
+
+
+def _worker(rank, world, port, mode, results):
+    import torch
+    import torch.distributed as dist
+
+    from oracle import tilesparse_oracle as orc
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        a, enc = _problem()
+        if mode == "columns":
+            shards = D.column_shards(enc, world)
+            rows = D.shard_rows(enc, shards)
+            lo, hi = shards[rank]
+            sub = D.shard_encoding(enc, lo, hi)
+            local = torch.from_numpy(np.ascontiguousarray(orc.c_gemm_cto_enc(a, sub).T))
+            full_t = D.gather_rows(local, rows)
+            results[rank] = full_t.numpy().T.copy()
+        else:
+            lo, hi = D.token_slice(a.shape[0], world, rank)
+            local = torch.from_numpy(orc.c_gemm_cto_enc(a[lo:hi], enc))
+            out = [torch.empty(0)] * world
+            dist.all_gather_object(out, (lo, hi, local.numpy()))
+            results[rank] = np.concatenate([o[2] for o in sorted(out, key=lambda t: t[0])])
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("mode", ["columns", "tokens"])
+def test_two_rank_sharding_equals_single_device(mode):
+    from oracle import tilesparse_oracle as orc
+
+    a, enc = _problem()
+    want = orc.c_gemm_cto_enc(a, enc)
+    mgr = mp.Manager()
+    results = mgr.dict()
+    mp.spawn(_worker, args=(2, _free_port(), mode, results), nprocs=2, join=True)
+    for r in range(2):
+        assert np.array_equal(results[r], want)
+
+
+def test_partition_contiguous_balances():
+    bounds = D.partition_contiguous([10] * 64, 8)
+    assert bounds == [(8 * i, 8 * i + 8) for i in range(8)]
+    b = D.partition_contiguous([100, 1, 1, 1, 1, 100], 2)
+    assert b == [(0, 3), (3, 6)]
+    b = D.partition_contiguous([5, 5], 4)
+    assert b[-1][1] == 2 and sum(hi - lo for lo, hi in b) == 2
+
+
+def test_token_slice_covers_m():
+    for m in (1, 127, 128, 1000, 8192):
+        for world in (1, 2, 3, 8):
+            spans = [D.token_slice(m, world, r) for r in range(world)]
+            assert spans[0][0] == 0 and spans[-1][1] == m
+            assert all(spans[i][1] == spans[i + 1][0] for i in range(world - 1))

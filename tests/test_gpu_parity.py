@@ -188,3 +188,16 @@ def test_nonfinite_activation_not_in_padding():
     a2[:, dead] = np.nan
     out = tw.gemm_tile_sparse(a2, tsm).condensed.cpu().numpy()
     assert np.all(np.isfinite(out))
+
+
+@pytest.mark.parametrize("k,n,m,g,s", [
+    (3072, 768, 8192, 128, 0.75),   # BERT FFN-2 shape: 192 units on 148 SMs -> stream-K
+    (1000, 2000, 2500, 64, 0.6),    # ragged K' per tile, 20 blocks x 25 tiles
+    (512, 4096, 4096, 256, 0.75),   # BN = 256
+])
+def test_stream_k_matches_oracle_and_is_deterministic(k, n, m, g, s):
+    w, a, plan, tsm = _problem(k, n, m, s, g, seed=k + n + m)
+    o1 = tw.gemm_tile_sparse(a, tsm).condensed.cpu().numpy()
+    o2 = tw.gemm_tile_sparse(a, tsm).condensed.cpu().numpy()
+    assert o1.tobytes() == o2.tobytes()
+    assert tw.relative_error(o1, _oracle_tw(a, tsm)) <= TOL["fp32"]
