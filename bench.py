@@ -15,10 +15,10 @@ value        effective TFLOP/s = surviving FLOPs (metrics.report.sparse_flops,
              every step streams cold activations, weights and outputs.  Each
              step is one CUDA-graph replay of the three layer launches (the
              dense cuBLAS arm is graph-captured the same way).
-e2e          same metric through the public API (prepare_activations +
-             TwPlan.run) from pinned HOST fp16 activations, with the H2D
-             copies, the A->A^T transpose kernel, the GEMM and the D2H copy
-             of the fp16 result inside the timed region.
+e2e          same metric through the public API (TwPlan.prepare + TwPlan.run)
+             from pinned HOST fp16 activations (M x K, the reference's layout),
+             with the H2D copies, the A -> grouped-input kernel (K4g), the
+             GEMM and the D2H copy of the fp16 result inside the timed region.
 cublas       dense torch.matmul (cuBLAS) at the same shapes and layout.
 roofline     K1 (tw_gather_gemm) launches timed per layer with CUDA events;
              achieved = algorithmic bytes / launch time vs the
@@ -256,7 +256,7 @@ def run_ours(args, cfg, rank: int, world: int) -> None:
         for li, L in enumerate(layers):
             plan = tw.TwPlan(L["enc"], L["ov"], compute_dtype="fp16")
             a = activations(cfg, L["k"], li, rank)
-            at = tw.prepare_activations(torch.from_numpy(a).to(dev))
+            at = plan.prepare(torch.from_numpy(a).to(dev))
             rows = plan.info.n_union if tew else plan.info.n_condensed
             ct = torch.empty((rows, m), dtype=torch.float16, device=dev)
             layer_set.append((plan, at, ct))
@@ -343,7 +343,9 @@ def run_ours(args, cfg, rank: int, world: int) -> None:
         row = []
         for li, L in enumerate(layers):
             wt = torch.from_numpy(np.ascontiguousarray(L["w"].T)).to(dev, torch.float16)
-            row.append((wt, sets[r][li][1],
+            a_nat = activations(cfg, L["k"], li, rank)
+            at_nat = tw.prepare_activations(torch.from_numpy(a_nat).to(dev))  # plain A^T
+            row.append((wt, at_nat,
                         torch.empty((L["n"], m), dtype=torch.float16, device=dev)))
         dense.append(row)
 
@@ -373,6 +375,24 @@ def run_ours(args, cfg, rank: int, world: int) -> None:
     dense_flops = sum(2 * m * L["k"] * L["n"] for L in layers)
     del dense, dense_graphs
 
+    # ---- layout prep: A (M x K, fp16, device) -> each plan's grouped input
+    a_dev = [torch.from_numpy(activations(cfg, L["k"], li, rank)).to(dev, torch.float16)
+             for li, L in enumerate(layers)]
+
+    def prep_set(r: int):
+        for li, (plan, x, _) in enumerate(sets[r]):
+            plan.prepare(a_dev[li], out=x.as_strided((x.shape[0], x.stride(0)), (x.stride(0), 1)))
+
+    prep_graphs = [capture_graph(lambda r=r: prep_set(r)) for r in range(N_ROTATE)]
+    p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    p0.record(stream)
+    for i in range(args.steps):
+        prep_graphs[i % N_ROTATE].replay()
+    p1.record(stream)
+    torch.cuda.synchronize()
+    prep_ms = p0.elapsed_time(p1) / args.steps
+    del prep_graphs
+
     # ---- e2e through the public API from pinned host memory
     host_a = [torch.from_numpy(activations(cfg, L["k"], li, rank)).to(torch.float16)
               .pin_memory() for li, L in enumerate(layers)]
@@ -385,7 +405,7 @@ def run_ours(args, cfg, rank: int, world: int) -> None:
     def e2e_step(i: int):
         for li, (plan, _, ct) in enumerate(sets[i % N_ROTATE]):
             dev_a[li].copy_(host_a[li], non_blocking=True)
-            at = tw.prepare_activations(dev_a[li])
+            at = plan.prepare(dev_a[li])
             if tew:
                 plan.run_tew(at, out=ct)
             else:
@@ -448,12 +468,18 @@ def run_ours(args, cfg, rank: int, world: int) -> None:
                    "parallelism": f"dp{world} (M-split, no collective)",
                    "l2": f"{N_ROTATE} rotating buffer sets (weights, A^T, C^T) > 2x L2"},
         "speedup_vs_cublas": dense_ms / ms_step,
+        "prep": {"ms_per_step": prep_ms,
+                 "what": "A (M x K fp16, device) -> grouped input X per layer (tw_prepare_input); "
+                         "not in value (a network's previous epilogue writes X directly), "
+                         "inside e2e",
+                 "value_incl_prep": world * flops_step / ((ms_step + prep_ms) * 1e-3) / 1e12,
+                 "speedup_vs_cublas_incl_prep": dense_ms / (ms_step + prep_ms)},
         "cublas": {"ms_per_step": dense_ms,
                    "tflops_dense": world * dense_flops / (dense_ms * 1e-3) / 1e12},
         "frac_of_dense_peak": value / world / pk["tc"],
         "e2e": {"value": e2e_value, "unit": "TFLOP/s", "ms_per_step": e2e_ms,
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "path": "pinned host fp16 A -> H2D -> tw_transpose_cast -> tw_gemm -> D2H fp16"},
+                "path": "pinned host fp16 A (M x K) -> H2D -> tw_prepare_input -> tw_gemm -> D2H fp16"},
         "roofline": roofline,
         "cpu_baseline": {"value": cpu_rate, "unit": "TFLOP/s", "cores": workers, "kind": "port",
                          "sample": f"{m_sample} of {m} tokens through every layer "

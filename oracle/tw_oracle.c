@@ -68,8 +68,9 @@ int tw_oracle_gemm_cto(const float* a, int64_t m, int64_t k, int32_t n_tiles,
                        double* out, int32_t threads) {
   int64_t n_cond = 0;
   for (int32_t t = 0; t < n_tiles; ++t) n_cond += col_counts[t];
-  if (threads < 1) threads = 1;
+  if (m <= 0) return 0;
   if (threads > m) threads = (int32_t)m;
+  if (threads < 1) threads = 1;
   pthread_t* tid = (pthread_t*)calloc((size_t)threads, sizeof(pthread_t));
   job_t* jobs = (job_t*)calloc((size_t)threads, sizeof(job_t));
   if (!tid || !jobs) return 1;

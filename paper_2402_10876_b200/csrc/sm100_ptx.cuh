@@ -203,6 +203,21 @@ __device__ __forceinline__ void tmem_ld_wait() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+// Programmatic dependent launch: block until the preceding grid in the stream
+// has completed (its memory is visible); allow the next grid to launch.
+__device__ __forceinline__ void grid_dependency_wait() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+__device__ __forceinline__ void grid_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
 // ------------------------------------------------- UMMA shared-memory descriptors
 // Bit layout (PTX "matrix descriptor", sm_100): [0,14) start>>4, [16,30) LBO>>4,
 // [32,46) SBO>>4, [46,48) version=1, [49,52) base offset, [61,64) layout type

@@ -1,8 +1,22 @@
 // C ABI (include/tw_gemm.h): host-side validation of CTO encodings and
-// overlays, construction of the device weight format, TMA descriptor
-// encoding, and kernel dispatch.  All numerics run in the kernels of
-// tw_gemm.cu / tw_aux.cu; nothing here computes on the CPU beyond index
-// bookkeeping.
+// overlays, construction of the device weight format and of the grouped input
+// layout, TMA descriptor encoding, and kernel dispatch.  All numerics run in
+// the kernels of tw_gemm.cu / tw_aux.cu; nothing here computes on the CPU
+// beyond index bookkeeping.
+//
+// Grouped input layout.  A TW tile keeps an arbitrary half of the K rows, so
+// gathering its rows from A^T row by row caps the load rate at ~6 TB/s on
+// B200 (measured, scripts/microbench_gather.cu) while TMA 2-D tiles over
+// contiguous rows reach ~12.6 TB/s.  The plan therefore defines the layout
+// the GEMM reads its activations in: tiles are taken in clusters of up to
+// `cluster` consecutive tiles; inside a cluster every kept row is placed in
+// the group of rows with the same tile-membership pattern, groups ordered in
+// reflected Gray-code order and padded to 8 rows.  Each tile's kept rows then
+// form <= 2^(c-1) (for c = 3: at most 2) contiguous runs, read with a handful
+// of TMA boxes per stage.  The layout is built by tw_prepare_input (or, in a
+// network, directly by the previous layer's epilogue); rows of the layout are
+// copies of original K rows, so results are unchanged (padding rows are zero
+// in both the activations and the payload).
 #include "../../include/tw_gemm.h"
 #include "tw_kernels.cuh"
 
@@ -10,12 +24,12 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
-#include <iterator>
-#include <memory>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <iterator>
+#include <memory>
 #include <numeric>
 #include <string>
 #include <vector>
@@ -64,9 +78,9 @@ EncodeTiledFn encode_fn() {
 }
 
 // 2-D tensor map over a row-major [rows][cols] matrix (cols contiguous).
+// swizzle: 0 = none, 64 = 64-byte, 128 = 128-byte.
 int make_map_2d(CUtensorMap* map, const void* base, int32_t dtype, uint64_t cols, uint64_t rows,
-                uint64_t pitch_elems, uint32_t box_cols, uint32_t box_rows,
-                bool swizzle128 = true) {
+                uint64_t pitch_elems, uint32_t box_cols, uint32_t box_rows, int swizzle = 128) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) return fail(TW_ERR_CUDA, "cuTensorMapEncodeTiled unavailable (driver too old?)");
   const CUtensorMapDataType dt = dtype == kBF16  ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
@@ -79,7 +93,9 @@ int make_map_2d(CUtensorMap* map, const void* base, int32_t dtype, uint64_t cols
   cuuint32_t estr[2] = {1, 1};
   CUresult r = fn(map, dt, 2, const_cast<void*>(base), dims, strides, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE,
-                  swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                  swizzle == 128  ? CU_TENSOR_MAP_SWIZZLE_128B
+                  : swizzle == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                  : CU_TENSOR_MAP_SWIZZLE_NONE,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
     return fail(TW_ERR_INVALID_INPUT,
@@ -110,24 +126,113 @@ int upload(T** dptr, const std::vector<T>& host, cudaStream_t s) {
   return TW_OK;
 }
 
+int32_t round_up(int32_t v, int32_t a) { return (v + a - 1) / a * a; }
+
+// ------------------------------------------------------ grouped input layout
+struct Layout {
+  std::vector<int32_t> src;                   // grouped row -> original row, -1 = zero
+  std::vector<std::vector<RunDesc>> runs;     // per tile, covering its padded sequence
+  std::vector<int32_t> seq_len;               // per tile: padded sequence length (mult. of kBK)
+  std::vector<std::vector<int32_t>> seq;      // per tile: grouped row of every sequence slot
+  std::vector<int32_t> home;                  // original row -> one grouped row holding it
+  int32_t zero_row = 0;                       // first of kBK zero rows at the end
+};
+
+void append_group(Layout& L, const std::vector<int32_t>& rows) {
+  L.src.insert(L.src.end(), rows.begin(), rows.end());
+  while (L.src.size() % kRunAlign) L.src.push_back(-1);
+}
+
+Layout build_layout(int32_t k, const std::vector<std::vector<int32_t>>& kept, int cluster) {
+  const int n_tiles = static_cast<int>(kept.size());
+  Layout L;
+  L.runs.resize(n_tiles);
+  L.seq.resize(n_tiles);
+  L.seq_len.resize(n_tiles);
+  L.home.assign(k, -1);
+  for (int c0 = 0; c0 < n_tiles; c0 += cluster) {
+    const int nc = std::min(cluster, n_tiles - c0);
+    std::vector<uint32_t> pat(k, 0);
+    for (int t = 0; t < nc; ++t)
+      for (int32_t r : kept[c0 + t]) pat[r] |= 1u << t;
+    // bucket rows by pattern, ascending original order inside a bucket
+    std::vector<std::vector<int32_t>> bucket(1u << nc);
+    for (int32_t r = 0; r < k; ++r)
+      if (pat[r]) bucket[pat[r]].push_back(r);
+    // groups in reflected Gray-code order; a tile's consecutive groups merge
+    // into one run
+    std::vector<int32_t> open_start(nc, -1);  // grouped row where the tile's current run began
+    std::vector<int32_t> seqpos(nc, 0);
+    auto close_run = [&](int t) {
+      if (open_start[t] < 0) return;
+      const int32_t len = static_cast<int32_t>(L.src.size()) - open_start[t];
+      L.runs[c0 + t].push_back(RunDesc{seqpos[t], open_start[t], len, 0});
+      seqpos[t] += len;
+      open_start[t] = -1;
+    };
+    for (uint32_t i = 1; i < (1u << nc); ++i) {
+      const uint32_t g = i ^ (i >> 1);
+      if (bucket[g].empty()) continue;
+      for (int t = 0; t < nc; ++t) {
+        if (g & (1u << t)) {
+          if (open_start[t] < 0) open_start[t] = static_cast<int32_t>(L.src.size());
+        } else {
+          close_run(t);
+        }
+      }
+      const int32_t base = static_cast<int32_t>(L.src.size());
+      for (size_t q = 0; q < bucket[g].size(); ++q)
+        if (L.home[bucket[g][q]] < 0) L.home[bucket[g][q]] = base + static_cast<int32_t>(q);
+      append_group(L, bucket[g]);
+    }
+    for (int t = 0; t < nc; ++t) close_run(t);
+  }
+  // rows kept by no tile (needed only by a TEW overlay) go in a rest region
+  std::vector<int32_t> rest;
+  for (int32_t r = 0; r < k; ++r)
+    if (L.home[r] < 0) rest.push_back(r);
+  for (size_t i = 0; i < rest.size(); ++i)
+    L.home[rest[i]] = static_cast<int32_t>(L.src.size() + i);
+  if (!rest.empty()) append_group(L, rest);
+  // kBK zero rows: every tile's sequence is padded to whole stages from here
+  L.zero_row = static_cast<int32_t>(L.src.size());
+  L.src.insert(L.src.end(), kBK, -1);
+  for (int t = 0; t < n_tiles; ++t) {
+    int32_t len = 0;
+    for (const RunDesc& rd : L.runs[t]) len = rd.seq_off + rd.len;
+    const int32_t padded = round_up(std::max(len, 1), kBK);
+    if (padded > len) L.runs[t].push_back(RunDesc{len, L.zero_row, padded - len, 0});
+    L.seq_len[t] = padded;
+    L.seq[t].reserve(padded);
+    for (const RunDesc& rd : L.runs[t])
+      for (int32_t j = 0; j < rd.len; ++j) L.seq[t].push_back(rd.row + j);
+  }
+  return L;
+}
+
 }  // namespace
 
 struct tw_plan {
   int32_t k = 0, n = 0, g = 0, n_tiles = 0, n_sub = 0, bn = 0, kp = 0, n_cond = 0;
-  int32_t dtype = kF16, schedule = TW_SCHEDULE_LPT, sm_count = 0;
+  int32_t dtype = kF16, schedule = TW_SCHEDULE_LPT, sm_count = 0, cluster = 3;
   std::vector<SubTile> subtiles;
   std::vector<int32_t> cond_cols;        // condensed col -> original col
   std::vector<int32_t> tile_of_col;      // original col -> tile (or -1)
   std::vector<std::vector<uint8_t>> tile_rows;  // per tile: K flags
   std::vector<int32_t> tile_first_cond;  // per tile: first condensed column
   int64_t kept_macs = 0;
-  // device
-  int32_t* d_rowidx = nullptr;
-  SubTile* d_subtiles = nullptr;
-  void* d_payload = nullptr;
+  Layout layout;
   int32_t spm = 0;
+  // device
+  SubTile* d_subtiles = nullptr;
+  RunDesc* d_runs = nullptr;
+  void* d_payload = nullptr;
   float* d_ws = nullptr;
   int32_t* d_ws_flags = nullptr;
+  int32_t* d_prep_ptr = nullptr;
+  int32_t* d_prep_rows = nullptr;
+  int32_t* d_prep_zero = nullptr;
+  int32_t n_prep_zero = 0;
   CUtensorMap map_pay;
   // TEW overlay
   bool has_overlay = false;
@@ -142,18 +247,20 @@ struct tw_plan {
   int32_t* d_ov_acc = nullptr;
 
   ~tw_plan() {
-    for (void* p : {(void*)d_rowidx, (void*)d_subtiles, (void*)d_ws, (void*)d_ws_flags, d_payload,
+    for (void* p : {(void*)d_subtiles, (void*)d_runs, d_payload, (void*)d_ws,
+                    (void*)d_ws_flags, (void*)d_prep_ptr, (void*)d_prep_rows, (void*)d_prep_zero,
                     (void*)d_union_rowmap, (void*)d_ov_start, (void*)d_ov_rows, (void*)d_ov_vals,
                     (void*)d_ov_out, (void*)d_ov_acc})
       if (p) cudaFree(p);
   }
+  int64_t input_rows() const { return static_cast<int64_t>(layout.src.size()); }
 };
 
 extern "C" {
 
 const char* tw_last_error(void) { return g_last_error.c_str(); }
 
-int32_t tw_abi_version(void) { return 100; }
+int32_t tw_abi_version(void) { return 200; }
 
 int tw_plan_create_cto(tw_plan** out, int32_t k, int32_t n, int32_t g, int32_t n_tiles,
                        const uint32_t* row_counts, const uint32_t* col_counts,
@@ -192,8 +299,10 @@ int tw_plan_create_cto(tw_plan** out, int32_t k, int32_t n, int32_t g, int32_t n
   plan->n_tiles = n_tiles;
   plan->dtype = compute_dtype;
   plan->schedule = schedule;
+  plan->cluster = std::max(1, std::min(env_int("TW_CLUSTER", 3), 5));
   if (int st = sm_count_of_current_device(&plan->sm_count)) return st;
   TW_CUDA(configure_gemm_kernels());
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
 
   // decode offsets: tile_rows / tile_cols (formats.py:138-158) and the column
   // order check of gemm_cto (executor.py:478-480)
@@ -235,10 +344,23 @@ int tw_plan_create_cto(tw_plan** out, int32_t k, int32_t n, int32_t g, int32_t n
   }
   plan->n_cond = (int32_t)plan->cond_cols.size();
 
-  // kernel geometry
-  const int bn = max_w <= 32 ? 32 : max_w <= 64 ? 64 : max_w <= 128 ? 128 : 256;
+  // grouped input layout and per-tile row runs
+  plan->layout = build_layout(k, rows, plan->cluster);
+  const Layout& L = plan->layout;
+  int32_t kp = kBK;
+  for (int i = 0; i < n_tiles; ++i) kp = std::max(kp, L.seq_len[i]);
+  plan->kp = kp;
+
+  // sub-tiles (128-column UMMA-M slices), runs table, payload sources
+  const int bn = kBN;
   plan->bn = bn;
-  plan->kp = (int32_t)(((max_h + kBK - 1) / kBK) * kBK);
+  std::vector<RunDesc> runs;
+  std::vector<int32_t> tile_run_off(n_tiles);
+  for (int i = 0; i < n_tiles; ++i) {
+    tile_run_off[i] = (int32_t)runs.size();
+    runs.insert(runs.end(), L.runs[i].begin(), L.runs[i].end());
+  }
+  std::vector<SubTile> subs;
   std::vector<int64_t> src_base;
   std::vector<int32_t> src_ld;
   int64_t pbase = 0;
@@ -246,78 +368,106 @@ int tw_plan_create_cto(tw_plan** out, int32_t k, int32_t n, int32_t g, int32_t n
     const int32_t h = (int32_t)row_counts[i], w = (int32_t)col_counts[i];
     for (int32_t c0 = 0; c0 < w; c0 += bn) {
       SubTile st{};
-      st.kp_steps = (h + kBK - 1) / kBK;
+      st.kp_steps = L.seq_len[i] / kBK;
       st.idx_row = i;
-      st.pay_row = 0;  // assigned after ordering
       st.width = std::min(bn, w - c0);
       st.out_row = plan->tile_first_cond[i] + c0;
       st.kept = h;
-      plan->subtiles.push_back(st);
+      st.run_off = tile_run_off[i];
+      st.n_runs = (int32_t)L.runs[i].size();
+      subs.push_back(st);
       src_base.push_back(pbase + (int64_t)c0 * h);
       src_ld.push_back(h);
     }
     pbase += (int64_t)h * w;
   }
-  plan->n_sub = (int32_t)plan->subtiles.size();
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  plan->n_sub = (int32_t)subs.size();
   std::vector<int32_t> order(plan->n_sub);
   std::iota(order.begin(), order.end(), 0);
   if (schedule == TW_SCHEDULE_LPT) {
     // executor.py:526 sorts tiles by (-macs, index); per 128-token block the
     // MACs of a sub-tile are proportional to K' * width
     std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
-      const int64_t wa = (int64_t)plan->subtiles[a].kept * plan->subtiles[a].width;
-      const int64_t wb = (int64_t)plan->subtiles[b].kept * plan->subtiles[b].width;
-      return wa > wb;
+      return (int64_t)subs[a].kept * subs[a].width > (int64_t)subs[b].kept * subs[b].width;
     });
   }
-  {
-    // the device table is stored in visiting order with stage offsets
-    std::vector<SubTile> ordered(plan->n_sub);
-    std::vector<int64_t> base2(plan->n_sub);
-    std::vector<int32_t> ld2(plan->n_sub);
-    int32_t off = 0;
-    for (int i = 0; i < plan->n_sub; ++i) {
-      ordered[i] = plan->subtiles[order[i]];
-      ordered[i].stage_off = off;
-      off += ordered[i].kp_steps;
-      base2[i] = src_base[order[i]];
-      ld2[i] = src_ld[order[i]];
-    }
-    plan->subtiles.swap(ordered);
-    src_base.swap(base2);
-    src_ld.swap(ld2);
-    plan->spm = off;
-    for (int i = 0; i < plan->n_sub; ++i) plan->subtiles[i].pay_row = i * bn;
+  // device table in visiting order with stage offsets and payload rows
+  std::vector<int64_t> base2(plan->n_sub);
+  std::vector<int32_t> ld2(plan->n_sub);
+  int32_t off = 0;
+  for (int i = 0; i < plan->n_sub; ++i) {
+    plan->subtiles.push_back(subs[order[i]]);
+    SubTile& st = plan->subtiles.back();
+    st.stage_off = off;
+    st.pay_row = i * bn;
+    off += st.kp_steps;
+    base2[i] = src_base[order[i]];
+    ld2[i] = src_ld[order[i]];
   }
-  // stream-K workspace: one [BN][128] fp32 partial + flag per CTA
-  TW_CUDA(cudaMalloc(&plan->d_ws, (size_t)plan->sm_count * bn * kBM * sizeof(float)));
+  plan->spm = off;
+
+  // payload slot positions: kept-row index of every sequence slot (-1 = zero)
+  std::vector<int32_t> seq_pos((size_t)n_tiles * kp, -1);
+  for (int i = 0; i < n_tiles; ++i) {
+    for (int32_t j = 0; j < L.seq_len[i]; ++j) {
+      const int32_t grow = L.seq[i][j];
+      const int32_t orow = L.src[grow];
+      if (orow >= 0) {
+        auto it = std::lower_bound(rows[i].begin(), rows[i].end(), orow);
+        if (it != rows[i].end() && *it == orow)
+          seq_pos[(size_t)i * kp + j] = (int32_t)(it - rows[i].begin());
+      }
+    }
+  }
+
+  // prep lists: copies of each original row, zero rows
+  std::vector<int32_t> prep_ptr(k + 1, 0), prep_rows, prep_zero;
+  for (size_t j = 0; j < L.src.size(); ++j) {
+    if (L.src[j] >= 0)
+      ++prep_ptr[L.src[j] + 1];
+    else
+      prep_zero.push_back((int32_t)j);
+  }
+  for (int32_t r = 0; r < k; ++r) prep_ptr[r + 1] += prep_ptr[r];
+  prep_rows.resize(prep_ptr[k]);
+  {
+    std::vector<int32_t> fill(prep_ptr.begin(), prep_ptr.end() - 1);
+    for (size_t j = 0; j < L.src.size(); ++j)
+      if (L.src[j] >= 0) prep_rows[fill[L.src[j]]++] = (int32_t)j;
+  }
+  plan->n_prep_zero = (int32_t)prep_zero.size();
+
+  if (int st = upload(&plan->d_subtiles, plan->subtiles, s)) return st;
+  if (int st = upload(&plan->d_runs, runs, s)) return st;
+  if (int st = upload(&plan->d_prep_ptr, prep_ptr, s)) return st;
+  if (int st = upload(&plan->d_prep_rows, prep_rows, s)) return st;
+  if (int st = upload(&plan->d_prep_zero, prep_zero, s)) return st;
+  // stream-K workspace: one [kBN][kTN] fp32 partial + flag per CTA
+  TW_CUDA(cudaMalloc(&plan->d_ws, (size_t)plan->sm_count * kBN * kTN * sizeof(float)));
   TW_CUDA(cudaMalloc(&plan->d_ws_flags, (size_t)plan->sm_count * sizeof(int32_t)));
   TW_CUDA(cudaMemsetAsync(plan->d_ws_flags, 0, (size_t)plan->sm_count * sizeof(int32_t), s));
-  std::vector<int32_t> rowidx((size_t)n_tiles * plan->kp, k);  // pad = K -> TMA OOB zero fill
-  for (int i = 0; i < n_tiles; ++i)
-    std::copy(rows[i].begin(), rows[i].end(), rowidx.begin() + (size_t)i * plan->kp);
 
-  if (int st = upload(&plan->d_rowidx, rowidx, s)) return st;
-  if (int st = upload(&plan->d_subtiles, plan->subtiles, s)) return st;
   int64_t* d_src_base = nullptr;
   int32_t* d_src_ld = nullptr;
+  int32_t* d_seq_pos = nullptr;
   float* d_src = nullptr;
-  if (int st = upload(&d_src_base, src_base, s)) return st;
-  if (int st = upload(&d_src_ld, src_ld, s)) return st;
+  if (int st = upload(&d_src_base, base2, s)) return st;
+  if (int st = upload(&d_src_ld, ld2, s)) return st;
+  if (int st = upload(&d_seq_pos, seq_pos, s)) return st;
   TW_CUDA(cudaMalloc(&d_src, std::max<int64_t>(pbase, 1) * sizeof(float)));
   TW_CUDA(cudaMemcpyAsync(d_src, payload, pbase * sizeof(float), cudaMemcpyHostToDevice, s));
-  const size_t pay_bytes = (size_t)plan->n_sub * bn * plan->kp * 2;
+  const size_t pay_bytes = (size_t)plan->n_sub * bn * kp * 2;
   TW_CUDA(cudaMalloc(&plan->d_payload, pay_bytes));
-  PayloadArgs pa{d_src, d_src_base, d_src_ld, plan->d_subtiles, plan->d_payload,
-                 compute_dtype, bn, plan->kp, plan->n_sub};
+  PayloadArgs pa{d_src, d_src_base, d_src_ld, d_seq_pos, plan->d_subtiles, plan->d_payload,
+                 compute_dtype, bn, kp, plan->n_sub};
   TW_CUDA(launch_build_payload(pa, s));
   TW_CUDA(cudaStreamSynchronize(s));
   cudaFree(d_src);
   cudaFree(d_src_base);
   cudaFree(d_src_ld);
-  if (int st = make_map_2d(&plan->map_pay, plan->d_payload, compute_dtype, plan->kp,
-                           (uint64_t)plan->n_sub * bn, plan->kp, kBK, bn))
+  cudaFree(d_seq_pos);
+  if (int st = make_map_2d(&plan->map_pay, plan->d_payload, compute_dtype, kp,
+                           (uint64_t)plan->n_sub * bn, kp, kBK, bn))
     return st;
   plan->union_cols = plan->cond_cols;
   *out = guard.release();
@@ -339,14 +489,16 @@ int tw_plan_attach_overlay(tw_plan* p, int32_t k, int32_t n, int64_t nnz, const 
   std::vector<int32_t> ov_cols;
   for (int32_t c = 0; c < n; ++c) {
     const int64_t lo = col_ptr[c], hi = col_ptr[c + 1];
-    if (hi < lo) return fail(TW_ERR_INVALID_INPUT, "overlay column pointers must be non-decreasing");
+    if (hi < lo)
+      return fail(TW_ERR_INVALID_INPUT, "overlay column pointers must be non-decreasing");
     if (hi == lo) continue;
     ov_cols.push_back(c);
     const int t = p->tile_of_col[c];
     for (int64_t e = lo; e < hi; ++e) {
       const int64_t r = row_idx[e];
       if (r < 0 || r >= k || (e > lo && r <= row_idx[e - 1]))
-        return fail(TW_ERR_INVALID_INPUT, "overlay rows must be strictly increasing within a column");
+        return fail(TW_ERR_INVALID_INPUT,
+                    "overlay rows must be strictly increasing within a column");
       if (t >= 0 && p->tile_rows[t][r])
         return fail(TW_ERR_CONTRACT, "overlay entries overlap tile payload positions");
     }
@@ -362,7 +514,7 @@ int tw_plan_attach_overlay(tw_plan* p, int32_t k, int32_t n, int64_t nnz, const 
   std::vector<float> vals;
   for (int32_t c : ov_cols) {
     for (int64_t e = col_ptr[c]; e < col_ptr[c + 1]; ++e) {
-      rows.push_back((int32_t)row_idx[e]);
+      rows.push_back(p->layout.home[row_idx[e]]);  // grouped-input row of the original row
       vals.push_back(values[e]);
     }
     start.push_back((int32_t)rows.size());
@@ -406,6 +558,9 @@ int tw_plan_get_info(const tw_plan* p, tw_plan_info* info) {
   info->kept_macs_per_token = p->kept_macs + p->nnz;
   info->sm_count = p->sm_count;
   info->has_overlay = p->has_overlay ? 1 : 0;
+  info->input_rows = p->input_rows();
+  info->cluster = p->cluster;
+  info->reserved = 0;
   return TW_OK;
 }
 
@@ -421,57 +576,95 @@ int tw_plan_union_columns(const tw_plan* p, int32_t* out) {
   return TW_OK;
 }
 
-static int check_io(const tw_plan* p, const void* at, int64_t m, int64_t ld_at, const void* ct,
-                    int64_t ld_ct, int32_t out_dtype) {
-  if (!p || !at || !ct) return fail(TW_ERR_INVALID_INPUT, "null argument");
-  if (m < 1 || m > INT32_MAX) return fail(TW_ERR_INVALID_INPUT, "m must be in [1, 2^31)");
-  if (ld_at < m || ld_at % 8 != 0)
-    return fail(TW_ERR_INVALID_INPUT, "ld_at (%lld) must be >= m and a multiple of 8",
-                (long long)ld_at);
-  if (reinterpret_cast<uintptr_t>(at) % 16 != 0)
-    return fail(TW_ERR_INVALID_INPUT, "A^T base must be 16-byte aligned");
-  if (ld_ct < m) return fail(TW_ERR_INVALID_INPUT, "ld_ct must be >= m");
-  if (out_dtype != kF32 && out_dtype != kF16 && out_dtype != kBF16)
-    return fail(TW_ERR_INVALID_INPUT, "unknown output dtype %d", out_dtype);
+int tw_plan_input_map(const tw_plan* p, int32_t* out) {
+  if (!p || !out) return fail(TW_ERR_INVALID_INPUT, "null argument");
+  std::copy(p->layout.src.begin(), p->layout.src.end(), out);
   return TW_OK;
 }
 
-static int run_tw(const tw_plan* p, const void* at, int64_t m, int64_t ld_at, void* ct,
+static int check_dtype(int32_t d) {
+  if (d != kF32 && d != kF16 && d != kBF16)
+    return fail(TW_ERR_INVALID_INPUT, "unknown dtype %d", d);
+  return TW_OK;
+}
+
+int tw_prepare_input(const tw_plan* p, const void* src, int32_t src_dtype, int32_t src_layout,
+                     int64_t m, int64_t ld_src, void* x, int64_t ld_x, void* stream) {
+  g_last_error.clear();
+  if (!p || !src || !x) return fail(TW_ERR_INVALID_INPUT, "null argument");
+  if (int st = check_dtype(src_dtype)) return st;
+  if (src_layout != TW_LAYOUT_MK && src_layout != TW_LAYOUT_KM)
+    return fail(TW_ERR_INVALID_INPUT, "unknown source layout %d", src_layout);
+  if (m < 1) return fail(TW_ERR_INVALID_INPUT, "m must be >= 1");
+  if (ld_src < (src_layout == TW_LAYOUT_MK ? p->k : m))
+    return fail(TW_ERR_INVALID_INPUT, "ld_src too small");
+  if (ld_x < m) return fail(TW_ERR_INVALID_INPUT, "ld_x must be >= m");
+  PrepArgs a{};
+  a.src = src;
+  a.src_dtype = src_dtype;
+  a.src_km = src_layout == TW_LAYOUT_KM ? 1 : 0;
+  a.ld_src = ld_src;
+  a.M = m;
+  a.K = p->k;
+  a.dst = x;
+  a.dst_dtype = p->dtype;
+  a.ld_dst = ld_x;
+  a.csr_ptr = p->d_prep_ptr;
+  a.csr_rows = p->d_prep_rows;
+  a.zero_rows = p->d_prep_zero;
+  a.n_zero = p->n_prep_zero;
+  TW_CUDA(launch_prepare_input(a, static_cast<cudaStream_t>(stream)));
+  return TW_OK;
+}
+
+static int check_io(const tw_plan* p, const void* x, int64_t m, int64_t ld_x, const void* ct,
+                    int64_t ld_ct, int32_t out_dtype) {
+  if (!p || !x || !ct) return fail(TW_ERR_INVALID_INPUT, "null argument");
+  if (m < 1 || m > INT32_MAX) return fail(TW_ERR_INVALID_INPUT, "m must be in [1, 2^31)");
+  if (ld_x < m || ld_x % 8 != 0)
+    return fail(TW_ERR_INVALID_INPUT, "ld_x (%lld) must be >= m and a multiple of 8",
+                (long long)ld_x);
+  if (reinterpret_cast<uintptr_t>(x) % 16 != 0)
+    return fail(TW_ERR_INVALID_INPUT, "input base must be 16-byte aligned");
+  if (ld_ct < m) return fail(TW_ERR_INVALID_INPUT, "ld_ct must be >= m");
+  return check_dtype(out_dtype);
+}
+
+static int run_tw(const tw_plan* p, const void* x, int64_t m, int64_t ld_x, void* ct,
                   int64_t ld_ct, int32_t out_dtype, const int32_t* rowmap, int64_t out_rows,
                   cudaStream_t s) {
-  CUtensorMap map_at;
-  if (int st = make_map_2d(&map_at, at, p->dtype, (uint64_t)m, (uint64_t)p->k, (uint64_t)ld_at,
-                           64, 1))
+  const uint64_t R = (uint64_t)p->input_rows();
+  CUtensorMap map_x, map_x8;
+  if (int st = make_map_2d(&map_x, x, p->dtype, (uint64_t)m, R, (uint64_t)ld_x, 64, kBK))
+    return st;
+  if (int st = make_map_2d(&map_x8, x, p->dtype, (uint64_t)m, R, (uint64_t)ld_x, 64, kRunAlign))
     return st;
   GemmArgs a{};
-  a.rowidx = p->d_rowidx;
   a.subtiles = p->d_subtiles;
+  a.runs = p->d_runs;
   a.rowmap = rowmap;
   a.out = ct;
   a.ld_out = ld_ct;
   a.out_dtype = out_dtype;
   a.M = (int32_t)m;
-  a.Kp = p->kp;
   a.n_sub = p->n_sub;
-  a.n_mblk = (int32_t)((m + kBM - 1) / kBM);
+  a.n_mblk = (int32_t)((m + kTN - 1) / kTN);
   a.n_units = a.n_sub * a.n_mblk;
-  a.K = p->k;
   a.flags = env_int("TW_DEBUG_FLAGS", 0);
   a.trace = g_trace;
   const int esz = out_dtype == kF32 ? 4 : 2;
   a.vec_ok = ((ld_ct * esz) % 16 == 0 && reinterpret_cast<uintptr_t>(ct) % 16 == 0) ? 1 : 0;
-  const int mode = env_int("TW_GATHER", kGatherCpAsync);
-  // condensed output: whole 32-column chunks leave through TMA 2-D stores
+  // condensed output: 32 x 32 blocks leave through TMA 2-D stores
   CUtensorMap map_out;
   std::memset(&map_out, 0, sizeof(map_out));
   a.use_tma_store = 0;
   if (a.vec_ok && rowmap == nullptr && !env_int("TW_NO_TMA_STORE", 0)) {
     if (make_map_2d(&map_out, ct, out_dtype, (uint64_t)m, (uint64_t)out_rows, (uint64_t)ld_ct,
-                    32, 32, /*swizzle128=*/false) == TW_OK)
+                    32, 32, esz == 4 ? 128 : 64) == TW_OK)
       a.use_tma_store = 1;
     g_last_error.clear();
   }
-  // Work split: whole units when they fit in one wave, else stream-K with
+  // Work split: whole units strided over the CTAs, or (opt-in) stream-K with
   // equal stage ranges (each range must hold the longest unit so a unit is
   // split at most once).
   int grid = std::min(a.n_units, p->sm_count);
@@ -487,31 +680,30 @@ static int run_tw(const tw_plan* p, const void* at, int64_t m, int64_t ld_at, vo
     grid = std::max(grid, 1);
     a.split = 1;
   }
-  TW_CUDA(launch_tw_gather_gemm(map_at, p->map_pay, map_out, a, at, ld_at, p->bn, p->dtype, mode,
-                                grid, s));
+  TW_CUDA(launch_tw_gemm(map_x, map_x8, p->map_pay, map_out, a, p->dtype, grid, s));
   return TW_OK;
 }
 
-int tw_gemm(const tw_plan* p, const void* at, int64_t m, int64_t ld_at, void* ct, int64_t ld_ct,
+int tw_gemm(const tw_plan* p, const void* x, int64_t m, int64_t ld_x, void* ct, int64_t ld_ct,
             int32_t out_dtype, void* stream) {
   g_last_error.clear();
-  if (int st = check_io(p, at, m, ld_at, ct, ld_ct, out_dtype)) return st;
-  return run_tw(p, at, m, ld_at, ct, ld_ct, out_dtype, nullptr, p->n_cond,
+  if (int st = check_io(p, x, m, ld_x, ct, ld_ct, out_dtype)) return st;
+  return run_tw(p, x, m, ld_x, ct, ld_ct, out_dtype, nullptr, p->n_cond,
                 static_cast<cudaStream_t>(stream));
 }
 
-int tw_gemm_tew(const tw_plan* p, const void* at, int64_t m, int64_t ld_at, void* ct,
+int tw_gemm_tew(const tw_plan* p, const void* x, int64_t m, int64_t ld_x, void* ct,
                 int64_t ld_ct, int32_t out_dtype, void* stream) {
   g_last_error.clear();
-  if (int st = check_io(p, at, m, ld_at, ct, ld_ct, out_dtype)) return st;
+  if (int st = check_io(p, x, m, ld_x, ct, ld_ct, out_dtype)) return st;
   if (!p->has_overlay) return fail(TW_ERR_INVALID_INPUT, "plan has no overlay attached");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (int st = run_tw(p, at, m, ld_at, ct, ld_ct, out_dtype, p->d_union_rowmap,
+  if (int st = run_tw(p, x, m, ld_x, ct, ld_ct, out_dtype, p->d_union_rowmap,
                       (int64_t)p->union_cols.size(), s))
     return st;
   ResidualArgs r{};
-  r.at = at;
-  r.ld_at = ld_at;
+  r.at = x;
+  r.ld_at = ld_x;
   r.in_dtype = p->dtype;
   r.col_start = p->d_ov_start;
   r.rows = p->d_ov_rows;
@@ -533,9 +725,8 @@ int tw_transpose_cast(const void* a, int32_t a_dtype, int64_t m, int64_t k, int6
   if (!a || !at) return fail(TW_ERR_INVALID_INPUT, "null argument");
   if (m < 1 || k < 1 || lda < k || ld_at < m)
     return fail(TW_ERR_INVALID_INPUT, "bad transpose geometry");
-  for (int32_t d : {a_dtype, at_dtype})
-    if (d != kF32 && d != kF16 && d != kBF16)
-      return fail(TW_ERR_INVALID_INPUT, "unknown dtype %d", d);
+  if (int st = check_dtype(a_dtype)) return st;
+  if (int st = check_dtype(at_dtype)) return st;
   TW_CUDA(launch_transpose_cast(a, a_dtype, m, k, lda, at, at_dtype, ld_at,
                                 static_cast<cudaStream_t>(stream)));
   return TW_OK;

@@ -151,20 +151,83 @@ class TwPlan:
         macs = self.info.kept_macs_per_token if tew else self.info.kept_macs_per_token - self.info.nnz
         return 2 * int(m) * int(macs)
 
-    # -- launches -------------------------------------------------------
-    def _check_at(self, at):
+    # -- input layout -----------------------------------------------------
+    @property
+    def input_rows(self) -> int:
+        """Rows of the grouped input layout X the GEMM reads (see tw_gemm.h)."""
+        return int(self.info.input_rows)
+
+    def input_map(self) -> np.ndarray:
+        """Original K row held by each row of X (-1 for zero rows)."""
+        lib = _native.load_library()
+        out = np.empty(self.input_rows, dtype=np.int32)
+        _native.check(lib.tw_plan_input_map(self._handle, _native.ptr(out, _native.ctypes.c_int32)))
+        return out
+
+    def prepare(self, a=None, *, at=None, out=None, stream=None):
+        """Build the grouped input X (input_rows x M, compute dtype) on the GPU.
+
+        ``a`` is the reference-layout activation matrix (M x K: numpy, nested
+        list, CPU or CUDA tensor); alternatively ``at`` is a CUDA A^T (K x M).
+        The row copy / transpose / cast runs in the K4g kernel.  The token
+        pitch is padded to a multiple of 8 so the TMA descriptors are legal.
+        """
         torch = _torch()
-        if not isinstance(at, torch.Tensor) or not at.is_cuda:
-            raise InvalidInputError("A^T must be a CUDA tensor (use prepare_activations)")
-        if at.dim() != 2 or at.shape[0] != self.original_dims[0]:
+        k = self.original_dims[0]
+        if (a is None) == (at is None):
+            raise InvalidInputError("pass exactly one of a (M x K) or at (K x M)")
+        if at is not None:
+            if not isinstance(at, torch.Tensor) or not at.is_cuda or at.dim() != 2:
+                raise InvalidInputError("at must be a 2-D CUDA tensor (K x M)")
+            if at.shape[0] != k:
+                raise InvalidInputError(f"inner dims disagree: at has {at.shape[0]} rows, "
+                                        f"weights have K={k}")
+            src, layout = at, _native.TW_LAYOUT_KM
+            m = int(at.shape[1])
+        else:
+            if isinstance(a, torch.Tensor):
+                if a.dim() != 2 or a.shape[0] < 1 or a.shape[1] < 1:
+                    raise InvalidInputError(
+                        f"matrix must be 2-D with dims >= 1, got {tuple(a.shape)}")
+                src = a if a.is_cuda else a.to(f"cuda:{self.device}", non_blocking=True)
+            else:
+                src = torch.from_numpy(as_matrix(a)).to(f"cuda:{self.device}")
+            if src.shape[1] != k:
+                raise InvalidInputError(f"inner dims disagree: a has {src.shape[1]} cols, "
+                                        f"weights have K={k}")
+            layout = _native.TW_LAYOUT_MK
+            m = int(src.shape[0])
+        if src.dtype not in (torch.float32, torch.float16, torch.bfloat16):
+            src = src.float()
+        if src.stride(1) != 1:
+            src = src.contiguous()
+        ld = (m + 7) // 8 * 8
+        if out is None:
+            out = torch.empty((self.input_rows, ld), dtype=_torch_dtype(self.compute_dtype),
+                              device=src.device)
+        elif out.shape[0] != self.input_rows or out.stride(1) != 1 or out.stride(0) < m:
+            raise InvalidInputError("out must be input_rows x (>= M) with unit token stride")
+        lib = _native.load_library()
+        _native.check(lib.tw_prepare_input(self._handle, src.data_ptr(),
+                                           _DTYPE_CODES[_dtype_name(src.dtype)], layout, m,
+                                           src.stride(0), out.data_ptr(), out.stride(0),
+                                           _native.stream_handle(stream)))
+        return out[:, :m]
+
+    # -- launches -------------------------------------------------------
+    def _check_x(self, x):
+        torch = _torch()
+        if not isinstance(x, torch.Tensor) or not x.is_cuda:
+            raise InvalidInputError("x must be the CUDA grouped input from TwPlan.prepare()")
+        if x.dim() != 2 or x.shape[0] != self.input_rows:
             raise InvalidInputError(
-                f"A^T must be K x M with K={self.original_dims[0]}, got {tuple(at.shape)}")
-        if at.dtype != _torch_dtype(self.compute_dtype):
-            raise InvalidInputError(f"A^T dtype {at.dtype} != plan compute dtype "
+                f"x must be input_rows x M = {self.input_rows} x M, got {tuple(x.shape)}")
+        if x.dtype != _torch_dtype(self.compute_dtype):
+            raise InvalidInputError(f"x dtype {x.dtype} != plan compute dtype "
                                     f"{self.compute_dtype}")
-        if at.stride(1) != 1:
-            raise InvalidInputError("A^T must have unit stride along tokens")
-        return int(at.shape[1]), int(at.stride(0))
+        if x.stride(1) != 1:
+            raise InvalidInputError("x must have unit stride along tokens")
+        return int(x.shape[1]), int(x.stride(0))
 
     def _out(self, rows: int, m: int, out, out_dtype):
         torch = _torch()
@@ -175,24 +238,24 @@ class TwPlan:
             raise InvalidInputError("out must be a (rows x M) CUDA tensor with unit token stride")
         return out
 
-    def run(self, at, out=None, out_dtype="fp32", stream=None):
-        """C'^T (N' x M) = TW product of A^T (K x M); K1 only."""
-        m, ld_at = self._check_at(at)
+    def run(self, x, out=None, out_dtype="fp32", stream=None):
+        """C'^T (N' x M) = TW product of the grouped input x; K1 only."""
+        m, ld = self._check_x(x)
         ct = self._out(self.info.n_condensed, m, out, out_dtype)
         lib = _native.load_library()
-        _native.check(lib.tw_gemm(self._handle, at.data_ptr(), m, ld_at, ct.data_ptr(),
+        _native.check(lib.tw_gemm(self._handle, x.data_ptr(), m, ld, ct.data_ptr(),
                                   ct.stride(0), _DTYPE_CODES[_dtype_name(ct.dtype)],
                                   _native.stream_handle(stream)))
         return ct
 
-    def run_tew(self, at, out=None, out_dtype="fp32", stream=None):
+    def run_tew(self, x, out=None, out_dtype="fp32", stream=None):
         """C^T over the union columns (|union| x M) = TW + overlay; K1 + K2."""
         if not self.has_overlay:
             raise InvalidInputError("plan has no overlay attached")
-        m, ld_at = self._check_at(at)
+        m, ld = self._check_x(x)
         ct = self._out(self.info.n_union, m, out, out_dtype)
         lib = _native.load_library()
-        _native.check(lib.tw_gemm_tew(self._handle, at.data_ptr(), m, ld_at, ct.data_ptr(),
+        _native.check(lib.tw_gemm_tew(self._handle, x.data_ptr(), m, ld, ct.data_ptr(),
                                       ct.stride(0), _DTYPE_CODES[_dtype_name(ct.dtype)],
                                       _native.stream_handle(stream)))
         return ct
@@ -348,20 +411,21 @@ def schedule_tiles(per_tile_macs: List[int], workers: int, strategy: str = "lpt"
     return out
 
 
-def _activations(a, k: int, compute_dtype: str):
+def _activations(a, plan: "TwPlan"):
+    """Reference-layout activations -> the plan's grouped input on the GPU."""
     torch = _torch()
+    k = plan.original_dims[0]
     m_k = tuple(a.shape) if isinstance(a, torch.Tensor) else as_matrix(a).shape
     if len(m_k) != 2 or m_k[1] != k:
         raise InvalidInputError(f"inner dims disagree: a has {m_k[-1]} cols, weights have K={k}")
-    return prepare_activations(a, compute_dtype)
+    return plan.prepare(a)
 
 
 def gemm_tile_sparse(a, b: TileSparseMatrix, *, compute_dtype: str = "fp16",
                      out_dtype: str = "fp32") -> GemmOutput:
     """Per-tile gather + GEMM over every tile; output condensed to N'."""
-    at = _activations(a, b.original_dims[0], compute_dtype)
     plan = plan_for(b, compute_dtype=compute_dtype)
-    ct = plan.run(at, out_dtype=out_dtype)
+    ct = plan.run(_activations(a, plan), out_dtype=out_dtype)
     return GemmOutput(condensed=ct.t(), column_map=b.column_mask)
 
 
@@ -374,9 +438,8 @@ def gemm_cto(a, c: CtoEncoding, check_padding: bool = False, *, compute_dtype: s
     entries, so padded offsets are never dereferenced; ``check_padding`` is
     accepted for signature compatibility.
     """
-    at = _activations(a, c.original_dims[0], compute_dtype)
     plan = plan_for(c, compute_dtype=compute_dtype)
-    ct = plan.run(at, out_dtype=out_dtype)
+    ct = plan.run(_activations(a, plan), out_dtype=out_dtype)
     return GemmOutput(condensed=ct.t(), column_map=IndexMask(c.original_dims[1],
                                                              plan.condensed_columns))
 
@@ -390,10 +453,10 @@ def execute_batched(a, b: TileSparseMatrix, workers: int, strategy: str = "lpt",
     ``workers`` lanes so accounting matches executor.py:241-265."""
     macs_per_token = [t.width * t.kept_rows.n_kept for t in b.tiles]
     assignment = schedule_tiles(macs_per_token, workers, strategy)
-    at = _activations(a, b.original_dims[0], compute_dtype)
-    m = int(at.shape[1])
     plan = plan_for(b, compute_dtype=compute_dtype, schedule=strategy)
-    ct = plan.run(at, out_dtype=out_dtype)
+    x = _activations(a, plan)
+    m = int(x.shape[1])
+    ct = plan.run(x, out_dtype=out_dtype)
     per_tile = [m * v for v in macs_per_token]
     per_worker = [0] * workers
     for i, w in enumerate(assignment):
@@ -413,9 +476,8 @@ def gemm_tew(a, b: TileSparseMatrix, ov: SparseOverlay,
     if tuple(ov.dims) != tuple(b.original_dims):
         raise InvalidInputError(f"overlay dims {tuple(ov.dims)} do not match weights "
                                 f"{tuple(b.original_dims)}")
-    at = _activations(a, b.original_dims[0], compute_dtype)
     plan = plan_for(b, overlay=ov, compute_dtype=compute_dtype)
-    ct = plan.run_tew(at, out_dtype=out_dtype)
+    ct = plan.run_tew(_activations(a, plan), out_dtype=out_dtype)
     return GemmOutput(condensed=ct.t(), column_map=IndexMask(b.original_dims[1],
                                                              plan.union_columns))
 

@@ -36,7 +36,7 @@ def main():
         _, tsm = tw.prune_tw(w, 0.75, args.g)
         plans.append([tw.TwPlan(tw.encode_cto(tsm)) for _ in range(4)])
         a = tw.round_to(tw.synthetic_matrix(0, args.m, k, 1), "fp16")
-        ats.append([tw.prepare_activations(torch.from_numpy(a).cuda()) for _ in range(4)])
+        ats.append([pl.prepare(torch.from_numpy(a).cuda()) for pl in plans[-1]])
         outs.append([torch.empty((tsm.n_condensed, args.m), dtype=torch.float16, device="cuda")
                      for _ in range(4)])
     ref = [plans[i][0].run(ats[i][0]).float() for i in range(3)]

@@ -31,7 +31,7 @@ def main():
     _, tsm = tw.prune_tw(w, 0.75, 128)
     plan = tw.TwPlan(tw.encode_cto(tsm))
     a = tw.round_to(tw.synthetic_matrix(0, args.m, k, 1), "fp16")
-    at = tw.prepare_activations(torch.from_numpy(a).cuda())
+    at = plan.prepare(torch.from_numpy(a).cuda())
     out = torch.empty((tsm.n_condensed, args.m), dtype=torch.float16, device="cuda")
     for _ in range(3):
         plan.run(at, out=out)
@@ -65,6 +65,12 @@ def main():
                   "epi " + ", ".join(f"[{a0 - t0}, {a1 - t0}]" for a0, a1 in e))
     q = lambda v: np.percentile(v, [10, 50, 90, 100]).astype(int).tolist() if len(v) else []
     print(" last-full p10/50/90/max", q(full_ts))
+    g0 = t[:, 3074][t[:, 3074] > 0]
+    g1 = t[:, 3075][t[:, 3075] > 0]
+    if len(g0) and len(g1):
+        print(f" globaltimer: CTA starts spread {int(g0.max() - g0.min())} ns, "
+              f"first start -> last epilogue end {int(g1.max() - g0.min())} ns, "
+              f"median CTA body {int(np.median(g1 - g0[:len(g1)]))} ns")
     print(" cta end (last epilogue) p10/50/90/max", q(ends))
     print(" epilogue per segment p10/50/90/max", q(epi))
 

@@ -136,6 +136,60 @@ __global__ void gather_hybrid(const __grid_constant__ CUtensorMap map, const __h
   if (tid == 0) cycles[blockIdx.x] = clock64() - t0;
 }
 
+// Decoupled hybrid: warps [0, cw) run an independent cp.async gather ring in
+// smem half 0; lane 0 of warps [cw, cw+tw) run an independent gather4 ring in
+// smem half 1.  Reports combined bytes.
+__global__ void gather_hybrid2(const __grid_constant__ CUtensorMap map, const __half* at, int64_t ld,
+                               const int* rows, int nrows, int M, int iters, int cw, int tw_,
+                               long long* cycles) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t bar[4];
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    for (int s = 0; s < 4; ++s) mbar_init(&bar[s], 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  long long t0 = clock64();
+  const int warp = tid >> 5, lane = tid & 31;
+  if (warp < cw) {
+    for (int it = 0; it < iters; ++it) {
+      const int stage = it % 4;
+      const int kb = (it * 64 + blockIdx.x * 64) % (nrows - 64);
+      const int m0 = ((it + blockIdx.x) * 128) % M;
+      const uint32_t base = smem_u32(smem + stage * kStageBytes);
+      for (int c = tid; c < 1024; c += 32 * cw) {
+        const int r = c >> 4, j = c & 15;
+        const int row = rows[kb + r];
+        const uint32_t dst = base + (j >> 3) * 8192 + r * 128 + (((j & 7) ^ (r & 7)) << 4);
+        cp_async_16(dst, at + (int64_t)row * ld + m0 + j * 8, 16);
+      }
+      asm volatile("cp.async.commit_group;");
+      asm volatile("cp.async.wait_group 2;");
+    }
+    asm volatile("cp.async.wait_group 0;");
+  } else if (warp < cw + tw_ && lane == 0) {
+    const int w = warp - cw;
+    const int per = 32 / tw_;
+    for (int it = 0; it < iters + 4; ++it) {
+      const int stage = it % 4;
+      if (it >= 4) mbar_wait(&bar[stage], ((it / 4) - 1) & 1);
+      if (it >= iters) continue;
+      if (w == 0) mbar_arrive_expect_tx(&bar[stage], kStageBytes);
+      const int kb = (it * 64 + blockIdx.x * 64 + 777) % (nrows - 64);
+      const int m0 = ((it + blockIdx.x + 3) * 128) % M;
+      for (int g = w * per; g < (w + 1) * per; ++g) {
+        const int half = g >> 4, r4 = (g & 15) * 4;
+        const int* rr = rows + kb + r4;
+        tma_gather4(smem + (4 + stage) * kStageBytes + half * 8192 + r4 * 128, &map, &bar[stage],
+                    m0 + half * 64, rr[0], rr[1], rr[2], rr[3]);
+      }
+    }
+  }
+  __syncthreads();
+  if (tid == 0) cycles[blockIdx.x] = clock64() - t0;
+}
+
 __global__ void dense_tma(const __grid_constant__ CUtensorMap map, int nrows, int M, int iters,
                           long long* cycles) {
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -235,6 +289,25 @@ int main() {
     char name[64];
     snprintf(name, 64, "tma gather4 %d issuers", issuers);
     report(name);
+  }
+  CK(cudaFuncSetAttribute(gather_hybrid2, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  for (int tw_ : {4, 8, 16}) {
+    for (int cw : {8, 16}) {
+      for (int rep = 0; rep < 2; ++rep) {
+        cudaEventRecord(e0);
+        gather_hybrid2<<<grid, 32 * (tw_ + cw), smem>>>(gmap, at, M, drows, nrows, M, iters, cw, tw_, cyc);
+        cudaEventRecord(e1);
+        CK(cudaDeviceSynchronize());
+      }
+      // both rings move iters stages each: report 2x bytes
+      std::vector<long long> c(grid);
+      CK(cudaMemcpy(c.data(), cyc, grid * 8, cudaMemcpyDeviceToHost));
+      std::sort(c.begin(), c.end());
+      float ms;
+      cudaEventElapsedTime(&ms, e0, e1);
+      printf("hybrid2 tma %2d + cp %2d warps  %8.1f GB/s  %6.1f B/cyc/SM\n", tw_, cw,
+             2.0 * grid * iters * kStageBytes / ms / 1e6, 2.0 * iters * kStageBytes / c[grid / 2]);
+    }
   }
   for (int tw_ : {2, 4, 8}) {
     for (int cw : {4, 8}) {

@@ -12,7 +12,7 @@ w = tw.round_to(tw.synthetic_matrix(0, k, n, 0), "fp16")
 _, tsm = tw.prune_tw(w, 0.75, 128)
 plan = tw.TwPlan(tw.encode_cto(tsm))
 a = tw.round_to(tw.synthetic_matrix(0, 8192, k, 1), "fp16")
-at = tw.prepare_activations(torch.from_numpy(a).cuda())
+at = plan.prepare(torch.from_numpy(a).cuda())
 out = torch.empty((tsm.n_condensed, 8192), dtype=torch.float16, device="cuda")
 ref = plan.run(at).float()
 torch.cuda.synchronize()

@@ -53,11 +53,17 @@ def _worker(rank, world, port, mode, results):
             full_t = D.gather_rows(local, rows)
             results[rank] = full_t.numpy().T.copy()
         else:
-            lo, hi = D.token_slice(a.shape[0], world, rank)
+            m = a.shape[0]
+            spans = [D.token_slice(m, world, r) for r in range(world)]
+            lo, hi = spans[rank]
             local = torch.from_numpy(orc.c_gemm_cto_enc(a[lo:hi], enc))
-            out = [torch.empty(0)] * world
-            dist.all_gather_object(out, (lo, hi, local.numpy()))
-            results[rank] = np.concatenate([o[2] for o in sorted(out, key=lambda t: t[0])])
+            tallest = max(h - l for l, h in spans)
+            pad = torch.zeros((tallest, local.shape[1]), dtype=local.dtype)
+            pad[:hi - lo] = local
+            bufs = [torch.empty_like(pad) for _ in range(world)]
+            dist.all_gather(bufs, pad)
+            results[rank] = np.concatenate([bufs[r][:h - l].numpy()
+                                            for r, (l, h) in enumerate(spans)])
     finally:
         dist.destroy_process_group()
 

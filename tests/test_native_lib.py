@@ -44,18 +44,19 @@ def test_library_exports_every_declared_symbol(lib):
 
 
 def test_abi_version(lib):
-    assert lib.tw_abi_version() == 100
+    assert lib.tw_abi_version() == 200
 
 
 def test_sass_is_blackwell_native():
-    """tcgen05 MMA, TMEM loads and TMA gather4 are in the shipped binary."""
+    """tcgen05 MMA, TMEM loads, TMA tile loads and TMA stores are in the shipped binary."""
     out = subprocess.run(["cuobjdump", "-sass", str(_native.LIB_PATH)], capture_output=True,
                          text=True)
     if out.returncode != 0:
         pytest.skip("cuobjdump unavailable")
     sass = out.stdout
     assert "UTCHMMA" in sass
-    assert "UTMALDG.2D.GATHER4" in sass
+    assert "UTMALDG.2D" in sass
+    assert "UTMASTG.2D" in sass
     assert "LDTM" in sass
 
 
