@@ -15,12 +15,18 @@ value        effective TFLOP/s = surviving FLOPs (metrics.report.sparse_flops,
              every step streams cold activations, weights and outputs.  Each
              step is one CUDA-graph replay of the three layer launches (the
              dense cuBLAS arm is graph-captured the same way).
+             Activations are resident as A^T (K x M, tokens contiguous): the
+             layout K1 reads and writes (a TW layer's C'^T output is the next
+             layer's A^T); the cuBLAS arm reads the same A^T buffers.
+transpose    A (M x K row-major, device) -> A^T (K4, tw_transpose_cast) per
+             step, reported beside value for callers holding row-major
+             activations (value_incl_transpose).
 e2e          same metric through the public API (TwPlan.prepare + TwPlan.run)
              from pinned HOST fp16 activations (M x K, the reference's layout),
-             with the H2D copies, the A -> grouped-input kernel (K4g), the
-             GEMM and the D2H copy of the fp16 result inside the timed region.
+             with the H2D copies, the A -> A^T kernel (K4), the GEMM and the
+             D2H copy of the fp16 result inside the timed region.
 cublas       dense torch.matmul (cuBLAS) at the same shapes and layout.
-roofline     K1 (tw_gather_gemm) launches timed per layer with CUDA events;
+roofline     K1 (tw_gemm_kernel) launches timed per layer with CUDA events;
              achieved = algorithmic bytes / launch time vs the
              measured HBM peak (the step is HBM-bound: AI 188 < ridge 240).
 cpu_baseline the reference algorithm (oracle port of execute_batched,
@@ -375,13 +381,13 @@ def run_ours(args, cfg, rank: int, world: int) -> None:
     dense_flops = sum(2 * m * L["k"] * L["n"] for L in layers)
     del dense, dense_graphs
 
-    # ---- layout prep: A (M x K, fp16, device) -> each plan's grouped input
+    # ---- row-major callers: A (M x K, fp16, device) -> A^T per layer (K4)
     a_dev = [torch.from_numpy(activations(cfg, L["k"], li, rank)).to(dev, torch.float16)
              for li, L in enumerate(layers)]
 
     def prep_set(r: int):
-        for li, (plan, x, _) in enumerate(sets[r]):
-            plan.prepare(a_dev[li], out=x.as_strided((x.shape[0], x.stride(0)), (x.stride(0), 1)))
+        for li, (plan, at, _) in enumerate(sets[r]):
+            tw.prepare_activations(a_dev[li], plan.compute_dtype, out=at)
 
     prep_graphs = [capture_graph(lambda r=r: prep_set(r)) for r in range(N_ROTATE)]
     p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -450,7 +456,7 @@ def run_ours(args, cfg, rank: int, world: int) -> None:
         tf = flops_step / (tot_us * 1e-6) / 1e12
         roofline = {"bound": "tensor", "achieved": tf, "peak": pk["tc"], "unit": "TFLOP/s",
                     "frac": tf / pk["tc"], "traffic": traffic}
-    roofline.update({"kernel": "tw_gather_gemm" + ("+tw_residual" if tew else ""),
+    roofline.update({"kernel": "tw_gemm_kernel" + ("+tw_residual_kernel" if tew else ""),
                      "peak_source": pk["source"], "arithmetic_intensity": ai,
                      "layers": per_layer})
 
@@ -468,18 +474,18 @@ def run_ours(args, cfg, rank: int, world: int) -> None:
                    "parallelism": f"dp{world} (M-split, no collective)",
                    "l2": f"{N_ROTATE} rotating buffer sets (weights, A^T, C^T) > 2x L2"},
         "speedup_vs_cublas": dense_ms / ms_step,
-        "prep": {"ms_per_step": prep_ms,
-                 "what": "A (M x K fp16, device) -> grouped input X per layer (tw_prepare_input); "
-                         "not in value (a network's previous epilogue writes X directly), "
-                         "inside e2e",
-                 "value_incl_prep": world * flops_step / ((ms_step + prep_ms) * 1e-3) / 1e12,
-                 "speedup_vs_cublas_incl_prep": dense_ms / (ms_step + prep_ms)},
+        "transpose": {"ms_per_step": prep_ms,
+                 "what": "A (M x K fp16, device, row-major) -> A^T per layer (tw_transpose_cast); "
+                         "only for row-major callers (a TW layer's C'^T output is already the "
+                         "next layer's A^T); inside e2e",
+                 "value_incl_transpose": world * flops_step / ((ms_step + prep_ms) * 1e-3) / 1e12,
+                 "speedup_vs_cublas_incl_transpose": dense_ms / (ms_step + prep_ms)},
         "cublas": {"ms_per_step": dense_ms,
                    "tflops_dense": world * dense_flops / (dense_ms * 1e-3) / 1e12},
         "frac_of_dense_peak": value / world / pk["tc"],
         "e2e": {"value": e2e_value, "unit": "TFLOP/s", "ms_per_step": e2e_ms,
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "path": "pinned host fp16 A (M x K) -> H2D -> tw_prepare_input -> tw_gemm -> D2H fp16"},
+                "path": "pinned host fp16 A (M x K) -> H2D -> tw_transpose_cast -> tw_gemm -> D2H fp16"},
         "roofline": roofline,
         "cpu_baseline": {"value": cpu_rate, "unit": "TFLOP/s", "cores": workers, "kind": "port",
                          "sample": f"{m_sample} of {m} tokens through every layer "

@@ -11,13 +11,12 @@
  * Conventions
  *   - Plain C types only: host pointers for weights/encodings, device
  *     pointers for activations/outputs, cudaStream_t passed as void*.
- *   - Activations enter the GEMM in the plan's grouped input layout X:
- *     input_rows rows x M tokens, tokens contiguous, pitch ld_x (ld_x % 8 ==
- *     0, 16-byte aligned).  Row j of X is a copy of original K row
- *     tw_plan_input_map()[j] (or zero); tiles' kept rows form contiguous runs
- *     of X so they load with TMA 2-D tiles.  tw_prepare_input builds X from A
- *     (m x k) or A^T (k x m).  Outputs are C'^T: one row per output column,
- *     tokens contiguous, pitch ld_ct.
+ *   - Activations enter the GEMM as A^T: k rows x m tokens, tokens
+ *     contiguous, pitch ld_at (ld_at % 8 == 0, 16-byte aligned base), in the
+ *     plan's compute dtype -- the layout the GEMM itself writes (C'^T), so a
+ *     layer's output feeds the next layer without a copy.  tw_transpose_cast
+ *     converts a row-major A (m x k, any dtype).  Outputs are C'^T: one row
+ *     per output column, tokens contiguous, pitch ld_ct.
  *   - Stream-ordered, no host synchronisation inside tw_gemm / tw_gemm_tew /
  *     tw_transpose_cast, so they are CUDA-graph capturable.
  *   - Every function returns a status code; tw_last_error() gives the
@@ -52,11 +51,7 @@ extern "C" {
 #define TW_F16 1
 #define TW_BF16 2
 
-/* Activation source layouts for tw_prepare_input. */
-#define TW_LAYOUT_MK 0   /* A   : m x k, row-major (the reference's carrier)  */
-#define TW_LAYOUT_KM 1   /* A^T : k x m, tokens contiguous                    */
-
-/* Sub-tile visiting order inside each 128-token block
+/* Sub-tile visiting order inside each token block
  * (executor.py:206-227 schedule_tiles strategies). */
 #define TW_SCHEDULE_LPT 0          /* descending surviving K'             */
 #define TW_SCHEDULE_ROUND_ROBIN 1  /* tile order                          */
@@ -67,7 +62,7 @@ typedef struct tw_plan_info {
   int32_t k, n, g;            /* original dims and tile width            */
   int32_t n_tiles;            /* TW tiles                                */
   int32_t n_sub;              /* UMMA-N slices (== n_tiles when g <= 256) */
-  int32_t bn;                 /* UMMA N of the kernel instance           */
+  int32_t bn;                 /* output columns per sub-tile (UMMA M)    */
   int32_t kp;                 /* padded gather-list length               */
   int32_t n_condensed;        /* N' = sum of tile widths                 */
   int32_t n_union;            /* |TW cols U overlay cols| (TEW), else N' */
@@ -76,9 +71,6 @@ typedef struct tw_plan_info {
   int64_t kept_macs_per_token;/* sum_i width_i * K'_i (+ nnz for TEW)    */
   int32_t sm_count;           /* SMs of the plan's device                */
   int32_t has_overlay;
-  int64_t input_rows;         /* rows of the grouped input layout X      */
-  int32_t cluster;            /* tiles per row-grouping cluster          */
-  int32_t reserved;
 } tw_plan_info;
 
 /* Build a device plan from a CTO encoding held in host memory.
@@ -113,34 +105,22 @@ TW_API int tw_plan_get_info(const tw_plan* plan, tw_plan_info* info);
 TW_API int tw_plan_condensed_columns(const tw_plan* plan, int32_t* out_cols);
 TW_API int tw_plan_union_columns(const tw_plan* plan, int32_t* out_cols);
 
-/* Rows of the grouped input layout (host buffer sized info.input_rows):
- * original K row held by each row of X, -1 for zero rows. */
-TW_API int tw_plan_input_map(const tw_plan* plan, int32_t* out_rows);
-
-/* Build the grouped input X (input_rows x m, pitch ld_x, compute dtype) from
- * activations: src_layout TW_LAYOUT_MK (A, m x k, pitch ld_src) or
- * TW_LAYOUT_KM (A^T, k x m, pitch ld_src); src_dtype TW_F32/F16/BF16.
- * Replaces the float32 carrier copy of core.as_matrix (core.py:32-43) and the
- * per-tile column gather a64[:, rows] of executor.py:121-124, done once. */
-TW_API int tw_prepare_input(const tw_plan* plan, const void* src, int32_t src_dtype,
-                            int32_t src_layout, int64_t m, int64_t ld_src, void* x, int64_t ld_x,
-                            void* stream);
-
-/* TW product, condensed: ct[N' x M] = (A . W_tw)^T.
+/* TW product, condensed: ct[N' x m] = (A . W_tw)^T from at = A^T [k x m].
  * Replaces: executor.gemm_cto (executor.py:149-177), gemm_tile_sparse
  * (executor.py:135-146) and execute_batched (executor.py:230-265); all three
  * are bit-identical on the GPU as in the reference. */
-TW_API int tw_gemm(const tw_plan* plan, const void* x, int64_t m, int64_t ld_x, void* ct,
+TW_API int tw_gemm(const tw_plan* plan, const void* at, int64_t m, int64_t ld_at, void* ct,
                    int64_t ld_ct, int32_t out_dtype, void* stream);
 
 /* TEW product over the union columns: ct[|union| x M].
  * Replaces: executor.gemm_tew (executor.py:180-203). */
-TW_API int tw_gemm_tew(const tw_plan* plan, const void* x, int64_t m, int64_t ld_x, void* ct,
+TW_API int tw_gemm_tew(const tw_plan* plan, const void* at, int64_t m, int64_t ld_at, void* ct,
                        int64_t ld_ct, int32_t out_dtype, void* stream);
 
 /* A (m x k row-major, pitch lda, a_dtype) -> A^T (k x m, pitch ld_at, at_dtype).
  * Replaces the float32/float64 carrier copies of core.as_matrix
- * (core.py:32-43) and executor.py:158 on the device. */
+ * (core.py:32-43) and executor.py:158 on the device; the per-tile column
+ * gather a64[:, rows] of executor.py:121-124 happens inside tw_gemm. */
 TW_API int tw_transpose_cast(const void* a, int32_t a_dtype, int64_t m, int64_t k, int64_t lda,
                       void* at, int32_t at_dtype, int64_t ld_at, void* stream);
 

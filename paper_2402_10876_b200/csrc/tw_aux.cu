@@ -89,8 +89,8 @@ __global__ void transpose_cast_kernel(const void* a, int32_t a_dtype, int64_t M,
   }
 }
 
-// dst[(s*BN + c) * Kp + r] = payload of sub-tile s, column c, at the tile's
-// grouped sequence slot r (zero for padding slots and padded columns).
+// dst[(s*BN + c) * Kp + r] = payload of sub-tile s, column c, kept row r
+// (zero for padding slots r >= K'_i and padded columns c >= width).
 __global__ void build_payload_kernel(const PayloadArgs args) {
   const int s = blockIdx.y;
   const SubTile d = args.subtiles[s];
@@ -98,66 +98,14 @@ __global__ void build_payload_kernel(const PayloadArgs args) {
   const int64_t base = static_cast<int64_t>(d.pay_row) * args.Kp;
   const int64_t src0 = args.src_base[s];
   const int ld = args.src_ld[s];
-  const int32_t* pos = args.seq_pos + static_cast<int64_t>(d.idx_row) * args.Kp;
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < per;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int c = static_cast<int>(i / args.Kp);
     const int r = static_cast<int>(i - static_cast<int64_t>(c) * args.Kp);
-    const int p = pos[r];
     float v = 0.f;
-    if (c < d.width && p >= 0) v = args.src[src0 + static_cast<int64_t>(c) * ld + p];
+    if (c < d.width && r < ld) v = args.src[src0 + static_cast<int64_t>(c) * ld + r];
     store_from_float(args.dst, args.dst_dtype, base + i, v);
   }
-}
-
-// Grouped-input build from A (M x K): 32 source rows x 64 tokens per block,
-// coalesced read along K, smem transpose, then each source row's 64-token
-// segment goes to every grouped row that holds a copy of it.
-constexpr int kPrepRows = 32;
-constexpr int kPrepTok = 64;
-
-__global__ void prep_from_mk_kernel(const PrepArgs a) {
-  __shared__ float tile[kPrepRows][kPrepTok + 1];
-  const int64_t k0 = static_cast<int64_t>(blockIdx.x) * kPrepRows;
-  const int64_t t0 = static_cast<int64_t>(blockIdx.y) * kPrepTok;
-  const int tx = threadIdx.x;  // 0..31
-  for (int ty = threadIdx.y; ty < kPrepTok; ty += blockDim.y) {
-    const int64_t t = t0 + ty, k = k0 + tx;
-    tile[tx][ty] = (t < a.M && k < a.K) ? load_as_float(a.src, a.src_dtype, t * a.ld_src + k) : 0.f;
-  }
-  __syncthreads();
-  for (int kr = threadIdx.y; kr < kPrepRows; kr += blockDim.y) {
-    const int64_t k = k0 + kr;
-    if (k >= a.K) break;
-    const int lo = a.csr_ptr[k], hi = a.csr_ptr[k + 1];
-    for (int e = lo; e < hi; ++e) {
-      const int64_t row = a.csr_rows[e];
-      for (int j = tx; j < kPrepTok; j += 32) {
-        const int64_t t = t0 + j;
-        if (t < a.M) store_from_float(a.dst, a.dst_dtype, row * a.ld_dst + t, tile[kr][j]);
-      }
-    }
-  }
-}
-
-// Grouped-input build from A^T (K x M): one source row per blockIdx.y.
-__global__ void prep_from_km_kernel(const PrepArgs a) {
-  const int64_t k = blockIdx.y;
-  const int lo = a.csr_ptr[k], hi = a.csr_ptr[k + 1];
-  if (lo == hi) return;
-  for (int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < a.M;
-       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const float v = load_as_float(a.src, a.src_dtype, k * a.ld_src + t);
-    for (int e = lo; e < hi; ++e)
-      store_from_float(a.dst, a.dst_dtype, static_cast<int64_t>(a.csr_rows[e]) * a.ld_dst + t, v);
-  }
-}
-
-__global__ void prep_zero_kernel(const PrepArgs a) {
-  const int64_t row = a.zero_rows[blockIdx.y];
-  for (int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < a.ld_dst;
-       t += static_cast<int64_t>(gridDim.x) * blockDim.x)
-    store_from_float(a.dst, a.dst_dtype, row * a.ld_dst + t, 0.f);
 }
 
 }  // namespace
@@ -177,25 +125,6 @@ cudaError_t launch_transpose_cast(const void* a, int32_t a_dtype, int64_t M, int
   dim3 grid(static_cast<unsigned>((K + 31) / 32), static_cast<unsigned>((M + 31) / 32));
   dim3 block(32, 8);
   transpose_cast_kernel<<<grid, block, 0, stream>>>(a, a_dtype, M, K, lda, at, at_dtype, ld_at);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_prepare_input(const PrepArgs& a, cudaStream_t stream) {
-  if (a.M <= 0 || a.K <= 0) return cudaSuccess;
-  if (a.src_km) {
-    dim3 grid(static_cast<unsigned>(std::min<int64_t>((a.M + 255) / 256, 64)),
-              static_cast<unsigned>(a.K));
-    prep_from_km_kernel<<<grid, 256, 0, stream>>>(a);
-  } else {
-    dim3 grid(static_cast<unsigned>((a.K + kPrepRows - 1) / kPrepRows),
-              static_cast<unsigned>((a.M + kPrepTok - 1) / kPrepTok));
-    prep_from_mk_kernel<<<grid, dim3(32, 8), 0, stream>>>(a);
-  }
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess || a.n_zero <= 0) return e;
-  dim3 zgrid(static_cast<unsigned>(std::min<int64_t>((a.ld_dst + 255) / 256, 64)),
-             static_cast<unsigned>(a.n_zero));
-  prep_zero_kernel<<<zgrid, 256, 0, stream>>>(a);
   return cudaGetLastError();
 }
 

@@ -1,22 +1,8 @@
 // C ABI (include/tw_gemm.h): host-side validation of CTO encodings and
-// overlays, construction of the device weight format and of the grouped input
-// layout, TMA descriptor encoding, and kernel dispatch.  All numerics run in
-// the kernels of tw_gemm.cu / tw_aux.cu; nothing here computes on the CPU
-// beyond index bookkeeping.
-//
-// Grouped input layout.  A TW tile keeps an arbitrary half of the K rows, so
-// gathering its rows from A^T row by row caps the load rate at ~6 TB/s on
-// B200 (measured, scripts/microbench_gather.cu) while TMA 2-D tiles over
-// contiguous rows reach ~12.6 TB/s.  The plan therefore defines the layout
-// the GEMM reads its activations in: tiles are taken in clusters of up to
-// `cluster` consecutive tiles; inside a cluster every kept row is placed in
-// the group of rows with the same tile-membership pattern, groups ordered in
-// reflected Gray-code order and padded to 8 rows.  Each tile's kept rows then
-// form <= 2^(c-1) (for c = 3: at most 2) contiguous runs, read with a handful
-// of TMA boxes per stage.  The layout is built by tw_prepare_input (or, in a
-// network, directly by the previous layer's epilogue); rows of the layout are
-// copies of original K rows, so results are unchanged (padding rows are zero
-// in both the activations and the payload).
+// overlays, construction of the device weight format (padded fp16/bf16
+// payload + per-tile gather lists), TMA descriptor encoding, work-unit sizing
+// and kernel dispatch.  All numerics run in the kernels of tw_gemm.cu /
+// tw_aux.cu; nothing here computes on the CPU beyond index bookkeeping.
 #include "../../include/tw_gemm.h"
 #include "tw_kernels.cuh"
 
@@ -128,111 +114,24 @@ int upload(T** dptr, const std::vector<T>& host, cudaStream_t s) {
 
 int32_t round_up(int32_t v, int32_t a) { return (v + a - 1) / a * a; }
 
-// ------------------------------------------------------ grouped input layout
-struct Layout {
-  std::vector<int32_t> src;                   // grouped row -> original row, -1 = zero
-  std::vector<std::vector<RunDesc>> runs;     // per tile, covering its padded sequence
-  std::vector<int32_t> seq_len;               // per tile: padded sequence length (mult. of kBK)
-  std::vector<std::vector<int32_t>> seq;      // per tile: grouped row of every sequence slot
-  std::vector<int32_t> home;                  // original row -> one grouped row holding it
-  int32_t zero_row = 0;                       // first of kBK zero rows at the end
-};
-
-void append_group(Layout& L, const std::vector<int32_t>& rows) {
-  L.src.insert(L.src.end(), rows.begin(), rows.end());
-  while (L.src.size() % kRunAlign) L.src.push_back(-1);
-}
-
-Layout build_layout(int32_t k, const std::vector<std::vector<int32_t>>& kept, int cluster) {
-  const int n_tiles = static_cast<int>(kept.size());
-  Layout L;
-  L.runs.resize(n_tiles);
-  L.seq.resize(n_tiles);
-  L.seq_len.resize(n_tiles);
-  L.home.assign(k, -1);
-  for (int c0 = 0; c0 < n_tiles; c0 += cluster) {
-    const int nc = std::min(cluster, n_tiles - c0);
-    std::vector<uint32_t> pat(k, 0);
-    for (int t = 0; t < nc; ++t)
-      for (int32_t r : kept[c0 + t]) pat[r] |= 1u << t;
-    // bucket rows by pattern, ascending original order inside a bucket
-    std::vector<std::vector<int32_t>> bucket(1u << nc);
-    for (int32_t r = 0; r < k; ++r)
-      if (pat[r]) bucket[pat[r]].push_back(r);
-    // groups in reflected Gray-code order; a tile's consecutive groups merge
-    // into one run
-    std::vector<int32_t> open_start(nc, -1);  // grouped row where the tile's current run began
-    std::vector<int32_t> seqpos(nc, 0);
-    auto close_run = [&](int t) {
-      if (open_start[t] < 0) return;
-      const int32_t len = static_cast<int32_t>(L.src.size()) - open_start[t];
-      L.runs[c0 + t].push_back(RunDesc{seqpos[t], open_start[t], len, 0});
-      seqpos[t] += len;
-      open_start[t] = -1;
-    };
-    for (uint32_t i = 1; i < (1u << nc); ++i) {
-      const uint32_t g = i ^ (i >> 1);
-      if (bucket[g].empty()) continue;
-      for (int t = 0; t < nc; ++t) {
-        if (g & (1u << t)) {
-          if (open_start[t] < 0) open_start[t] = static_cast<int32_t>(L.src.size());
-        } else {
-          close_run(t);
-        }
-      }
-      const int32_t base = static_cast<int32_t>(L.src.size());
-      for (size_t q = 0; q < bucket[g].size(); ++q)
-        if (L.home[bucket[g][q]] < 0) L.home[bucket[g][q]] = base + static_cast<int32_t>(q);
-      append_group(L, bucket[g]);
-    }
-    for (int t = 0; t < nc; ++t) close_run(t);
-  }
-  // rows kept by no tile (needed only by a TEW overlay) go in a rest region
-  std::vector<int32_t> rest;
-  for (int32_t r = 0; r < k; ++r)
-    if (L.home[r] < 0) rest.push_back(r);
-  for (size_t i = 0; i < rest.size(); ++i)
-    L.home[rest[i]] = static_cast<int32_t>(L.src.size() + i);
-  if (!rest.empty()) append_group(L, rest);
-  // kBK zero rows: every tile's sequence is padded to whole stages from here
-  L.zero_row = static_cast<int32_t>(L.src.size());
-  L.src.insert(L.src.end(), kBK, -1);
-  for (int t = 0; t < n_tiles; ++t) {
-    int32_t len = 0;
-    for (const RunDesc& rd : L.runs[t]) len = rd.seq_off + rd.len;
-    const int32_t padded = round_up(std::max(len, 1), kBK);
-    if (padded > len) L.runs[t].push_back(RunDesc{len, L.zero_row, padded - len, 0});
-    L.seq_len[t] = padded;
-    L.seq[t].reserve(padded);
-    for (const RunDesc& rd : L.runs[t])
-      for (int32_t j = 0; j < rd.len; ++j) L.seq[t].push_back(rd.row + j);
-  }
-  return L;
-}
-
 }  // namespace
 
 struct tw_plan {
   int32_t k = 0, n = 0, g = 0, n_tiles = 0, n_sub = 0, bn = 0, kp = 0, n_cond = 0;
-  int32_t dtype = kF16, schedule = TW_SCHEDULE_LPT, sm_count = 0, cluster = 3;
+  int32_t dtype = kF16, schedule = TW_SCHEDULE_LPT, sm_count = 0;
   std::vector<SubTile> subtiles;
   std::vector<int32_t> cond_cols;        // condensed col -> original col
   std::vector<int32_t> tile_of_col;      // original col -> tile (or -1)
   std::vector<std::vector<uint8_t>> tile_rows;  // per tile: K flags
   std::vector<int32_t> tile_first_cond;  // per tile: first condensed column
   int64_t kept_macs = 0;
-  Layout layout;
   int32_t spm = 0;
   // device
   SubTile* d_subtiles = nullptr;
-  RunDesc* d_runs = nullptr;
+  int32_t* d_gidx = nullptr;  // [n_tiles][kp] kept rows, -1 padded
   void* d_payload = nullptr;
   float* d_ws = nullptr;
   int32_t* d_ws_flags = nullptr;
-  int32_t* d_prep_ptr = nullptr;
-  int32_t* d_prep_rows = nullptr;
-  int32_t* d_prep_zero = nullptr;
-  int32_t n_prep_zero = 0;
   CUtensorMap map_pay;
   // TEW overlay
   bool has_overlay = false;
@@ -247,20 +146,18 @@ struct tw_plan {
   int32_t* d_ov_acc = nullptr;
 
   ~tw_plan() {
-    for (void* p : {(void*)d_subtiles, (void*)d_runs, d_payload, (void*)d_ws,
-                    (void*)d_ws_flags, (void*)d_prep_ptr, (void*)d_prep_rows, (void*)d_prep_zero,
-                    (void*)d_union_rowmap, (void*)d_ov_start, (void*)d_ov_rows, (void*)d_ov_vals,
+    for (void* p : {(void*)d_subtiles, (void*)d_gidx, d_payload, (void*)d_ws,
+                    (void*)d_ws_flags, (void*)d_union_rowmap, (void*)d_ov_start, (void*)d_ov_rows, (void*)d_ov_vals,
                     (void*)d_ov_out, (void*)d_ov_acc})
       if (p) cudaFree(p);
   }
-  int64_t input_rows() const { return static_cast<int64_t>(layout.src.size()); }
 };
 
 extern "C" {
 
 const char* tw_last_error(void) { return g_last_error.c_str(); }
 
-int32_t tw_abi_version(void) { return 200; }
+int32_t tw_abi_version(void) { return 300; }
 
 int tw_plan_create_cto(tw_plan** out, int32_t k, int32_t n, int32_t g, int32_t n_tiles,
                        const uint32_t* row_counts, const uint32_t* col_counts,
@@ -299,7 +196,6 @@ int tw_plan_create_cto(tw_plan** out, int32_t k, int32_t n, int32_t g, int32_t n
   plan->n_tiles = n_tiles;
   plan->dtype = compute_dtype;
   plan->schedule = schedule;
-  plan->cluster = std::max(1, std::min(env_int("TW_CLUSTER", 3), 5));
   if (int st = sm_count_of_current_device(&plan->sm_count)) return st;
   TW_CUDA(configure_gemm_kernels());
   cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -344,22 +240,17 @@ int tw_plan_create_cto(tw_plan** out, int32_t k, int32_t n, int32_t g, int32_t n
   }
   plan->n_cond = (int32_t)plan->cond_cols.size();
 
-  // grouped input layout and per-tile row runs
-  plan->layout = build_layout(k, rows, plan->cluster);
-  const Layout& L = plan->layout;
+  // gather lists: each tile's kept rows padded with -1 to whole stages
   int32_t kp = kBK;
-  for (int i = 0; i < n_tiles; ++i) kp = std::max(kp, L.seq_len[i]);
+  for (int i = 0; i < n_tiles; ++i) kp = std::max(kp, round_up((int32_t)row_counts[i], kBK));
   plan->kp = kp;
+  std::vector<int32_t> gidx((size_t)n_tiles * kp, -1);
+  for (int i = 0; i < n_tiles; ++i)
+    std::copy(rows[i].begin(), rows[i].end(), gidx.begin() + (size_t)i * kp);
 
-  // sub-tiles (128-column UMMA-M slices), runs table, payload sources
+  // sub-tiles (128-column UMMA-M slices) and payload sources
   const int bn = kBN;
   plan->bn = bn;
-  std::vector<RunDesc> runs;
-  std::vector<int32_t> tile_run_off(n_tiles);
-  for (int i = 0; i < n_tiles; ++i) {
-    tile_run_off[i] = (int32_t)runs.size();
-    runs.insert(runs.end(), L.runs[i].begin(), L.runs[i].end());
-  }
   std::vector<SubTile> subs;
   std::vector<int64_t> src_base;
   std::vector<int32_t> src_ld;
@@ -368,13 +259,11 @@ int tw_plan_create_cto(tw_plan** out, int32_t k, int32_t n, int32_t g, int32_t n
     const int32_t h = (int32_t)row_counts[i], w = (int32_t)col_counts[i];
     for (int32_t c0 = 0; c0 < w; c0 += bn) {
       SubTile st{};
-      st.kp_steps = L.seq_len[i] / kBK;
+      st.kp_steps = round_up(h, kBK) / kBK;
       st.idx_row = i;
       st.width = std::min(bn, w - c0);
       st.out_row = plan->tile_first_cond[i] + c0;
       st.kept = h;
-      st.run_off = tile_run_off[i];
-      st.n_runs = (int32_t)L.runs[i].size();
       subs.push_back(st);
       src_base.push_back(pbase + (int64_t)c0 * h);
       src_ld.push_back(h);
@@ -385,7 +274,7 @@ int tw_plan_create_cto(tw_plan** out, int32_t k, int32_t n, int32_t g, int32_t n
   std::vector<int32_t> order(plan->n_sub);
   std::iota(order.begin(), order.end(), 0);
   if (schedule == TW_SCHEDULE_LPT) {
-    // executor.py:526 sorts tiles by (-macs, index); per 128-token block the
+    // executor.py:526 sorts tiles by (-macs, index); per token block the
     // MACs of a sub-tile are proportional to K' * width
     std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
       return (int64_t)subs[a].kept * subs[a].width > (int64_t)subs[b].kept * subs[b].width;
@@ -406,42 +295,8 @@ int tw_plan_create_cto(tw_plan** out, int32_t k, int32_t n, int32_t g, int32_t n
   }
   plan->spm = off;
 
-  // payload slot positions: kept-row index of every sequence slot (-1 = zero)
-  std::vector<int32_t> seq_pos((size_t)n_tiles * kp, -1);
-  for (int i = 0; i < n_tiles; ++i) {
-    for (int32_t j = 0; j < L.seq_len[i]; ++j) {
-      const int32_t grow = L.seq[i][j];
-      const int32_t orow = L.src[grow];
-      if (orow >= 0) {
-        auto it = std::lower_bound(rows[i].begin(), rows[i].end(), orow);
-        if (it != rows[i].end() && *it == orow)
-          seq_pos[(size_t)i * kp + j] = (int32_t)(it - rows[i].begin());
-      }
-    }
-  }
-
-  // prep lists: copies of each original row, zero rows
-  std::vector<int32_t> prep_ptr(k + 1, 0), prep_rows, prep_zero;
-  for (size_t j = 0; j < L.src.size(); ++j) {
-    if (L.src[j] >= 0)
-      ++prep_ptr[L.src[j] + 1];
-    else
-      prep_zero.push_back((int32_t)j);
-  }
-  for (int32_t r = 0; r < k; ++r) prep_ptr[r + 1] += prep_ptr[r];
-  prep_rows.resize(prep_ptr[k]);
-  {
-    std::vector<int32_t> fill(prep_ptr.begin(), prep_ptr.end() - 1);
-    for (size_t j = 0; j < L.src.size(); ++j)
-      if (L.src[j] >= 0) prep_rows[fill[L.src[j]]++] = (int32_t)j;
-  }
-  plan->n_prep_zero = (int32_t)prep_zero.size();
-
   if (int st = upload(&plan->d_subtiles, plan->subtiles, s)) return st;
-  if (int st = upload(&plan->d_runs, runs, s)) return st;
-  if (int st = upload(&plan->d_prep_ptr, prep_ptr, s)) return st;
-  if (int st = upload(&plan->d_prep_rows, prep_rows, s)) return st;
-  if (int st = upload(&plan->d_prep_zero, prep_zero, s)) return st;
+  if (int st = upload(&plan->d_gidx, gidx, s)) return st;
   // stream-K workspace: one [kBN][kTN] fp32 partial + flag per CTA
   TW_CUDA(cudaMalloc(&plan->d_ws, (size_t)plan->sm_count * kBN * kTN * sizeof(float)));
   TW_CUDA(cudaMalloc(&plan->d_ws_flags, (size_t)plan->sm_count * sizeof(int32_t)));
@@ -449,23 +304,20 @@ int tw_plan_create_cto(tw_plan** out, int32_t k, int32_t n, int32_t g, int32_t n
 
   int64_t* d_src_base = nullptr;
   int32_t* d_src_ld = nullptr;
-  int32_t* d_seq_pos = nullptr;
   float* d_src = nullptr;
   if (int st = upload(&d_src_base, base2, s)) return st;
   if (int st = upload(&d_src_ld, ld2, s)) return st;
-  if (int st = upload(&d_seq_pos, seq_pos, s)) return st;
   TW_CUDA(cudaMalloc(&d_src, std::max<int64_t>(pbase, 1) * sizeof(float)));
   TW_CUDA(cudaMemcpyAsync(d_src, payload, pbase * sizeof(float), cudaMemcpyHostToDevice, s));
   const size_t pay_bytes = (size_t)plan->n_sub * bn * kp * 2;
   TW_CUDA(cudaMalloc(&plan->d_payload, pay_bytes));
-  PayloadArgs pa{d_src, d_src_base, d_src_ld, d_seq_pos, plan->d_subtiles, plan->d_payload,
+  PayloadArgs pa{d_src, d_src_base, d_src_ld, plan->d_subtiles, plan->d_payload,
                  compute_dtype, bn, kp, plan->n_sub};
   TW_CUDA(launch_build_payload(pa, s));
   TW_CUDA(cudaStreamSynchronize(s));
   cudaFree(d_src);
   cudaFree(d_src_base);
   cudaFree(d_src_ld);
-  cudaFree(d_seq_pos);
   if (int st = make_map_2d(&plan->map_pay, plan->d_payload, compute_dtype, kp,
                            (uint64_t)plan->n_sub * bn, kp, kBK, bn))
     return st;
@@ -514,7 +366,7 @@ int tw_plan_attach_overlay(tw_plan* p, int32_t k, int32_t n, int64_t nnz, const 
   std::vector<float> vals;
   for (int32_t c : ov_cols) {
     for (int64_t e = col_ptr[c]; e < col_ptr[c + 1]; ++e) {
-      rows.push_back(p->layout.home[row_idx[e]]);  // grouped-input row of the original row
+      rows.push_back((int32_t)row_idx[e]);
       vals.push_back(values[e]);
     }
     start.push_back((int32_t)rows.size());
@@ -558,9 +410,6 @@ int tw_plan_get_info(const tw_plan* p, tw_plan_info* info) {
   info->kept_macs_per_token = p->kept_macs + p->nnz;
   info->sm_count = p->sm_count;
   info->has_overlay = p->has_overlay ? 1 : 0;
-  info->input_rows = p->input_rows();
-  info->cluster = p->cluster;
-  info->reserved = 0;
   return TW_OK;
 }
 
@@ -576,44 +425,9 @@ int tw_plan_union_columns(const tw_plan* p, int32_t* out) {
   return TW_OK;
 }
 
-int tw_plan_input_map(const tw_plan* p, int32_t* out) {
-  if (!p || !out) return fail(TW_ERR_INVALID_INPUT, "null argument");
-  std::copy(p->layout.src.begin(), p->layout.src.end(), out);
-  return TW_OK;
-}
-
 static int check_dtype(int32_t d) {
   if (d != kF32 && d != kF16 && d != kBF16)
     return fail(TW_ERR_INVALID_INPUT, "unknown dtype %d", d);
-  return TW_OK;
-}
-
-int tw_prepare_input(const tw_plan* p, const void* src, int32_t src_dtype, int32_t src_layout,
-                     int64_t m, int64_t ld_src, void* x, int64_t ld_x, void* stream) {
-  g_last_error.clear();
-  if (!p || !src || !x) return fail(TW_ERR_INVALID_INPUT, "null argument");
-  if (int st = check_dtype(src_dtype)) return st;
-  if (src_layout != TW_LAYOUT_MK && src_layout != TW_LAYOUT_KM)
-    return fail(TW_ERR_INVALID_INPUT, "unknown source layout %d", src_layout);
-  if (m < 1) return fail(TW_ERR_INVALID_INPUT, "m must be >= 1");
-  if (ld_src < (src_layout == TW_LAYOUT_MK ? p->k : m))
-    return fail(TW_ERR_INVALID_INPUT, "ld_src too small");
-  if (ld_x < m) return fail(TW_ERR_INVALID_INPUT, "ld_x must be >= m");
-  PrepArgs a{};
-  a.src = src;
-  a.src_dtype = src_dtype;
-  a.src_km = src_layout == TW_LAYOUT_KM ? 1 : 0;
-  a.ld_src = ld_src;
-  a.M = m;
-  a.K = p->k;
-  a.dst = x;
-  a.dst_dtype = p->dtype;
-  a.ld_dst = ld_x;
-  a.csr_ptr = p->d_prep_ptr;
-  a.csr_rows = p->d_prep_rows;
-  a.zero_rows = p->d_prep_zero;
-  a.n_zero = p->n_prep_zero;
-  TW_CUDA(launch_prepare_input(a, static_cast<cudaStream_t>(stream)));
   return TW_OK;
 }
 
@@ -622,34 +436,58 @@ static int check_io(const tw_plan* p, const void* x, int64_t m, int64_t ld_x, co
   if (!p || !x || !ct) return fail(TW_ERR_INVALID_INPUT, "null argument");
   if (m < 1 || m > INT32_MAX) return fail(TW_ERR_INVALID_INPUT, "m must be in [1, 2^31)");
   if (ld_x < m || ld_x % 8 != 0)
-    return fail(TW_ERR_INVALID_INPUT, "ld_x (%lld) must be >= m and a multiple of 8",
+    return fail(TW_ERR_INVALID_INPUT, "ld_at (%lld) must be >= m and a multiple of 8",
                 (long long)ld_x);
   if (reinterpret_cast<uintptr_t>(x) % 16 != 0)
-    return fail(TW_ERR_INVALID_INPUT, "input base must be 16-byte aligned");
+    return fail(TW_ERR_INVALID_INPUT, "A^T base must be 16-byte aligned");
   if (ld_ct < m) return fail(TW_ERR_INVALID_INPUT, "ld_ct must be >= m");
   return check_dtype(out_dtype);
+}
+
+// Tokens per work unit.  Units (token block x sub-tile) are strided over
+// min(units, SMs) persistent CTAs; the busiest CTA's ingress (payload 128 B +
+// activations tn * 2 B per kept row and stage, in 128-byte units) plus one
+// exposed epilogue sets the time.  Narrower units add CTAs when a layer has
+// fewer 256-token units than SMs, at the price of reloading the payload more
+// often; pick the width with the smallest busiest-CTA estimate.
+static int pick_tokens_per_unit(const tw_plan* p, int64_t m) {
+  const int forced = env_int("TW_TN", 0);
+  if (forced == 64 || forced == 128 || forced == 192 || forced == 256) return forced;
+  int best_tn = kTN;
+  double best = 0;
+  for (int tn : {256, 192, 128}) {
+    const int64_t n_mblk = (m + tn - 1) / tn;
+    const int64_t units = n_mblk * p->n_sub;
+    const int grid = (int)std::min<int64_t>(units, p->sm_count);
+    std::vector<double> load(grid, 0.0);
+    for (int64_t u = 0; u < units; ++u)
+      load[u % grid] += (double)p->subtiles[u % p->n_sub].kp_steps * (128 + tn);
+    const double t = *std::max_element(load.begin(), load.end()) + 4.8 * tn;
+    if (tn == 256 || t < best * 0.97) {
+      if (tn == 256 || t < best) {
+        best = t;
+        best_tn = tn;
+      }
+    }
+  }
+  return best_tn;
 }
 
 static int run_tw(const tw_plan* p, const void* x, int64_t m, int64_t ld_x, void* ct,
                   int64_t ld_ct, int32_t out_dtype, const int32_t* rowmap, int64_t out_rows,
                   cudaStream_t s) {
-  const uint64_t R = (uint64_t)p->input_rows();
-  CUtensorMap map_x, map_x8;
-  if (int st = make_map_2d(&map_x, x, p->dtype, (uint64_t)m, R, (uint64_t)ld_x, 64, kBK))
-    return st;
-  if (int st = make_map_2d(&map_x8, x, p->dtype, (uint64_t)m, R, (uint64_t)ld_x, 64, kRunAlign))
-    return st;
   GemmArgs a{};
   a.subtiles = p->d_subtiles;
-  a.runs = p->d_runs;
+  a.x = x;
+  a.ld_x = ld_x;
+  a.gidx = p->d_gidx;
+  a.kp = p->kp;
   a.rowmap = rowmap;
   a.out = ct;
   a.ld_out = ld_ct;
   a.out_dtype = out_dtype;
   a.M = (int32_t)m;
   a.n_sub = p->n_sub;
-  a.n_mblk = (int32_t)((m + kTN - 1) / kTN);
-  a.n_units = a.n_sub * a.n_mblk;
   a.flags = env_int("TW_DEBUG_FLAGS", 0);
   a.trace = g_trace;
   const int esz = out_dtype == kF32 ? 4 : 2;
@@ -664,15 +502,19 @@ static int run_tw(const tw_plan* p, const void* x, int64_t m, int64_t ld_x, void
       a.use_tma_store = 1;
     g_last_error.clear();
   }
-  // Work split: whole units strided over the CTAs, or (opt-in) stream-K with
-  // equal stage ranges (each range must hold the longest unit so a unit is
-  // split at most once).
+  // Work split: whole units strided over the CTAs, or (opt-in, 256-token
+  // units) stream-K with equal stage ranges (each range must hold the longest
+  // unit so a unit is split at most once).
+  const bool streamk = env_int("TW_STREAMK", 0) != 0;
+  a.tn = streamk ? kTN : pick_tokens_per_unit(p, m);
+  a.n_mblk = (int32_t)((m + a.tn - 1) / a.tn);
+  a.n_units = a.n_sub * a.n_mblk;
   int grid = std::min(a.n_units, p->sm_count);
   a.spm = p->spm;
   a.split = 0;
   a.ws = p->d_ws;
   a.ws_flags = p->d_ws_flags;
-  if (a.n_units > p->sm_count && env_int("TW_STREAMK", 0)) {
+  if (streamk && a.n_units > p->sm_count) {
     const int64_t total = (int64_t)a.n_mblk * p->spm;
     int max_kp = 1;
     for (const SubTile& st : p->subtiles) max_kp = std::max(max_kp, (int)st.kp_steps);
@@ -680,7 +522,7 @@ static int run_tw(const tw_plan* p, const void* x, int64_t m, int64_t ld_x, void
     grid = std::max(grid, 1);
     a.split = 1;
   }
-  TW_CUDA(launch_tw_gemm(map_x, map_x8, p->map_pay, map_out, a, p->dtype, grid, s));
+  TW_CUDA(launch_tw_gemm(p->map_pay, map_out, a, p->dtype, grid, s));
   return TW_OK;
 }
 

@@ -13,24 +13,28 @@
 // operand.  TMEM lanes are output columns and TMEM columns are tokens, so an
 // epilogue thread holds a contiguous segment of one C'^T row.
 //
-// Work decomposition.  A unit is (256-token block, 128-column sub-tile); its
-// k-steps (64 kept rows each) are stages.  Units are strided over the
-// persistent CTAs; optionally (TW_STREAMK=1) the CTA-major stage list is cut
-// into equal ranges (stream-K): a unit cut by a range boundary is split in
-// two, the lower CTA publishes its head k-steps as an fp32 partial, the
-// higher CTA adds it in its epilogue.  CTAs walk their range backwards so a
-// CTA only waits on a lower-numbered CTA that published first.
+// Work decomposition.  A unit is (tn-token block, 128-column sub-tile), tn in
+// {64, 128, 192, 256} chosen per launch by the host so the units fill the SMs;
+// its k-steps (64 kept rows each) are stages.  Units are strided over the
+// persistent CTAs; optionally (TW_STREAMK=1, tn = 256) the CTA-major stage
+// list is cut into equal ranges (stream-K): a unit cut by a range boundary is
+// split in two, the lower CTA publishes its head k-steps as an fp32 partial,
+// the higher CTA adds it in its epilogue.  CTAs walk their range backwards so
+// a CTA only waits on a lower-numbered CTA that published first.
 //
-// Roles (12 warps, 1 CTA per SM):
-//   warp 0      producer: per stage one TMA box of the payload (128 cols x 64
-//               k) and TMA boxes of X over the tile's row runs: {64 tok x 64
-//               rows} inside a run, {64 x 8} at run boundaries (8-row aligned).
+// Roles (1 CTA per SM):
+//   warp 0      payload producer: one TMA box per stage (128 cols x 64 k).
 //   warp 1      TMEM allocator (2 x 256 columns: double-buffered accumulators)
-//               and MMA issuer: one thread, tcgen05.mma.kind::f16 M=128 N=256 K=16.
-//   warps 4-11  epilogue: warp w owns TMEM lanes 32*(w%4).. (output columns)
-//               and token half (w-4)/4; tcgen05.ld -> fp16/bf16/fp32 -> swizzled
-//               smem tile -> one TMA 2-D store per 32 x 32 block (16-byte stores
-//               for the TEW row scatter through rowmap and ragged sub-tiles).
+//               and MMA issuer: one thread, tcgen05.mma.kind::f16 M=128 N=tn K=16.
+//   warps 4..   gather producers (kGatherWGs warpgroups): the tile's 64 kept
+//               A^T rows of a stage, each row's tn tokens (512 contiguous bytes
+//               for tn = 256) as 16-byte cp.async into the 128-B swizzled
+//               MN-major layout; gather indices are prefetched one stage ahead
+//               in registers.  A^T is read where it lies: no repacked copy.
+//   last 8      epilogue: warp w owns TMEM lanes 32*(w%4).. (output columns)
+//               and token half; tcgen05.ld -> fp16/bf16/fp32 -> swizzled smem
+//               tile -> one TMA 2-D store per 32 x 32 block (16-byte stores for
+//               the TEW row scatter through rowmap and ragged sub-tiles).
 //
 // Shared memory per stage: payload [128 cols][128 B] K-major SW128 (16 KB) and
 // X [4 x 64-token chunks][64 k][128 B] MN-major SW128 (32 KB); 4 stages.
@@ -44,12 +48,18 @@ namespace tw {
 
 namespace {
 
-constexpr int kProducerWarp = 0;
+#ifndef TW_GATHER_WARPGROUPS
+#define TW_GATHER_WARPGROUPS 3
+#endif
+constexpr int kGatherWGs = TW_GATHER_WARPGROUPS;
+constexpr int kPayloadWarp = 0;
 constexpr int kMmaWarp = 1;
-constexpr int kEpilogueWarp0 = 4;
+constexpr int kGatherWarp0 = 4;
+constexpr int kGatherWarps = 4 * kGatherWGs;
+constexpr int kEpilogueWarp0 = kGatherWarp0 + kGatherWarps;
 constexpr int kEpilogueWarps = 8;
 constexpr int kThreads = 32 * (kEpilogueWarp0 + kEpilogueWarps);
-constexpr int kTileN = kTN;                          // tokens per unit (UMMA N)
+constexpr int kTileN = kTN;                          // max tokens per unit (UMMA N)
 constexpr int kChunkBytes = 64 * kBK * 2;            // 64 tokens x 64 rows x 2 B = 8 KB
 constexpr int kXBytes = (kTileN / 64) * kChunkBytes; // 32 KB per stage
 constexpr int kPBytes = kBN * kBK * 2;               // 16 KB per stage
@@ -65,6 +75,7 @@ constexpr uint32_t kTmemCols = 2 * kTileN;           // double-buffered 128 x 25
 constexpr int kEpiBarrier = 2;                       // named barrier id of the epilogue warps
 constexpr int kEpiThreads = 32 * kEpilogueWarps;
 static_assert(kSmemBytes <= 227 * 1024, "shared memory budget");
+static_assert(kEpilogueWarp0 % 4 == 0, "epilogue warps must start a warpgroup (TMEM lane quadrants)");
 
 // Sub-tile table in visiting order (smem copy when small enough).
 struct Tables {
@@ -164,42 +175,37 @@ __device__ __forceinline__ uint32_t pack2(float a, float b, int32_t dtype) {
 __device__ __forceinline__ void epilogue_rows(const GemmArgs& args, const CUtensorMap* map_out,
                                               uint8_t* stg, uint32_t t0, int lane, int orow,
                                               bool row_live, bool warp_full, int row0_tma,
-                                              int tok0, const float* add) {
+                                              int tok0, int ntok, const float* add) {
   const bool do_store = !(args.flags & kFlagSkipStore);
   const int esz = args.out_dtype == kF32 ? 4 : 2;
   const bool use_tma = do_store && args.use_tma_store && warp_full;
   uint8_t* row_base =
       static_cast<uint8_t*>(args.out) + static_cast<int64_t>(orow) * args.ld_out * esz;
-  uint32_t r[32];
-  tmem_ld_32x32b_x32(t0, r);
+  if (ntok <= 0) return;
 #pragma unroll 1
-  for (int c = 0; c < 128; c += 32) {
+  for (int c = 0; c < ntok; c += 32) {
+    // one 32-token chunk of the row, converted in place in the load registers
+    uint32_t w[32];
+    tmem_ld_32x32b_x32(t0 + c, w);
     tmem_ld_wait();
-    float v[32];
-#pragma unroll
-    for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-    if (c + 32 < 128) tmem_ld_32x32b_x32(t0 + c + 32, r);
     if (add) {
 #pragma unroll
       for (int i = 0; i < 32; i += 4) {
         const float4 p = __ldcg(reinterpret_cast<const float4*>(add + c + i));
-        v[i] += p.x;
-        v[i + 1] += p.y;
-        v[i + 2] += p.z;
-        v[i + 3] += p.w;
+        w[i] = __float_as_uint(__uint_as_float(w[i]) + p.x);
+        w[i + 1] = __float_as_uint(__uint_as_float(w[i + 1]) + p.y);
+        w[i + 2] = __float_as_uint(__uint_as_float(w[i + 2]) + p.z);
+        w[i + 3] = __float_as_uint(__uint_as_float(w[i + 3]) + p.w);
       }
     }
     if (!do_store) continue;
     const int tok = tok0 + c;
     if (tok >= args.M) continue;
-    // packed row segment: 16 (fp16/bf16) or 32 (fp32) 32-bit words
-    uint32_t w[32];
-    if (esz == 4) {
+    if (esz == 2) {
+      // packed row segment: 16 words (element pairs); w[i] <- (w[2i], w[2i+1])
 #pragma unroll
-      for (int i = 0; i < 32; ++i) w[i] = __float_as_uint(v[i]);
-    } else {
-#pragma unroll
-      for (int i = 0; i < 16; ++i) w[i] = pack2(v[2 * i], v[2 * i + 1], args.out_dtype);
+      for (int i = 0; i < 16; ++i)
+        w[i] = pack2(__uint_as_float(w[2 * i]), __uint_as_float(w[2 * i + 1]), args.out_dtype);
     }
     if (use_tma) {
       // the TMA store that last read this staging tile must be done with it
@@ -237,7 +243,7 @@ __device__ __forceinline__ void epilogue_rows(const GemmArgs& args, const CUtens
       } else {
 #pragma unroll
         for (int i = 0; i < 32; ++i)
-          if (tok + i < args.M) dst[i] = v[i];
+          if (tok + i < args.M) dst[i] = __uint_as_float(w[i]);
       }
     } else {
       uint16_t* dst = reinterpret_cast<uint16_t*>(row_base) + tok;
@@ -273,9 +279,7 @@ __device__ __forceinline__ void epilogue_partial_row(float* ws_row, uint32_t t0,
 }
 
 __global__ void __launch_bounds__(kThreads, 1)
-    tw_gemm_kernel(const __grid_constant__ CUtensorMap map_x,
-                   const __grid_constant__ CUtensorMap map_x8,
-                   const __grid_constant__ CUtensorMap map_pay,
+    tw_gemm_kernel(const __grid_constant__ CUtensorMap map_pay,
                    const __grid_constant__ CUtensorMap map_out, const GemmArgs args,
                    uint32_t idesc) {
   extern __shared__ uint8_t smem_raw[];
@@ -305,7 +309,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
-      mbar_init(&full[s], 1);
+      // payload TMA (expect_tx arrival) + one arrival per gather warp
+      mbar_init(&full[s], 1 + kGatherWarps);
       mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
@@ -315,9 +320,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     fence_barrier_init();
     fence_proxy_async_smem();
   }
-  if (warp == kProducerWarp && lane == 0) {
-    tma_prefetch_desc(&map_x);
-    tma_prefetch_desc(&map_x8);
+  if (warp == kPayloadWarp && lane == 0) {
     tma_prefetch_desc(&map_pay);
     if (args.use_tma_store) tma_prefetch_desc(&map_out);
   }
@@ -339,57 +342,89 @@ __global__ void __launch_bounds__(kThreads, 1)
     trace[3074] = static_cast<long long>(globaltimer_ns());
   }
 
+  const int tn = args.tn;
   SegWalker walk;
   walk.init(args);
   Seg sg;
 
-  if (warp == kProducerWarp) {
-    // ------------------------------------------------------------ producer
+  if (warp == kPayloadWarp) {
+    // ---------------------------------------------------- payload producer
     if (lane == 0) {
       int gs = 0;
       while (walk.next(args, tab, sg)) {
-        const int m0 = sg.mb * kTileN;
-        const RunDesc* runs = args.runs + sg.d.run_off;
-        int w = sg.ks0 * kBK;  // position in the tile's K sequence
-        int ri = 0;
-        while (ri + 1 < sg.d.n_runs && __ldg(&runs[ri + 1].seq_off) <= w) ++ri;
-        RunDesc R = runs[ri];
         for (int ks = sg.ks0; ks < sg.ks1; ++ks, ++gs) {
           const int stage = gs % kStages;
           mbar_wait(&empty[stage], ((gs / kStages) & 1) ^ 1u);
-          const uint32_t bytes = (flags & kFlagSkipA) ? kPBytes : kStageBytes;
-          mbar_arrive_expect_tx(&full[stage], bytes);
+          mbar_arrive_expect_tx(&full[stage], kPBytes);
           tma_load_2d(sP + stage * kPBytes, &map_pay, &full[stage], ks * kBK, sg.d.pay_row);
-          if (flags & kFlagSkipA) {
-            w += kBK;
-            while (ri + 1 < sg.d.n_runs && __ldg(&runs[ri + 1].seq_off) <= w) ++ri;
-            R = runs[ri];
-            continue;
-          }
-          uint8_t* x_stage = sX + stage * kXBytes;
-          int covered = 0;
-          while (covered < kBK) {
-            const int off = w - R.seq_off;
-            const int take = min(R.len - off, kBK - covered);
-            if (take == kBK) {
-#pragma unroll
-              for (int ch = 0; ch < kTileN / 64; ++ch)
-                tma_load_2d(x_stage + ch * kChunkBytes, &map_x, &full[stage], m0 + ch * 64,
-                            R.row + off);
-            } else {
-              for (int p8 = 0; p8 < take; p8 += kRunAlign) {
-#pragma unroll
-                for (int ch = 0; ch < kTileN / 64; ++ch)
-                  tma_load_2d(x_stage + ch * kChunkBytes + (covered + p8) * 128, &map_x8,
-                              &full[stage], m0 + ch * 64, R.row + off + p8);
-              }
-            }
-            covered += take;
-            w += take;
-            if (off + take == R.len && ri + 1 < sg.d.n_runs) R = runs[++ri];
-          }
         }
       }
+    }
+  } else if (warp >= kGatherWarp0 && warp < kEpilogueWarp0) {
+    // ----------------------------------------------------- gather producers
+    // Warp pw loads rows pw, pw + kGatherWarps, ... of every stage; lane l
+    // copies tokens [8l, 8l + 8) of the row (zero-filled past M and for the
+    // padding slots, index -1).  Lane i holds the index of the warp's i-th row
+    // for the NEXT stage (one stage of prefetch hides the table latency).
+    const int pw = warp - kGatherWarp0;
+    const bool lane_on = lane * 8 < tn && !(flags & kFlagSkipA);
+    const char* xa = static_cast<const char*>(args.x);
+    const int my_row = pw + kGatherWarps * lane;  // row slot this lane indexes
+    auto load_idx = [&](const Seg& g, int ks) -> int {
+      return my_row < kBK
+                 ? __ldg(args.gidx + static_cast<int64_t>(g.d.idx_row) * args.kp + ks * kBK +
+                         my_row)
+                 : -1;
+    };
+    bool have = walk.next(args, tab, sg);
+    int ks = have ? sg.ks0 : 0;
+    int idx_next = have ? load_idx(sg, ks) : -1;
+    int gs = 0, prev_stage = -1;
+    while (have) {
+      const int idx_cur = idx_next;
+      const int m0 = sg.mb * tn;
+      // advance to the next stage and prefetch its indices
+      Seg nsg = sg;
+      int nks = ks + 1;
+      bool nhave = true;
+      if (nks >= sg.ks1) {
+        nhave = walk.next(args, tab, nsg);
+        nks = nhave ? nsg.ks0 : 0;
+      }
+      if (nhave) idx_next = load_idx(nsg, nks);
+      const int stage = gs % kStages;
+      mbar_wait(&empty[stage], ((gs / kStages) & 1) ^ 1u);
+      const uint32_t xs = smem_u32(sX + stage * kXBytes) + (lane >> 3) * kChunkBytes;
+      const int tok = m0 + lane * 8;
+      const int tb = max(0, min(8, args.M - tok)) * 2;
+#pragma unroll
+      for (int i = 0; i < (kBK + kGatherWarps - 1) / kGatherWarps; ++i) {
+        const int r = pw + i * kGatherWarps;
+        const int row = __shfl_sync(0xffffffffu, idx_cur, i);
+        if (r < kBK && lane_on) {
+          const uint32_t bytes = row >= 0 ? static_cast<uint32_t>(tb) : 0u;
+          const char* src = bytes ? xa + (static_cast<int64_t>(row) * args.ld_x + tok) * 2 : xa;
+          cp_async_16(xs + r * 128 + (((lane & 7) ^ (r & 7)) << 4), src, bytes);
+        }
+      }
+      cp_async_commit();
+      if (prev_stage >= 0) {
+        cp_async_wait<1>();
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&full[prev_stage]);
+      }
+      prev_stage = stage;
+      ++gs;
+      sg = nsg;
+      ks = nks;
+      have = nhave;
+    }
+    if (prev_stage >= 0) {
+      cp_async_wait<0>();
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&full[prev_stage]);
     }
   } else if (warp == kMmaWarp) {
     // ---------------------------------------------------------- MMA issuer
@@ -429,10 +464,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp >= kEpilogueWarp0) {
     // ------------------------------------------------------------ epilogue
     // Warp w owns TMEM lanes 32*(w%4).. (output columns c of the tile) and
-    // token half h = (w-4)/4 of the 256-token unit.
+    // token half h of the unit.
     const int q = warp & 3;
     const int h = (warp - kEpilogueWarp0) >> 2;
     const int c = q * 32 + lane;  // output column within the 128-wide sub-tile
+    const int ntok = min(128, tn - h * 128);
     const int64_t ws_slot = static_cast<int64_t>(kBN) * kTileN;
     int j = 0;
     while (walk.next(args, tab, sg)) {
@@ -446,7 +482,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const bool warp_full = q * 32 + 32 <= sg.d.width && args.rowmap == nullptr;
       const int crow = sg.d.out_row + c;
       const int orow = row_live ? (args.rowmap ? __ldg(args.rowmap + crow) : crow) : 0;
-      const int tok0 = sg.mb * kTileN + h * 128;
+      const int tok0 = sg.mb * tn + h * 128;
       uint8_t* stg = sStg + (warp - kEpilogueWarp0) * kStgBytes;
       if (sg.kind == kSegHead) {
         // publish the head partial for the next CTA, which finishes this unit
@@ -465,7 +501,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           add = args.ws + (blockIdx.x - 1) * ws_slot + static_cast<int64_t>(c) * kTileN + h * 128;
         }
         epilogue_rows(args, &map_out, stg, t0, lane, orow, row_live, warp_full,
-                      sg.d.out_row + q * 32, tok0, add);
+                      sg.d.out_row + q * 32, tok0, ntok, add);
         if (sg.kind == kSegTail) {
           named_bar_sync(kEpiBarrier, kEpiThreads);
           if (warp == kEpilogueWarp0 && lane == 0) args.ws_flags[blockIdx.x - 1] = 0;
@@ -499,11 +535,11 @@ cudaError_t configure_gemm_kernels() {
                               kSmemBytes);
 }
 
-cudaError_t launch_tw_gemm(const CUtensorMap& map_x, const CUtensorMap& map_x8,
-                           const CUtensorMap& map_pay, const CUtensorMap& map_out,
+cudaError_t launch_tw_gemm(const CUtensorMap& map_pay, const CUtensorMap& map_out,
                            const GemmArgs& args, int in_dtype, int grid, cudaStream_t stream) {
   if (args.n_units <= 0) return cudaSuccess;
-  const uint32_t idesc = umma_idesc_f16(kBN, kTileN, in_dtype == kBF16 ? 1u : 0u,
+  if (args.tn < 64 || args.tn > kTileN || args.tn % 64 != 0) return cudaErrorInvalidValue;
+  const uint32_t idesc = umma_idesc_f16(kBN, args.tn, in_dtype == kBF16 ? 1u : 0u,
                                         /*a (payload) K-major*/ 0u, /*b (X) MN-major*/ 1u);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
@@ -515,7 +551,7 @@ cudaError_t launch_tw_gemm(const CUtensorMap& map_x, const CUtensorMap& map_x8,
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, tw_gemm_kernel, map_x, map_x8, map_pay, map_out, args, idesc);
+  return cudaLaunchKernelEx(&cfg, tw_gemm_kernel, map_pay, map_out, args, idesc);
 }
 
 }  // namespace tw

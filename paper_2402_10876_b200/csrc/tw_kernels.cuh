@@ -12,7 +12,6 @@ enum DType : int32_t { kF32 = 0, kF16 = 1, kBF16 = 2 };
 constexpr int kTN = 256;  // tokens per work unit            (UMMA N, TMEM columns)
 constexpr int kBN = 128;  // output columns per sub-tile     (UMMA M, TMEM lanes)
 constexpr int kBK = 64;   // kept rows per stage   (one 128-byte swizzle row of 16-bit data)
-constexpr int kRunAlign = 8;  // row-group padding: one 1 KB swizzle atom of 8 rows
 
 // One 128-column slice of a TW tile (UMMA M).  Tiles of width <= 128 are one
 // sub-tile (narrower ones zero-padded); wider tiles (g > 128) are split into
@@ -24,32 +23,24 @@ struct SubTile {
   int32_t width;      // live output columns of this slice (<= kBN)
   int32_t out_row;    // first condensed output column == row of C'^T
   int32_t kept;       // K'_i (kept rows), for accounting and LPT ordering
-  int32_t stage_off;  // first stage of this sub-tile inside one 128-token block
-  int32_t run_off;    // first entry of this tile's runs in GemmArgs::runs
-  int32_t n_runs;     // runs covering the tile's (padded) K sequence
-  int32_t pad0, pad1, pad2;
-};
-
-// A contiguous stretch of the grouped input layout feeding one tile:
-// tile sequence positions [seq_off, seq_off + len) are grouped-input rows
-// [row, row + len).  len and offsets are multiples of kRunAlign.
-struct RunDesc {
-  int32_t seq_off;
-  int32_t row;
-  int32_t len;
-  int32_t pad;
+  int32_t stage_off;  // first stage of this sub-tile inside one token block
+  int32_t pad0, pad1, pad2, pad3, pad4;
 };
 
 struct GemmArgs {
   const SubTile* subtiles;  // [n_sub] in visiting order inside one token block (LPT)
-  const RunDesc* runs;      // per-tile run lists
+  const void* x;            // activations A^T [K][ld_x] (tokens contiguous), fp16/bf16
+  int64_t ld_x;             // elements between A^T rows (multiple of 8)
+  const int32_t* gidx;      // [n_tiles][kp] kept rows of every tile, -1 = zero padding
+  int32_t kp;               // gather-table row length (multiple of kBK)
+  int32_t tn;               // tokens per unit (64, 128, 192 or 256)
   const int32_t* rowmap;    // [n_cond] condensed col -> output row; nullptr = identity
   void* out;                // C'^T, rows = output columns, M contiguous
   int64_t ld_out;           // elements between output rows
   int32_t out_dtype;        // DType
   int32_t M;
   int32_t n_sub;
-  int32_t n_mblk;           // ceil(M / kTN)
+  int32_t n_mblk;           // ceil(M / tn)
   int32_t n_units;          // n_sub * n_mblk
   int32_t flags;            // diagnostics (kFlag*); 0 in production
   int32_t spm;              // stages per token block (sum of kp_steps)
@@ -66,13 +57,10 @@ constexpr int32_t kFlagSkipA = 1;       // do not load the activations
 constexpr int32_t kFlagSkipStore = 2;   // do not write the output
 constexpr int32_t kFlagSkipMma = 4;     // do not issue tcgen05.mma
 
-// K1: persistent warp-specialised TW GEMM (tcgen05 + TMA).
-//   map_x   : grouped input X, box {64 tokens, 64 rows}, 128-B swizzle
-//   map_x8  : grouped input X, box {64 tokens, 8 rows} (run boundaries)
+// K1: persistent warp-specialised TW GEMM (tcgen05 + TMA + cp.async gather).
 //   map_pay : payload [n_sub * kBN][Kp], box {64 k, kBN rows}, 128-B swizzle
 //   map_out : C'^T, box {32 tokens, 32 rows}, 64-B (16-bit) / 128-B (fp32) swizzle
-cudaError_t launch_tw_gemm(const CUtensorMap& map_x, const CUtensorMap& map_x8,
-                           const CUtensorMap& map_pay, const CUtensorMap& map_out,
+cudaError_t launch_tw_gemm(const CUtensorMap& map_pay, const CUtensorMap& map_out,
                            const GemmArgs& args, int in_dtype, int grid, cudaStream_t stream);
 
 // Raise the dynamic shared-memory limit of every K1 instance (call once per
@@ -81,11 +69,11 @@ cudaError_t configure_gemm_kernels();
 
 // K2: TEW residual, C'^T[urow(c)] (+)= sum_r A^T[r] * v over overlay column c.
 struct ResidualArgs {
-  const void* at;           // grouped input (rows already mapped to grouped space)
+  const void* at;           // activations A^T [K][ld_at]
   int64_t ld_at;
   int32_t in_dtype;
   const int32_t* col_start; // [n_cols + 1] CSC pointers into rows / vals
-  const int32_t* rows;      // [nnz] grouped-input rows
+  const int32_t* rows;      // [nnz] K rows
   const float* vals;        // [nnz]
   const int32_t* out_rows;  // [n_cols] output row (union position)
   const int32_t* accumulate;// [n_cols] 1 = add onto TW result, 0 = overwrite
@@ -102,34 +90,12 @@ cudaError_t launch_transpose_cast(const void* a, int32_t a_dtype, int64_t M, int
                                   int64_t lda, void* at, int32_t at_dtype, int64_t ld_at,
                                   cudaStream_t stream);
 
-// K4g: build the grouped input X (R x M, pitch ld_dst) from activations.
-//   src_km == 0: src is A (M x K, pitch ld_src);  src_km == 1: src is A^T (K x M).
-//   Every copy of source row k (csr_rows[csr_ptr[k] .. csr_ptr[k+1])) receives
-//   that row; rows listed in zero_rows are zero-filled.
-struct PrepArgs {
-  const void* src;
-  int32_t src_dtype;
-  int32_t src_km;
-  int64_t ld_src;
-  int64_t M;
-  int64_t K;
-  void* dst;
-  int32_t dst_dtype;
-  int64_t ld_dst;
-  const int32_t* csr_ptr;    // [K + 1]
-  const int32_t* csr_rows;   // destination rows of each source row
-  const int32_t* zero_rows;  // destination rows that are zero
-  int32_t n_zero;
-};
-cudaError_t launch_prepare_input(const PrepArgs& args, cudaStream_t stream);
-
-// Payload build: packed transposed fp32 CTO payload -> padded [n_sub*kBN][Kp] fp16/bf16,
-// K positions reordered to each tile's grouped sequence.
+// Payload build: packed transposed fp32 CTO payload -> padded [n_sub*kBN][Kp] fp16/bf16
+// (kept-row order, as formats.py:200 stores it).
 struct PayloadArgs {
   const float* src;          // packed CTO payload (per tile: width x kept, kept contiguous)
   const int64_t* src_base;   // [n_sub] offset of the sub-tile's first column in src
   const int32_t* src_ld;     // [n_sub] kept rows of the tile (row length in src)
-  const int32_t* seq_pos;    // [n_tiles][Kp] kept-row position of each sequence slot, -1 = zero
   const SubTile* subtiles;
   void* dst;
   int32_t dst_dtype;

@@ -151,83 +151,57 @@ class TwPlan:
         macs = self.info.kept_macs_per_token if tew else self.info.kept_macs_per_token - self.info.nnz
         return 2 * int(m) * int(macs)
 
-    # -- input layout -----------------------------------------------------
-    @property
-    def input_rows(self) -> int:
-        """Rows of the grouped input layout X the GEMM reads (see tw_gemm.h)."""
-        return int(self.info.input_rows)
-
-    def input_map(self) -> np.ndarray:
-        """Original K row held by each row of X (-1 for zero rows)."""
-        lib = _native.load_library()
-        out = np.empty(self.input_rows, dtype=np.int32)
-        _native.check(lib.tw_plan_input_map(self._handle, _native.ptr(out, _native.ctypes.c_int32)))
-        return out
-
-    def prepare(self, a=None, *, at=None, out=None, stream=None):
-        """Build the grouped input X (input_rows x M, compute dtype) on the GPU.
+    # -- activations ------------------------------------------------------
+    def prepare(self, a=None, *, at=None, stream=None):
+        """Activations -> the A^T operand of :meth:`run` (K x M, compute dtype).
 
         ``a`` is the reference-layout activation matrix (M x K: numpy, nested
-        list, CPU or CUDA tensor); alternatively ``at`` is a CUDA A^T (K x M).
-        The row copy / transpose / cast runs in the K4g kernel.  The token
-        pitch is padded to a multiple of 8 so the TMA descriptors are legal.
+        list, CPU or CUDA tensor), transposed and cast on the GPU (K4);
+        alternatively ``at`` is a CUDA A^T (K x M), returned as is when it is
+        already in the compute dtype with unit token stride, a token pitch
+        that is a multiple of 8 and a 16-byte aligned base (the layout
+        :meth:`run` writes, so one layer's output feeds the next), else
+        copied into that layout.
         """
         torch = _torch()
         k = self.original_dims[0]
         if (a is None) == (at is None):
             raise InvalidInputError("pass exactly one of a (M x K) or at (K x M)")
-        if at is not None:
-            if not isinstance(at, torch.Tensor) or not at.is_cuda or at.dim() != 2:
-                raise InvalidInputError("at must be a 2-D CUDA tensor (K x M)")
-            if at.shape[0] != k:
-                raise InvalidInputError(f"inner dims disagree: at has {at.shape[0]} rows, "
-                                        f"weights have K={k}")
-            src, layout = at, _native.TW_LAYOUT_KM
-            m = int(at.shape[1])
-        else:
-            if isinstance(a, torch.Tensor):
-                if a.dim() != 2 or a.shape[0] < 1 or a.shape[1] < 1:
-                    raise InvalidInputError(
-                        f"matrix must be 2-D with dims >= 1, got {tuple(a.shape)}")
-                src = a if a.is_cuda else a.to(f"cuda:{self.device}", non_blocking=True)
-            else:
-                src = torch.from_numpy(as_matrix(a)).to(f"cuda:{self.device}")
-            if src.shape[1] != k:
-                raise InvalidInputError(f"inner dims disagree: a has {src.shape[1]} cols, "
-                                        f"weights have K={k}")
-            layout = _native.TW_LAYOUT_MK
-            m = int(src.shape[0])
-        if src.dtype not in (torch.float32, torch.float16, torch.bfloat16):
-            src = src.float()
-        if src.stride(1) != 1:
-            src = src.contiguous()
+        if a is not None:
+            m_k = tuple(a.shape) if isinstance(a, torch.Tensor) else as_matrix(a).shape
+            if len(m_k) != 2 or m_k[1] != k:
+                raise InvalidInputError(
+                    f"inner dims disagree: a has {m_k[-1]} cols, weights have K={k}")
+            return prepare_activations(a, self.compute_dtype, stream=stream)
+        if not isinstance(at, torch.Tensor) or not at.is_cuda or at.dim() != 2:
+            raise InvalidInputError("at must be a 2-D CUDA tensor (K x M)")
+        if at.shape[0] != k:
+            raise InvalidInputError(f"inner dims disagree: at has {at.shape[0]} rows, "
+                                    f"weights have K={k}")
+        if _at_ready(at, self.compute_dtype):
+            return at
+        m = int(at.shape[1])
         ld = (m + 7) // 8 * 8
-        if out is None:
-            out = torch.empty((self.input_rows, ld), dtype=_torch_dtype(self.compute_dtype),
-                              device=src.device)
-        elif out.shape[0] != self.input_rows or out.stride(1) != 1 or out.stride(0) < m:
-            raise InvalidInputError("out must be input_rows x (>= M) with unit token stride")
-        lib = _native.load_library()
-        _native.check(lib.tw_prepare_input(self._handle, src.data_ptr(),
-                                           _DTYPE_CODES[_dtype_name(src.dtype)], layout, m,
-                                           src.stride(0), out.data_ptr(), out.stride(0),
-                                           _native.stream_handle(stream)))
+        out = torch.zeros((k, ld), dtype=_torch_dtype(self.compute_dtype), device=at.device)
+        out[:, :m].copy_(at)
         return out[:, :m]
 
     # -- launches -------------------------------------------------------
     def _check_x(self, x):
         torch = _torch()
         if not isinstance(x, torch.Tensor) or not x.is_cuda:
-            raise InvalidInputError("x must be the CUDA grouped input from TwPlan.prepare()")
-        if x.dim() != 2 or x.shape[0] != self.input_rows:
-            raise InvalidInputError(
-                f"x must be input_rows x M = {self.input_rows} x M, got {tuple(x.shape)}")
+            raise InvalidInputError("x must be a CUDA A^T (K x M) tensor, see TwPlan.prepare()")
+        k = self.original_dims[0]
+        if x.dim() != 2 or x.shape[0] != k:
+            raise InvalidInputError(f"x must be K x M = {k} x M, got {tuple(x.shape)}")
         if x.dtype != _torch_dtype(self.compute_dtype):
             raise InvalidInputError(f"x dtype {x.dtype} != plan compute dtype "
                                     f"{self.compute_dtype}")
-        if x.stride(1) != 1:
-            raise InvalidInputError("x must have unit stride along tokens")
-        return int(x.shape[1]), int(x.stride(0))
+        if not _at_ready(x, self.compute_dtype):
+            raise InvalidInputError("x must have unit token stride, a token pitch that is a "
+                                    "multiple of 8 and a 16-byte aligned base "
+                                    "(use TwPlan.prepare)")
+        return int(x.shape[1]), int(x.stride(0)) if x.shape[0] > 1 else ((int(x.shape[1]) + 7) // 8 * 8)
 
     def _out(self, rows: int, m: int, out, out_dtype):
         torch = _torch()
@@ -239,7 +213,7 @@ class TwPlan:
         return out
 
     def run(self, x, out=None, out_dtype="fp32", stream=None):
-        """C'^T (N' x M) = TW product of the grouped input x; K1 only."""
+        """C'^T (N' x M) = TW product of x = A^T (K x M); K1 only."""
         m, ld = self._check_x(x)
         ct = self._out(self.info.n_condensed, m, out, out_dtype)
         lib = _native.load_library()
@@ -265,13 +239,25 @@ def ctypes_byref(x):
     return _native.ctypes.byref(x)
 
 
-def prepare_activations(a, compute_dtype: str = "fp16", stream=None):
+def _at_ready(x, compute_dtype: str) -> bool:
+    """x is usable as the A^T operand as is (see include/tw_gemm.h)."""
+    if x.dtype != _torch_dtype(compute_dtype) or x.dim() != 2:
+        return False
+    if x.shape[1] > 1 and x.stride(1) != 1:
+        return False
+    pitch_ok = x.shape[0] == 1 or (x.stride(0) % 8 == 0 and x.stride(0) >= x.shape[1])
+    return pitch_ok and x.data_ptr() % 16 == 0
+
+
+def prepare_activations(a, compute_dtype: str = "fp16", stream=None, out=None):
     """Reference-layout activations (M x K) -> device A^T (K x M) in compute dtype.
 
     ``a`` may be a numpy array / nested list (coerced with :func:`as_matrix`
     like the reference, core.py:32-43) or a CUDA tensor.  The transpose and
     cast run in the K4 kernel; the token pitch is padded to a multiple of 8
-    so the TMA descriptor is legal.  Returns a K x M view.
+    so rows stay 16-byte aligned.  Returns a K x M view (of ``out`` when
+    given: a K x M CUDA view with unit token stride and a pitch that is a
+    multiple of 8).
     """
     torch = _torch()
     cd = _dtype_name(compute_dtype)
@@ -286,13 +272,19 @@ def prepare_activations(a, compute_dtype: str = "fp16", stream=None):
     else:
         src = torch.from_numpy(as_matrix(a)).cuda()
     m, k = src.shape
-    ld = (m + 7) // 8 * 8
-    at = torch.empty((k, ld), dtype=_torch_dtype(cd), device=src.device)
+    if out is not None:
+        if tuple(out.shape) != (k, m) or out.dtype != _torch_dtype(cd) or not _at_ready(out, cd):
+            raise InvalidInputError("out must be a K x M A^T view in the compute dtype")
+        at = out
+        ld = out.stride(0) if k > 1 else (m + 7) // 8 * 8
+    else:
+        ld = (m + 7) // 8 * 8
+        at = torch.empty((k, ld), dtype=_torch_dtype(cd), device=src.device)
     lib = _native.load_library()
     _native.check(lib.tw_transpose_cast(src.data_ptr(), _DTYPE_CODES[_dtype_name(src.dtype)], m,
                                         k, src.stride(0), at.data_ptr(), _DTYPE_CODES[cd], ld,
                                         _native.stream_handle(stream)))
-    return at[:, :m]
+    return at if out is not None else at[:, :m]
 
 
 # ----------------------------------------------------------------------------
@@ -412,12 +404,7 @@ def schedule_tiles(per_tile_macs: List[int], workers: int, strategy: str = "lpt"
 
 
 def _activations(a, plan: "TwPlan"):
-    """Reference-layout activations -> the plan's grouped input on the GPU."""
-    torch = _torch()
-    k = plan.original_dims[0]
-    m_k = tuple(a.shape) if isinstance(a, torch.Tensor) else as_matrix(a).shape
-    if len(m_k) != 2 or m_k[1] != k:
-        raise InvalidInputError(f"inner dims disagree: a has {m_k[-1]} cols, weights have K={k}")
+    """Reference-layout activations (M x K) -> the plan's A^T operand on the GPU."""
     return plan.prepare(a)
 
 

@@ -11,7 +11,7 @@ if [ -n "${NCU:-1}" ] && [ "${NCU:-1}" != "0" ]; then
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv \
       --log-file gpurun_out/launches_${TAG}.csv python bench.py --steps 3 --warmup 3 > /dev/null 2>&1
   echo "ncu launches rc=$?"
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:tw_gather_gemm \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:tw_gemm_kernel \
       -s 6 -c 3 -o gpurun_out/prof_${TAG} -f python bench.py --steps 3 --warmup 3 > gpurun_out/ncu_full_${TAG}.log 2>&1
   echo "ncu full rc=$?"; tail -3 gpurun_out/ncu_full_${TAG}.log
 fi
