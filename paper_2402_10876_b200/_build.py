@@ -51,7 +51,8 @@ def build_native(force: bool = False, verbose: bool = False) -> Path:
         return LIB
     LIB_DIR.mkdir(exist_ok=True)
     tmp = LIB.with_suffix(".so.tmp")
-    cmd = [nvcc_path(), *NVCC_FLAGS, "-I", str(ROOT / "include"),
+    extra = os.environ.get("TW_NVCC_EXTRA", "").split()
+    cmd = [nvcc_path(), *NVCC_FLAGS, *extra, "-I", str(ROOT / "include"),
            *[str(CSRC / s) for s in SOURCES], "-o", str(tmp)]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")

@@ -125,13 +125,14 @@ struct tw_plan {
   std::vector<std::vector<uint8_t>> tile_rows;  // per tile: K flags
   std::vector<int32_t> tile_first_cond;  // per tile: first condensed column
   int64_t kept_macs = 0;
-  int32_t spm = 0;
+  bool owner = false;                    // n_sub <= SMs: one sub-tile per CTA
+  bool resident = false;                 // owner and every payload fits in smem
+  std::vector<int32_t> cta_first;        // owner mode: [n_sub + 1]
   // device
   SubTile* d_subtiles = nullptr;
+  int32_t* d_cta_first = nullptr;
   int32_t* d_gidx = nullptr;  // [n_tiles][kp] kept rows, -1 padded
   void* d_payload = nullptr;
-  float* d_ws = nullptr;
-  int32_t* d_ws_flags = nullptr;
   CUtensorMap map_pay;
   // TEW overlay
   bool has_overlay = false;
@@ -146,8 +147,8 @@ struct tw_plan {
   int32_t* d_ov_acc = nullptr;
 
   ~tw_plan() {
-    for (void* p : {(void*)d_subtiles, (void*)d_gidx, d_payload, (void*)d_ws,
-                    (void*)d_ws_flags, (void*)d_union_rowmap, (void*)d_ov_start, (void*)d_ov_rows, (void*)d_ov_vals,
+    for (void* p : {(void*)d_subtiles, (void*)d_cta_first, (void*)d_gidx, d_payload,
+                    (void*)d_union_rowmap, (void*)d_ov_start, (void*)d_ov_rows, (void*)d_ov_vals,
                     (void*)d_ov_out, (void*)d_ov_acc})
       if (p) cudaFree(p);
   }
@@ -293,14 +294,46 @@ int tw_plan_create_cto(tw_plan** out, int32_t k, int32_t n, int32_t g, int32_t n
     base2[i] = src_base[order[i]];
     ld2[i] = src_ld[order[i]];
   }
-  plan->spm = off;
+  (void)off;
+
+  // Owner-mode split: sub-tile s gets c_s CTAs, c_s proportional to its
+  // k-steps (the per-token cost of its gather and MMA), largest remainder,
+  // at least one each.  Mirrors the LPT balancing of executor.py:206-227.
+  const int G = plan->sm_count;
+  plan->owner = plan->n_sub <= G;
+  if (plan->owner) {
+    std::vector<int32_t> c(plan->n_sub, 1);
+    int64_t w = 0;
+    for (const SubTile& st : plan->subtiles) w += st.kp_steps;
+    std::vector<std::pair<double, int>> frac;
+    int used = 0;
+    for (int i = 0; i < plan->n_sub; ++i) {
+      const double q = (double)G * plan->subtiles[i].kp_steps / (double)w;
+      c[i] = std::max(1, (int)q);
+      used += c[i];
+      frac.push_back({q - (int)q, i});
+    }
+    std::stable_sort(frac.begin(), frac.end(),
+                     [](const std::pair<double, int>& a, const std::pair<double, int>& b) {
+                       return a.first > b.first;
+                     });
+    for (size_t t = 0; used < G && t < frac.size(); ++t, ++used) c[frac[t].second] += 1;
+    while (used > G) {  // only when the max(1, .) floor overshot
+      int big = (int)(std::max_element(c.begin(), c.end()) - c.begin());
+      c[big] -= 1;
+      --used;
+    }
+    plan->cta_first.assign(plan->n_sub + 1, 0);
+    for (int i = 0; i < plan->n_sub; ++i) plan->cta_first[i + 1] = plan->cta_first[i] + c[i];
+    int max_steps = 0;
+    for (const SubTile& st : plan->subtiles) max_steps = std::max(max_steps, (int)st.kp_steps);
+    plan->resident = max_steps <= kResSteps && !env_int("TW_NO_RESIDENT", 0);
+  }
 
   if (int st = upload(&plan->d_subtiles, plan->subtiles, s)) return st;
   if (int st = upload(&plan->d_gidx, gidx, s)) return st;
-  // stream-K workspace: one [kBN][kTN] fp32 partial + flag per CTA
-  TW_CUDA(cudaMalloc(&plan->d_ws, (size_t)plan->sm_count * kBN * kTN * sizeof(float)));
-  TW_CUDA(cudaMalloc(&plan->d_ws_flags, (size_t)plan->sm_count * sizeof(int32_t)));
-  TW_CUDA(cudaMemsetAsync(plan->d_ws_flags, 0, (size_t)plan->sm_count * sizeof(int32_t), s));
+  if (plan->owner)
+    if (int st = upload(&plan->d_cta_first, plan->cta_first, s)) return st;
 
   int64_t* d_src_base = nullptr;
   int32_t* d_src_ld = nullptr;
@@ -444,44 +477,17 @@ static int check_io(const tw_plan* p, const void* x, int64_t m, int64_t ld_x, co
   return check_dtype(out_dtype);
 }
 
-// Tokens per work unit.  Units (token block x sub-tile) are strided over
-// min(units, SMs) persistent CTAs; the busiest CTA's ingress (payload 128 B +
-// activations tn * 2 B per kept row and stage, in 128-byte units) plus one
-// exposed epilogue sets the time.  Narrower units add CTAs when a layer has
-// fewer 256-token units than SMs, at the price of reloading the payload more
-// often; pick the width with the smallest busiest-CTA estimate.
-static int pick_tokens_per_unit(const tw_plan* p, int64_t m) {
-  const int forced = env_int("TW_TN", 0);
-  if (forced == 64 || forced == 128 || forced == 192 || forced == 256) return forced;
-  int best_tn = kTN;
-  double best = 0;
-  for (int tn : {256, 192, 128}) {
-    const int64_t n_mblk = (m + tn - 1) / tn;
-    const int64_t units = n_mblk * p->n_sub;
-    const int grid = (int)std::min<int64_t>(units, p->sm_count);
-    std::vector<double> load(grid, 0.0);
-    for (int64_t u = 0; u < units; ++u)
-      load[u % grid] += (double)p->subtiles[u % p->n_sub].kp_steps * (128 + tn);
-    const double t = *std::max_element(load.begin(), load.end()) + 4.8 * tn;
-    if (tn == 256 || t < best * 0.97) {
-      if (tn == 256 || t < best) {
-        best = t;
-        best_tn = tn;
-      }
-    }
-  }
-  return best_tn;
-}
-
 static int run_tw(const tw_plan* p, const void* x, int64_t m, int64_t ld_x, void* ct,
                   int64_t ld_ct, int32_t out_dtype, const int32_t* rowmap, int64_t out_rows,
                   cudaStream_t s) {
   GemmArgs a{};
   a.subtiles = p->d_subtiles;
+  a.cta_first = p->d_cta_first;
   a.x = x;
   a.ld_x = ld_x;
   a.gidx = p->d_gidx;
   a.kp = p->kp;
+  a.in_dtype = p->dtype;
   a.rowmap = rowmap;
   a.out = ct;
   a.ld_out = ld_ct;
@@ -492,37 +498,32 @@ static int run_tw(const tw_plan* p, const void* x, int64_t m, int64_t ld_x, void
   a.trace = g_trace;
   const int esz = out_dtype == kF32 ? 4 : 2;
   a.vec_ok = ((ld_ct * esz) % 16 == 0 && reinterpret_cast<uintptr_t>(ct) % 16 == 0) ? 1 : 0;
-  // condensed output: 32 x 32 blocks leave through TMA 2-D stores
+  // condensed 16-bit output: 32 x 32 blocks leave through TMA 2-D stores
   CUtensorMap map_out;
   std::memset(&map_out, 0, sizeof(map_out));
   a.use_tma_store = 0;
-  if (a.vec_ok && rowmap == nullptr && !env_int("TW_NO_TMA_STORE", 0)) {
+  if (esz == 2 && a.vec_ok && rowmap == nullptr && !env_int("TW_NO_TMA_STORE", 0)) {
     if (make_map_2d(&map_out, ct, out_dtype, (uint64_t)m, (uint64_t)out_rows, (uint64_t)ld_ct,
-                    32, 32, esz == 4 ? 128 : 64) == TW_OK)
+                    32, 32, 64) == TW_OK)
       a.use_tma_store = 1;
     g_last_error.clear();
   }
-  // Work split: whole units strided over the CTAs, or (opt-in, 256-token
-  // units) stream-K with equal stage ranges (each range must hold the longest
-  // unit so a unit is split at most once).
-  const bool streamk = env_int("TW_STREAMK", 0) != 0;
-  a.tn = streamk ? kTN : pick_tokens_per_unit(p, m);
-  a.n_mblk = (int32_t)((m + a.tn - 1) / a.tn);
-  a.n_units = a.n_sub * a.n_mblk;
-  int grid = std::min(a.n_units, p->sm_count);
-  a.spm = p->spm;
-  a.split = 0;
-  a.ws = p->d_ws;
-  a.ws_flags = p->d_ws_flags;
-  if (streamk && a.n_units > p->sm_count) {
-    const int64_t total = (int64_t)a.n_mblk * p->spm;
-    int max_kp = 1;
-    for (const SubTile& st : p->subtiles) max_kp = std::max(max_kp, (int)st.kp_steps);
-    grid = (int)std::min<int64_t>(p->sm_count, total / max_kp);
-    grid = std::max(grid, 1);
-    a.split = 1;
+  // Owner mode (one sub-tile + token range per CTA) whenever the sub-tiles fit
+  // on the SMs; otherwise 256-token units strided over the CTAs.
+  int grid;
+  if (p->owner && !env_int("TW_STRIDED", 0)) {
+    a.owner = 1;
+    a.gran = env_int("TW_GRAN", 64);
+    if (a.gran != 16 && a.gran != 32 && a.gran != 64) a.gran = 64;
+    a.split_single = env_int("TW_SPLIT1", 0);
+    grid = p->cta_first.back();
+  } else {
+    a.owner = 0;
+    a.n_units = (int32_t)(p->n_sub * ((m + kTN - 1) / kTN));
+    grid = std::min(a.n_units, p->sm_count);
   }
-  TW_CUDA(launch_tw_gemm(p->map_pay, map_out, a, p->dtype, grid, s));
+  const bool resident = a.owner && p->resident;
+  TW_CUDA(launch_tw_gemm(p->map_pay, map_out, a, resident, grid, s));
   return TW_OK;
 }
 

@@ -27,28 +27,31 @@ struct SubTile {
   int32_t pad0, pad1, pad2, pad3, pad4;
 };
 
+// Resident-payload kernel: a sub-tile's whole payload (<= kResSteps k-steps,
+// i.e. K' <= 448) stays in shared memory for all of the CTA's tokens.
+constexpr int kResSteps = 7;
+
 struct GemmArgs {
-  const SubTile* subtiles;  // [n_sub] in visiting order inside one token block (LPT)
+  const SubTile* subtiles;  // [n_sub] in visiting order (LPT)
+  const int32_t* cta_first; // owner mode: [n_sub + 1] first CTA of every sub-tile
   const void* x;            // activations A^T [K][ld_x] (tokens contiguous), fp16/bf16
   int64_t ld_x;             // elements between A^T rows (multiple of 8)
   const int32_t* gidx;      // [n_tiles][kp] kept rows of every tile, -1 = zero padding
   int32_t kp;               // gather-table row length (multiple of kBK)
-  int32_t tn;               // tokens per unit (64, 128, 192 or 256)
+  int32_t in_dtype;         // kF16 / kBF16 (activations and payload)
   const int32_t* rowmap;    // [n_cond] condensed col -> output row; nullptr = identity
   void* out;                // C'^T, rows = output columns, M contiguous
   int64_t ld_out;           // elements between output rows
   int32_t out_dtype;        // DType
   int32_t M;
   int32_t n_sub;
-  int32_t n_mblk;           // ceil(M / tn)
-  int32_t n_units;          // n_sub * n_mblk
+  int32_t n_units;          // strided mode: n_sub * ceil(M / kTN)
+  int32_t owner;            // 1 = one sub-tile + token range per CTA, 0 = strided units
+  int32_t gran;             // owner mode: token-range granularity (16, 32 or 64)
+  int32_t split_single;     // owner mode: split a one-unit range into two units
   int32_t flags;            // diagnostics (kFlag*); 0 in production
-  int32_t spm;              // stages per token block (sum of kp_steps)
-  int32_t split;            // 1 = stream-K ranges, 0 = whole units strided by gridDim.x
-  float* ws;                // stream-K partials, gridDim.x x [kBN][kTN] fp32
-  int32_t* ws_flags;        // gridDim.x publish flags (0 between launches)
   int32_t vec_ok;           // output rows 16-byte aligned: vector stores allowed
-  int32_t use_tma_store;    // map_out valid: 32 x 32 output blocks via TMA 2-D stores
+  int32_t use_tma_store;    // map_out valid (16-bit output): 32 x 32 blocks via TMA stores
   long long* trace;         // optional per-CTA clock64 trace (4096 entries per CTA)
 };
 
@@ -59,9 +62,10 @@ constexpr int32_t kFlagSkipMma = 4;     // do not issue tcgen05.mma
 
 // K1: persistent warp-specialised TW GEMM (tcgen05 + TMA + cp.async gather).
 //   map_pay : payload [n_sub * kBN][Kp], box {64 k, kBN rows}, 128-B swizzle
-//   map_out : C'^T, box {32 tokens, 32 rows}, 64-B (16-bit) / 128-B (fp32) swizzle
+//   map_out : C'^T (16-bit), box {32 tokens, 32 rows}, 64-B swizzle
+//   resident: payload held in shared memory (owner mode, kp_steps <= kResSteps)
 cudaError_t launch_tw_gemm(const CUtensorMap& map_pay, const CUtensorMap& map_out,
-                           const GemmArgs& args, int in_dtype, int grid, cudaStream_t stream);
+                           const GemmArgs& args, bool resident, int grid, cudaStream_t stream);
 
 // Raise the dynamic shared-memory limit of every K1 instance (call once per
 // device before launching or capturing).

@@ -59,6 +59,10 @@ def main():
         if len(e):
             ends.append(e[-1, 1] - t0)
             epi.extend((e[:, 1] - e[:, 0]).tolist())
+        if c == 0:
+            iss = np.where(t[c, 0:ns] > 0, t[c, 0:ns] - t0, 0)
+            f = ful[:ns] - t0
+            print("  cta0 issue/full/lat: " + " ".join(f"{int(a)}/{int(b)}/{int(b - a)}" for a, b in zip(iss[:16], f[:16])))
         if c < 4 or c in (74, 147):
             f = ful[:ns] - t0
             print(f" cta {c}: stages {ns}, full at {f[:3].tolist()}..{f[-2:].tolist()}, "

@@ -23,7 +23,7 @@ using namespace tw;
 #define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("%s: %s\n", #x, cudaGetErrorString(e)); exit(1);} } while (0)
 
 constexpr int kStage = 32768;
-constexpr int kSt = 4;
+constexpr int kSt = 6;  // max stages (runtime nst <= kSt)
 constexpr int kNRows = 1536;
 
 __device__ __forceinline__ void load_rows(int* s_rows, const int* rows) {
@@ -32,7 +32,7 @@ __device__ __forceinline__ void load_rows(int* s_rows, const int* rows) {
 
 // mode 0 dense TMA, 1 gather4
 __global__ void tma_ring(const __grid_constant__ CUtensorMap map, const int* rows, int M,
-                         int iters, int issuers, int mode, long long* cycles) {
+                         int iters, int issuers, int mode, long long* cycles, int nst) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   __shared__ uint64_t bar[kSt];
@@ -40,15 +40,15 @@ __global__ void tma_ring(const __grid_constant__ CUtensorMap map, const int* row
   load_rows(s_rows, rows);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
-    for (int s = 0; s < kSt; ++s) mbar_init(&bar[s], 1);
+    for (int s = 0; s < nst; ++s) mbar_init(&bar[s], 1);
     fence_barrier_init();
   }
   __syncthreads();
   const long long t0 = clock64();
   if (lane == 0 && warp < issuers) {
-    for (int it = 0; it < iters + kSt; ++it) {
-      const int stage = it % kSt;
-      if (it >= kSt) mbar_wait(&bar[stage], ((it / kSt) - 1) & 1);
+    for (int it = 0; it < iters + nst; ++it) {
+      const int stage = it % nst;
+      if (it >= nst) mbar_wait(&bar[stage], ((it / nst) - 1) & 1);
       if (it >= iters) continue;
       if (warp == 0) mbar_arrive_expect_tx(&bar[stage], kStage);
       const int kb = ((it + blockIdx.x * 7) * 64) % (kNRows - 64);
@@ -72,7 +72,7 @@ __global__ void tma_ring(const __grid_constant__ CUtensorMap map, const int* row
 }
 
 __global__ void cp_ring(const __half* at, int64_t ld, const int* rows, int M, int iters,
-                        long long* cycles) {
+                        long long* cycles, int nst) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   __shared__ int s_rows[kNRows];
@@ -81,7 +81,7 @@ __global__ void cp_ring(const __half* at, int64_t ld, const int* rows, int M, in
   const int tid = threadIdx.x, nthr = blockDim.x;
   const long long t0 = clock64();
   for (int it = 0; it < iters; ++it) {
-    const int stage = it % kSt;
+    const int stage = it % nst;
     const int kb = ((it + blockIdx.x * 7) * 64) % (kNRows - 64);
     const int m0 = ((it * 3 + blockIdx.x) * 256) % M;
     const uint32_t base = smem_u32(smem + stage * kStage);
@@ -94,7 +94,9 @@ __global__ void cp_ring(const __half* at, int64_t ld, const int* rows, int M, in
       cp_async_16(dst, at + static_cast<int64_t>(row) * ld + m0 + j * 8, 16);
     }
     asm volatile("cp.async.commit_group;");
-    asm volatile("cp.async.wait_group 2;" ::: "memory");
+    if (nst <= 2) asm volatile("cp.async.wait_group 0;" ::: "memory");
+    else if (nst <= 4) asm volatile("cp.async.wait_group 2;" ::: "memory");
+    else asm volatile("cp.async.wait_group 4;" ::: "memory");
   }
   asm volatile("cp.async.wait_group 0;");
   __syncthreads();
@@ -140,7 +142,8 @@ int main() {
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
-  for (int grid : {148, 96}) {
+  char name[64];
+  for (int nst : {2, 4, 6}) for (int grid : {148, 96}) {
     auto report = [&](const char* name) {
       float ms;
       cudaEventElapsedTime(&ms, e0, e1);
@@ -151,32 +154,32 @@ int main() {
       printf("grid %3d %-26s %8.1f GB/s  %6.1f B/cyc/SM (median)\n", grid, name,
              bytes / ms / 1e6, (double)iters * kStage / c[grid / 2]);
     };
-    char name[64];
     for (int rep = 0; rep < 2; ++rep) {
       cudaEventRecord(e0);
-      tma_ring<<<grid, 128, smem>>>(dmap, drows, M, iters, 1, 0, cyc);
+      tma_ring<<<grid, 128, smem>>>(dmap, drows, M, iters, 1, 0, cyc, nst);
       cudaEventRecord(e1);
       CK(cudaDeviceSynchronize());
     }
-    report("dense tma 2d");
-    for (int is : {1, 2, 4, 8}) {
+    snprintf(name, 64, "dense tma 2d st%d", nst);
+    report(name);
+    for (int is : {8}) {
       for (int rep = 0; rep < 2; ++rep) {
         cudaEventRecord(e0);
-        tma_ring<<<grid, 32 * std::max(is, 4), smem>>>(gmap, drows, M, iters, is, 1, cyc);
+        tma_ring<<<grid, 32 * std::max(is, 4), smem>>>(gmap, drows, M, iters, is, 1, cyc, nst);
         cudaEventRecord(e1);
         CK(cudaDeviceSynchronize());
       }
-      snprintf(name, 64, "gather4 %d issuers", is);
+      snprintf(name, 64, "gather4 %d issuers st%d", is, nst);
       report(name);
     }
     for (int w : {4, 8, 16}) {
       for (int rep = 0; rep < 2; ++rep) {
         cudaEventRecord(e0);
-        cp_ring<<<grid, 32 * w, smem>>>(at, M, drows, M, iters, cyc);
+        cp_ring<<<grid, 32 * w, smem>>>(at, M, drows, M, iters, cyc, nst);
         cudaEventRecord(e1);
         CK(cudaDeviceSynchronize());
       }
-      snprintf(name, 64, "cp.async %d warps", w);
+      snprintf(name, 64, "cp.async %d warps st%d", w, nst);
       report(name);
     }
   }
