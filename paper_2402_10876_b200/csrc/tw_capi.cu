@@ -6,6 +6,9 @@
 #include "../../include/tw_gemm.h"
 #include "tw_kernels.cuh"
 
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -114,6 +117,16 @@ int upload(T** dptr, const std::vector<T>& host, cudaStream_t s) {
 
 int32_t round_up(int32_t v, int32_t a) { return (v + a - 1) / a * a; }
 
+// IEEE binary16 / bfloat16 bits of a float, round to nearest even.
+uint32_t float_to_half_bits(float f) {
+  const __half h = __float2half_rn(f);
+  return (uint32_t)__half_as_ushort(h);
+}
+uint32_t float_to_bf16_bits(float f) {
+  const __nv_bfloat16 h = __float2bfloat16_rn(f);
+  return (uint32_t)__bfloat16_as_ushort(h);
+}
+
 }  // namespace
 
 struct tw_plan {
@@ -145,11 +158,13 @@ struct tw_plan {
   float* d_ov_vals = nullptr;
   int32_t* d_ov_out = nullptr;
   int32_t* d_ov_acc = nullptr;
+  uint32_t* d_ov_rv = nullptr;         // K2 lists: row << 16 | 16-bit value
+  int32_t ov_block_tokens = 0, ov_col_groups = 1, ov_max_group_nnz = 0;
 
   ~tw_plan() {
     for (void* p : {(void*)d_subtiles, (void*)d_cta_first, (void*)d_gidx, d_payload,
                     (void*)d_union_rowmap, (void*)d_ov_start, (void*)d_ov_rows, (void*)d_ov_vals,
-                    (void*)d_ov_out, (void*)d_ov_acc})
+                    (void*)d_ov_out, (void*)d_ov_acc, (void*)d_ov_rv})
       if (p) cudaFree(p);
   }
 };
@@ -395,6 +410,11 @@ int tw_plan_attach_overlay(tw_plan* p, int32_t k, int32_t n, int64_t nnz, const 
   for (size_t i = 0; i < uni.size(); ++i) pos_of[uni[i]] = (int32_t)i;
   std::vector<int32_t> rowmap(p->n_cond);
   for (int32_t i = 0; i < p->n_cond; ++i) rowmap[i] = pos_of[p->cond_cols[i]];
+  // K2 visits overlay columns in descending-nnz order (lane groups of a warp
+  // then finish together); results do not depend on the order.
+  std::stable_sort(ov_cols.begin(), ov_cols.end(), [&](int32_t a, int32_t b) {
+    return col_ptr[a + 1] - col_ptr[a] > col_ptr[b + 1] - col_ptr[b];
+  });
   std::vector<int32_t> start(1, 0), rows, out_rows, acc;
   std::vector<float> vals;
   for (int32_t c : ov_cols) {
@@ -408,8 +428,9 @@ int tw_plan_attach_overlay(tw_plan* p, int32_t k, int32_t n, int64_t nnz, const 
   }
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   for (void* q : {(void*)p->d_union_rowmap, (void*)p->d_ov_start, (void*)p->d_ov_rows,
-                  (void*)p->d_ov_vals, (void*)p->d_ov_out, (void*)p->d_ov_acc})
+                  (void*)p->d_ov_vals, (void*)p->d_ov_out, (void*)p->d_ov_acc, (void*)p->d_ov_rv})
     if (q) cudaFree(q);
+  p->d_ov_rv = nullptr;
   p->d_union_rowmap = nullptr;
   p->d_ov_start = p->d_ov_rows = p->d_ov_out = p->d_ov_acc = nullptr;
   p->d_ov_vals = nullptr;
@@ -419,6 +440,35 @@ int tw_plan_attach_overlay(tw_plan* p, int32_t k, int32_t n, int64_t nnz, const 
   if (int st = upload(&p->d_ov_vals, vals, s)) return st;
   if (int st = upload(&p->d_ov_out, out_rows, s)) return st;
   if (int st = upload(&p->d_ov_acc, acc, s)) return st;
+  // K2 geometry: A^T block of T tokens + the column group's packed list in
+  // shared memory; split columns into more groups until the largest fits.
+  p->ov_block_tokens = 0;
+  const int64_t n_ov = (int64_t)ov_cols.size();
+  int T = 0, groups = 1;
+  if (k <= 65535 && n_ov > 0 && !env_int("TW_RESIDUAL_DIRECT", 0) &&
+      residual_geometry(k, (int64_t)rows.size() * 4, &T, &groups)) {
+    const int64_t limit = 227 * 1024 - (int64_t)k * T * 2;
+    for (;; ++groups) {
+      int64_t worst = 0;
+      for (int g = 0; g < groups; ++g) {
+        const int64_t c0 = (int64_t)g * n_ov / groups, c1 = (int64_t)(g + 1) * n_ov / groups;
+        worst = std::max<int64_t>(worst, start[c1] - start[c0]);
+      }
+      if (worst * 4 <= limit || groups >= n_ov) {
+        p->ov_max_group_nnz = (int32_t)worst;
+        break;
+      }
+    }
+    if ((int64_t)p->ov_max_group_nnz * 4 <= limit) {
+      p->ov_block_tokens = T;
+      p->ov_col_groups = groups;
+      std::vector<uint32_t> rv(rows.size());
+      for (size_t e = 0; e < rows.size(); ++e)
+        rv[e] = ((uint32_t)rows[e] << 16) |
+                (p->dtype == kBF16 ? float_to_bf16_bits(vals[e]) : float_to_half_bits(vals[e]));
+      if (int st = upload(&p->d_ov_rv, rv, s)) return st;
+    }
+  }
   TW_CUDA(cudaStreamSynchronize(s));
   p->union_cols = uni;
   p->n_ov_cols = (int32_t)ov_cols.size();
@@ -541,9 +591,13 @@ int tw_gemm_tew(const tw_plan* p, const void* x, int64_t m, int64_t ld_x, void* 
   if (int st = check_io(p, x, m, ld_x, ct, ld_ct, out_dtype)) return st;
   if (!p->has_overlay) return fail(TW_ERR_INVALID_INPUT, "plan has no overlay attached");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (int st = run_tw(p, x, m, ld_x, ct, ld_ct, out_dtype, p->d_union_rowmap,
-                      (int64_t)p->union_cols.size(), s))
-    return st;
+  // TW_TEW_PARTS (diagnostics): 1 = K1 only, 2 = K2 only, otherwise both
+  const int parts = env_int("TW_TEW_PARTS", 3);
+  if (parts != 2)
+    if (int st = run_tw(p, x, m, ld_x, ct, ld_ct, out_dtype, p->d_union_rowmap,
+                        (int64_t)p->union_cols.size(), s))
+      return st;
+  if (parts == 1) return TW_OK;
   ResidualArgs r{};
   r.at = x;
   r.ld_at = ld_x;
@@ -558,6 +612,11 @@ int tw_gemm_tew(const tw_plan* p, const void* x, int64_t m, int64_t ld_x, void* 
   r.out_dtype = out_dtype;
   r.M = (int32_t)m;
   r.n_cols = p->n_ov_cols;
+  r.K = p->k;
+  r.rv = p->d_ov_rv;
+  r.block_tokens = p->ov_block_tokens;
+  r.col_groups = p->ov_col_groups;
+  r.max_group_nnz = p->ov_max_group_nnz;
   TW_CUDA(launch_tw_residual(r, s));
   return TW_OK;
 }

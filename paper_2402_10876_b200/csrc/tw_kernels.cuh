@@ -86,8 +86,16 @@ struct ResidualArgs {
   int32_t out_dtype;
   int32_t M;
   int32_t n_cols;
+  int32_t K;                // rows of A^T
+  const uint32_t* rv;       // [nnz] row << 16 | 16-bit value; nullptr = direct kernel
+  int32_t block_tokens;     // T of the staged A^T block
+  int32_t col_groups;       // column groups (contiguous in processing order)
+  int32_t max_group_nnz;    // largest group's nnz (shared-memory list size)
 };
 cudaError_t launch_tw_residual(const ResidualArgs& args, cudaStream_t stream);
+// Staged-block geometry of the overlay SpMM for K rows and a list of
+// `list_bytes` bytes: tokens per block and column groups; false = direct path.
+bool residual_geometry(int32_t K, int64_t list_bytes, int* T, int* groups);
 
 // K4: A (M x K, row-major, lda) -> A^T (K x M, ld_at) with a dtype cast.
 cudaError_t launch_transpose_cast(const void* a, int32_t a_dtype, int64_t M, int64_t K,

@@ -57,14 +57,21 @@ def main():
     ap.add_argument("--layers", default="0,1,2")
     ap.add_argument("--sets", type=int, default=4, help="rotating buffer sets (1 = L2-warm)")
     ap.add_argument("--pad", type=int, default=0, help="extra tokens of A^T row pitch")
+    ap.add_argument("--tew", type=float, default=0.0, help="TEW delta (0 = TW)")
     args = ap.parse_args()
     torch.cuda.set_device(0)
     layers = [LAYERS[int(i)] for i in args.layers.split(",")]
     data = []
     for k, n in layers:
         w = tw.round_to(tw.synthetic_matrix(0, k, n, 0), "fp16")
-        _, tsm = tw.prune_tw(w, 0.75, args.g)
-        plans = [tw.TwPlan(tw.encode_cto(tsm)) for _ in range(4)]
+        if args.tew:
+            _, tsm, ov = tw.prune_tew(w, 0.75, args.tew, args.g)
+            plans = [tw.TwPlan(tw.encode_cto(tsm), overlay=ov) for _ in range(4)]
+            for pl in plans:
+                pl.run = pl.run_tew
+        else:
+            _, tsm = tw.prune_tw(w, 0.75, args.g)
+            plans = [tw.TwPlan(tw.encode_cto(tsm)) for _ in range(4)]
         a = tw.round_to(tw.synthetic_matrix(0, args.m, k, 1), "fp16")
         ats = [pl.prepare(torch.from_numpy(a).cuda()) for pl in plans]
         if args.pad:
@@ -75,7 +82,8 @@ def main():
                 buf[:, :at.shape[1]] = at
                 padded.append(buf[:, :at.shape[1]])
             ats = padded
-        outs = [torch.empty((tsm.n_condensed, args.m), dtype=torch.float16, device="cuda")
+        rows = plans[0].info.n_union if args.tew else tsm.n_condensed
+        outs = [torch.empty((rows, args.m), dtype=torch.float16, device="cuda")
                 for _ in range(4)]
         ref = plans[0].run(ats[0]).float()
         data.append((plans, ats, outs, ref))
