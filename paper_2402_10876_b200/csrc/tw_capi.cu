@@ -67,7 +67,7 @@ EncodeTiledFn encode_fn() {
 }
 
 // 2-D tensor map over a row-major [rows][cols] matrix (cols contiguous).
-// swizzle: 0 = none, 64 = 64-byte, 128 = 128-byte.
+// swizzle: 0 = none, 32 / 64 / 128 = that many bytes.
 int make_map_2d(CUtensorMap* map, const void* base, int32_t dtype, uint64_t cols, uint64_t rows,
                 uint64_t pitch_elems, uint32_t box_cols, uint32_t box_rows, int swizzle = 128) {
   EncodeTiledFn fn = encode_fn();
@@ -84,6 +84,7 @@ int make_map_2d(CUtensorMap* map, const void* base, int32_t dtype, uint64_t cols
                   CU_TENSOR_MAP_INTERLEAVE_NONE,
                   swizzle == 128  ? CU_TENSOR_MAP_SWIZZLE_128B
                   : swizzle == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                  : swizzle == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
                                   : CU_TENSOR_MAP_SWIZZLE_NONE,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
@@ -143,7 +144,6 @@ struct tw_plan {
   std::vector<int32_t> cta_first;        // owner mode: [n_sub + 1]
   // device
   SubTile* d_subtiles = nullptr;
-  int32_t* d_cta_first = nullptr;
   int32_t* d_gidx = nullptr;  // [n_tiles][kp] kept rows, -1 padded
   void* d_payload = nullptr;
   CUtensorMap map_pay;
@@ -162,7 +162,7 @@ struct tw_plan {
   int32_t ov_block_tokens = 0, ov_col_groups = 1, ov_max_group_nnz = 0;
 
   ~tw_plan() {
-    for (void* p : {(void*)d_subtiles, (void*)d_cta_first, (void*)d_gidx, d_payload,
+    for (void* p : {(void*)d_subtiles, (void*)d_gidx, d_payload,
                     (void*)d_union_rowmap, (void*)d_ov_start, (void*)d_ov_rows, (void*)d_ov_vals,
                     (void*)d_ov_out, (void*)d_ov_acc, (void*)d_ov_rv})
       if (p) cudaFree(p);
@@ -315,7 +315,7 @@ int tw_plan_create_cto(tw_plan** out, int32_t k, int32_t n, int32_t g, int32_t n
   // k-steps (the per-token cost of its gather and MMA), largest remainder,
   // at least one each.  Mirrors the LPT balancing of executor.py:206-227.
   const int G = plan->sm_count;
-  plan->owner = plan->n_sub <= G;
+  plan->owner = plan->n_sub <= G && G <= kMaxCtas;
   if (plan->owner) {
     std::vector<int32_t> c(plan->n_sub, 1);
     int64_t w = 0;
@@ -347,8 +347,6 @@ int tw_plan_create_cto(tw_plan** out, int32_t k, int32_t n, int32_t g, int32_t n
 
   if (int st = upload(&plan->d_subtiles, plan->subtiles, s)) return st;
   if (int st = upload(&plan->d_gidx, gidx, s)) return st;
-  if (plan->owner)
-    if (int st = upload(&plan->d_cta_first, plan->cta_first, s)) return st;
 
   int64_t* d_src_base = nullptr;
   int32_t* d_src_ld = nullptr;
@@ -532,7 +530,6 @@ static int run_tw(const tw_plan* p, const void* x, int64_t m, int64_t ld_x, void
                   cudaStream_t s) {
   GemmArgs a{};
   a.subtiles = p->d_subtiles;
-  a.cta_first = p->d_cta_first;
   a.x = x;
   a.ld_x = ld_x;
   a.gidx = p->d_gidx;
@@ -548,32 +545,60 @@ static int run_tw(const tw_plan* p, const void* x, int64_t m, int64_t ld_x, void
   a.trace = g_trace;
   const int esz = out_dtype == kF32 ? 4 : 2;
   a.vec_ok = ((ld_ct * esz) % 16 == 0 && reinterpret_cast<uintptr_t>(ct) % 16 == 0) ? 1 : 0;
-  // condensed 16-bit output: 32 x 32 blocks leave through TMA 2-D stores
+  // condensed 16-bit output: 32 x 16 blocks leave through TMA 2-D stores
   CUtensorMap map_out;
   std::memset(&map_out, 0, sizeof(map_out));
   a.use_tma_store = 0;
   if (esz == 2 && a.vec_ok && rowmap == nullptr && !env_int("TW_NO_TMA_STORE", 0)) {
     if (make_map_2d(&map_out, ct, out_dtype, (uint64_t)m, (uint64_t)out_rows, (uint64_t)ld_ct,
-                    32, 32, 64) == TW_OK)
+                    16, 32, 32) == TW_OK)
       a.use_tma_store = 1;
     g_last_error.clear();
   }
   // Owner mode (one sub-tile + token range per CTA) whenever the sub-tiles fit
   // on the SMs; otherwise 256-token units strided over the CTAs.
   int grid;
+  WorkTable work;
   if (p->owner && !env_int("TW_STRIDED", 0)) {
     a.owner = 1;
-    a.gran = env_int("TW_GRAN", 64);
-    if (a.gran != 16 && a.gran != 32 && a.gran != 64) a.gran = 64;
-    a.split_single = env_int("TW_SPLIT1", 0);
+    int gran = env_int("TW_GRAN", 64);
+    if (gran != 16 && gran != 32 && gran != 64) gran = 64;
+    const bool split_single = env_int("TW_SPLIT1", 0) != 0;
     grid = p->cta_first.back();
+    if (grid > kMaxCtas) return fail(TW_ERR_INVALID_INPUT, "owner grid %d > %d", grid, kMaxCtas);
+    // CTA j of sub-tile s (c_s CTAs): tokens cut into c_s ranges on `gran`
+    // boundaries, processed in units of <= kTN tokens with the remainder last
+    // (shortest final epilogue); split_single halves a one-unit range so the
+    // first half's epilogue overlaps the second half's mainloop.
+    const int64_t ch = (m + gran - 1) / gran;
+    for (int sidx = 0; sidx < p->n_sub; ++sidx) {
+      const SubTile& st = p->subtiles[sidx];
+      const int c0 = p->cta_first[sidx], c = p->cta_first[sidx + 1] - c0;
+      for (int j = 0; j < c; ++j) {
+        CtaWork& w = work.w[c0 + j];
+        w.kp_steps = st.kp_steps;
+        w.idx_row = st.idx_row;
+        w.pay_row = st.pay_row;
+        w.width = st.width;
+        w.out_row = st.out_row;
+        const int64_t b = (int64_t)j * ch / c * gran;
+        const int64_t e = std::min<int64_t>(m, (int64_t)(j + 1) * ch / c * gran);
+        const int64_t len = std::max<int64_t>(0, e - b);
+        int64_t n = (len + kTN - 1) / kTN;
+        if (split_single && n == 1 && len >= 2 * gran) n = 2;
+        w.b = (int32_t)b;
+        w.e = (int32_t)std::max(b, e);
+        w.usz = n > 0 ? (int32_t)std::min<int64_t>(kTN, ((len + n - 1) / n + gran - 1) / gran * gran)
+                      : 0;
+      }
+    }
   } else {
     a.owner = 0;
     a.n_units = (int32_t)(p->n_sub * ((m + kTN - 1) / kTN));
     grid = std::min(a.n_units, p->sm_count);
   }
   const bool resident = a.owner && p->resident;
-  TW_CUDA(launch_tw_gemm(p->map_pay, map_out, a, resident, grid, s));
+  TW_CUDA(launch_tw_gemm(p->map_pay, map_out, a, work, resident, grid, s));
   return TW_OK;
 }
 

@@ -69,7 +69,7 @@ constexpr int kChunkBytes = 64 * kBK * 2;            // 64 tokens x 64 rows x 2 
 constexpr int kXBytes = (kTileN / 64) * kChunkBytes; // 32 KB per stage
 constexpr int kPBytes = kBN * kBK * 2;               // 16 KB per k-step of payload
 constexpr int kMaxSmemSub = 32;                      // strided mode: sub-tile table in smem
-constexpr int kStgBytes = 2048;                      // per epilogue warp: [32 rows][64 B]
+constexpr int kStgBytes = 2048;                      // per epilogue warp: 2 x [32 rows][32 B]
 constexpr uint32_t kTmemCols = 2 * kTileN;           // double-buffered 128 x 256 fp32
 constexpr int kMaxItems = (kBK * kTileN / 8 + kGatherThreads - 1) / kGatherThreads;
 static_assert(kEpilogueWarp0 % 4 == 0, "epilogue warps must start a warpgroup (TMEM lane quadrants)");
@@ -95,43 +95,28 @@ struct Seg {
 
 // Deterministic per-CTA unit sequence, identical in every role.
 struct Walker {
-  // owner mode
-  int s, b, e, nu, i, usz;
+  // owner mode: this CTA's sub-tile and token range (host work table)
+  int b, e, nu, i, usz;
+  SubTile d;
   // strided mode
   int u;
   const SubTile* tab;
 
-  __device__ __forceinline__ void init(const GemmArgs& a, const SubTile* table) {
+  __device__ __forceinline__ void init(const GemmArgs& a, const WorkTable& work,
+                                       const SubTile* table) {
     tab = table;
     i = 0;
     if (a.owner) {
-      // sub-tile owned by this CTA: cta_first[s] <= blockIdx.x < cta_first[s + 1]
-      const int cta = blockIdx.x;
-      int lo = 0, hi = a.n_sub;  // invariant: cta_first[lo] <= cta < cta_first[hi]
-      if (cta >= __ldg(a.cta_first + a.n_sub)) {
-        s = -1;
-        nu = 0;
-        return;
-      }
-      while (hi - lo > 1) {
-        const int mid = (lo + hi) >> 1;
-        if (__ldg(a.cta_first + mid) <= cta) lo = mid; else hi = mid;
-      }
-      s = lo;
-      const int c0 = __ldg(a.cta_first + s), c = __ldg(a.cta_first + s + 1) - c0;
-      const int j = cta - c0;
-      const int gr = a.gran;           // token granularity of the ranges
-      const int ch = (a.M + gr - 1) / gr;
-      b = static_cast<int>(static_cast<int64_t>(j) * ch / c) * gr;
-      e = min(a.M, static_cast<int>(static_cast<int64_t>(j + 1) * ch / c) * gr);
-      // Units of usz tokens, the remainder last (shortest final epilogue); the
-      // resident kernel also splits a single-unit range in two so the first
-      // half's epilogue overlaps the second half's mainloop.
-      const int len = e - b;
-      int n = (len + kTileN - 1) / kTileN;
-      if (a.split_single && n == 1 && len >= 2 * gr) n = 2;
-      usz = n > 0 ? min(kTileN, ((len + n - 1) / n + gr - 1) / gr * gr) : 0;
-      nu = n > 0 ? (len + usz - 1) / usz : 0;
+      const CtaWork& w = work.w[blockIdx.x];
+      d.kp_steps = w.kp_steps;
+      d.idx_row = w.idx_row;
+      d.pay_row = w.pay_row;
+      d.width = w.width;
+      d.out_row = w.out_row;
+      b = w.b;
+      e = w.e;
+      usz = w.usz;
+      nu = usz > 0 ? (e - b + usz - 1) / usz : 0;
     } else {
       u = blockIdx.x;
     }
@@ -139,10 +124,10 @@ struct Walker {
   __device__ __forceinline__ bool next(const GemmArgs& a, Seg& g) {
     if (a.owner) {
       if (i >= nu) return false;
-      g.sub = s;
+      g.sub = 0;
       g.ub = b + i * usz;
       g.ue = min(e, g.ub + usz);
-      g.d = tab[s];
+      g.d = d;
       ++i;
       return true;
     }
@@ -166,79 +151,93 @@ __device__ __forceinline__ uint32_t pack2(float a, float b, int32_t dtype) {
   return *reinterpret_cast<const uint32_t*>(&h);
 }
 
+// Keeps the compiler from hoisting reads of tcgen05.ld destinations above
+// the tcgen05.wait::ld that completes them.
+__device__ __forceinline__ void reg_fence(uint32_t (&w)[16]) {
+#pragma unroll
+  for (int i = 0; i < 16; ++i) asm volatile("" : "+r"(w[i]));
+}
+
 // Epilogue of one accumulator quarter: the warp's 32 output rows (columns
-// q*32.. of the sub-tile) x tokens [tok0, tok0 + ntok), in chunks of 32
+// q*32.. of the sub-tile) x tokens [tok0, tok0 + ntok), in pieces of 16
 // tokens; tokens >= lim belong to another CTA (or are past M) and are never
-// written.  Per chunk: tcgen05.ld, convert, then either stage [32 rows][32 tok]
-// in this warp's swizzled smem tile and issue one TMA 2-D store (16-bit
-// condensed output, whole chunk inside [tok0, lim), all 32 rows inside the
-// sub-tile), or 16-byte / scalar stores of each thread's row segment.
+// written.  The next piece's tcgen05.ld is issued as soon as the current one
+// is packed, so TMEM latency overlaps the stores.  16-bit condensed output
+// leaves through TMA 2-D stores of [32 rows][16 tokens] from two 1 KB staging
+// buffers used alternately (sbuf), so filling one overlaps the bulk read of
+// the other; otherwise 16-byte / scalar stores of each thread's row segment.
 __device__ __forceinline__ void epilogue_rows(const GemmArgs& args, const CUtensorMap* map_out,
-                                              uint8_t* stg, uint32_t t0, int lane, int orow,
-                                              bool row_live, bool warp_full, int row0_tma,
-                                              int tok0, int ntok, int lim) {
+                                              uint8_t* stg, int& sbuf, uint32_t t0, int lane,
+                                              int orow, bool row_live, bool warp_full,
+                                              int row0_tma, int tok0, int ntok, int lim) {
   const bool do_store = !(args.flags & kFlagSkipStore);
   const int esz = args.out_dtype == kF32 ? 4 : 2;
   uint8_t* row_base =
       static_cast<uint8_t*>(args.out) + static_cast<int64_t>(orow) * args.ld_out * esz;
+  uint32_t w[16];
+  if (ntok <= 0) return;
+  tmem_ld_32x32b_x16(t0, w);
 #pragma unroll 1
-  for (int c = 0; c < ntok; c += 32) {
-    uint32_t w[32];
-    tmem_ld_32x32b_x32(t0 + c, w);
+  for (int c = 0; c < ntok; c += 16) {
     tmem_ld_wait();
-    if (!do_store) continue;
+    reg_fence(w);
+    const bool more = c + 16 < ntok;
     const int tok = tok0 + c;
-    if (tok >= lim) continue;
-    const bool whole = tok + 32 <= lim;
-    if (esz == 2) {
-      // packed row segment: 16 words (element pairs); w[i] <- (w[2i], w[2i+1])
+    const bool live = do_store && tok < lim;
+    const bool whole = tok + 16 <= lim;
+    if (esz == 4) {
+      if (live && row_live) {
+        float* dst = reinterpret_cast<float*>(row_base) + tok;
+        if (args.vec_ok && whole) {
 #pragma unroll
-      for (int i = 0; i < 16; ++i)
-        w[i] = pack2(__uint_as_float(w[2 * i]), __uint_as_float(w[2 * i + 1]), args.out_dtype);
+          for (int i = 0; i < 16; i += 4)
+            *reinterpret_cast<uint4*>(dst + i) = make_uint4(w[i], w[i + 1], w[i + 2], w[i + 3]);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 16; ++i)
+            if (tok + i < lim) dst[i] = __uint_as_float(w[i]);
+        }
+      }
+      if (more) tmem_ld_32x32b_x16(t0 + c + 16, w);
+      continue;
     }
-    if (esz == 2 && args.use_tma_store && warp_full && whole) {
-      // the TMA store that last read this staging tile must be done with it
-      if (lane == 0) bulk_wait_read<0>();
-      __syncwarp();
-      // row `lane` of the tile; 16-byte chunk index XOR-swizzled to match the
-      // tensor map's SWIZZLE_64B
+    // packed row segment: 8 words (element pairs)
+    uint32_t pk[8];
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
-        *reinterpret_cast<uint4*>(stg + lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4)) =
-            make_uint4(w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
+    for (int i = 0; i < 8; ++i)
+      pk[i] = pack2(__uint_as_float(w[2 * i]), __uint_as_float(w[2 * i + 1]), args.out_dtype);
+    if (more) tmem_ld_32x32b_x16(t0 + c + 16, w);
+    if (!live) continue;
+    if (args.use_tma_store && warp_full && whole) {
+      // the store that last read this buffer (two stores ago) must be done
+      if (lane == 0) bulk_wait_read<1>();
+      __syncwarp();
+      uint8_t* buf = stg + sbuf * 1024;
+      // row `lane` = 32 bytes, 16-byte halves XOR-swizzled (SWIZZLE_32B)
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+        *reinterpret_cast<uint4*>(buf + lane * 32 + ((j ^ ((lane >> 2) & 1)) << 4)) =
+            make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) {
-        tma_store_2d(map_out, stg, tok, row0_tma);
+        tma_store_2d(map_out, buf, tok, row0_tma);
         bulk_commit();
       }
+      sbuf ^= 1;
       continue;
     }
     if (!row_live) continue;
-    const bool vec = args.vec_ok && whole;
-    if (esz == 4) {
-      float* dst = reinterpret_cast<float*>(row_base) + tok;
-      if (vec) {
+    uint16_t* dst = reinterpret_cast<uint16_t*>(row_base) + tok;
+    if (args.vec_ok && whole) {
 #pragma unroll
-        for (int i = 0; i < 32; i += 4)
-          *reinterpret_cast<uint4*>(dst + i) = make_uint4(w[i], w[i + 1], w[i + 2], w[i + 3]);
-      } else {
-#pragma unroll
-        for (int i = 0; i < 32; ++i)
-          if (tok + i < lim) dst[i] = __uint_as_float(w[i]);
-      }
+      for (int i = 0; i < 8; i += 4)
+        *reinterpret_cast<uint4*>(dst + 2 * i) = make_uint4(pk[i], pk[i + 1], pk[i + 2], pk[i + 3]);
     } else {
-      uint16_t* dst = reinterpret_cast<uint16_t*>(row_base) + tok;
-      if (vec) {
 #pragma unroll
-        for (int i = 0; i < 16; i += 4)
-          *reinterpret_cast<uint4*>(dst + 2 * i) = make_uint4(w[i], w[i + 1], w[i + 2], w[i + 3]);
-      } else {
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          if (tok + 2 * i < lim) dst[2 * i] = static_cast<uint16_t>(w[i] & 0xFFFFu);
-          if (tok + 2 * i + 1 < lim) dst[2 * i + 1] = static_cast<uint16_t>(w[i] >> 16);
-        }
+      for (int i = 0; i < 8; ++i) {
+        if (tok + 2 * i < lim) dst[2 * i] = static_cast<uint16_t>(pk[i] & 0xFFFFu);
+        if (tok + 2 * i + 1 < lim) dst[2 * i + 1] = static_cast<uint16_t>(pk[i] >> 16);
       }
     }
   }
@@ -247,7 +246,8 @@ __device__ __forceinline__ void epilogue_rows(const GemmArgs& args, const CUtens
 template <bool kRes>
 __global__ void __launch_bounds__(kThreads, 1)
     tw_gemm_kernel(const __grid_constant__ CUtensorMap map_pay,
-                   const __grid_constant__ CUtensorMap map_out, const GemmArgs args) {
+                   const __grid_constant__ CUtensorMap map_out, const __grid_constant__ GemmArgs args,
+                   const __grid_constant__ WorkTable work) {
   using C = Cfg<kRes>;
   constexpr int kStages = C::kStages;
   extern __shared__ uint8_t smem_raw[];
@@ -315,7 +315,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 
   Walker walk;
-  walk.init(args, tab);
+  walk.init(args, work, tab);
   Seg sg;
 
   if (warp == kPayloadWarp) {
@@ -353,8 +353,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     // kept-row indices of the next stage are prefetched in registers.  Copies
     // are zero-filled past M and for padding slots (index -1).  Each thread's
     // cp.async completion arrives on full[stage] asynchronously (noinc), so
-    // every stage can be in flight at once; the MMA thread fences the
-    // generic -> async proxy after its wait.
+    // every stage can be in flight at once without blocking the warp (a
+    // per-warp arrival after cp.async.wait_group measured 20% slower); the MMA
+    // thread fences the generic -> async proxy after its wait.
     const int gt = threadIdx.x - 32 * kGatherWarp0;
     const bool skip_a = flags & kFlagSkipA;
     const char* xa = static_cast<const char*>(args.x);
@@ -464,6 +465,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int h = (warp - kEpilogueWarp0) >> 2;
     const int c = q * 32 + lane;  // output column within the 128-wide sub-tile
     uint8_t* stg = sStg + (warp - kEpilogueWarp0) * kStgBytes;
+    int sbuf = 0;
     grid_dependency_wait();  // the previous kernel may still read our output buffer
     int j = 0;
     while (walk.next(args, sg)) {
@@ -480,7 +482,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int tok0 = sg.ub + h * 128;
       const int ntok = min(128, ((sg.ue - sg.ub + 15) & ~15) - h * 128);
       if (ntok > 0)
-        epilogue_rows(args, &map_out, stg, t0, lane, orow, row_live, warp_full,
+        epilogue_rows(args, &map_out, stg, sbuf, t0, lane, orow, row_live, warp_full,
                       sg.d.out_row + q * 32, tok0, ntok, sg.ue);
       tc_fence_before();
       __syncwarp();
@@ -515,9 +517,11 @@ cudaError_t configure_gemm_kernels() {
 }
 
 cudaError_t launch_tw_gemm(const CUtensorMap& map_pay, const CUtensorMap& map_out,
-                           const GemmArgs& args, bool resident, int grid, cudaStream_t stream) {
+                           const GemmArgs& args, const WorkTable& work, bool resident, int grid,
+                           cudaStream_t stream) {
   if (grid <= 0) return cudaSuccess;
   if (resident && !args.owner) return cudaErrorInvalidValue;
+  if (args.owner && grid > kMaxCtas) return cudaErrorInvalidValue;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kThreads);
@@ -528,8 +532,9 @@ cudaError_t launch_tw_gemm(const CUtensorMap& map_pay, const CUtensorMap& map_ou
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  if (resident) return cudaLaunchKernelEx(&cfg, tw_gemm_kernel<true>, map_pay, map_out, args);
-  return cudaLaunchKernelEx(&cfg, tw_gemm_kernel<false>, map_pay, map_out, args);
+  if (resident)
+    return cudaLaunchKernelEx(&cfg, tw_gemm_kernel<true>, map_pay, map_out, args, work);
+  return cudaLaunchKernelEx(&cfg, tw_gemm_kernel<false>, map_pay, map_out, args, work);
 }
 
 }  // namespace tw

@@ -31,9 +31,21 @@ struct SubTile {
 // i.e. K' <= 448) stays in shared memory for all of the CTA's tokens.
 constexpr int kResSteps = 7;
 
+// Owner mode: the whole assignment of every CTA (its sub-tile and token
+// range), computed on the host per call and passed as a kernel parameter so
+// a CTA starts its pipeline without dependent global loads.
+constexpr int kMaxCtas = 160;
+struct CtaWork {
+  int32_t kp_steps, idx_row, pay_row, width, out_row;  // the owned sub-tile
+  int32_t b, e;                                        // token range [b, e)
+  int32_t usz;                                         // tokens per unit (0 = idle CTA)
+};
+struct WorkTable {
+  CtaWork w[kMaxCtas];
+};
+
 struct GemmArgs {
   const SubTile* subtiles;  // [n_sub] in visiting order (LPT)
-  const int32_t* cta_first; // owner mode: [n_sub + 1] first CTA of every sub-tile
   const void* x;            // activations A^T [K][ld_x] (tokens contiguous), fp16/bf16
   int64_t ld_x;             // elements between A^T rows (multiple of 8)
   const int32_t* gidx;      // [n_tiles][kp] kept rows of every tile, -1 = zero padding
@@ -46,12 +58,10 @@ struct GemmArgs {
   int32_t M;
   int32_t n_sub;
   int32_t n_units;          // strided mode: n_sub * ceil(M / kTN)
-  int32_t owner;            // 1 = one sub-tile + token range per CTA, 0 = strided units
-  int32_t gran;             // owner mode: token-range granularity (16, 32 or 64)
-  int32_t split_single;     // owner mode: split a one-unit range into two units
+  int32_t owner;            // 1 = one sub-tile + token range per CTA (WorkTable), 0 = strided units
   int32_t flags;            // diagnostics (kFlag*); 0 in production
   int32_t vec_ok;           // output rows 16-byte aligned: vector stores allowed
-  int32_t use_tma_store;    // map_out valid (16-bit output): 32 x 32 blocks via TMA stores
+  int32_t use_tma_store;    // map_out valid (16-bit output): 32 x 16 blocks via TMA stores
   long long* trace;         // optional per-CTA clock64 trace (4096 entries per CTA)
 };
 
@@ -62,10 +72,11 @@ constexpr int32_t kFlagSkipMma = 4;     // do not issue tcgen05.mma
 
 // K1: persistent warp-specialised TW GEMM (tcgen05 + TMA + cp.async gather).
 //   map_pay : payload [n_sub * kBN][Kp], box {64 k, kBN rows}, 128-B swizzle
-//   map_out : C'^T (16-bit), box {32 tokens, 32 rows}, 64-B swizzle
+//   map_out : C'^T (16-bit), box {16 tokens, 32 rows}, 32-B swizzle
 //   resident: payload held in shared memory (owner mode, kp_steps <= kResSteps)
 cudaError_t launch_tw_gemm(const CUtensorMap& map_pay, const CUtensorMap& map_out,
-                           const GemmArgs& args, bool resident, int grid, cudaStream_t stream);
+                           const GemmArgs& args, const WorkTable& work, bool resident, int grid,
+                           cudaStream_t stream);
 
 // Raise the dynamic shared-memory limit of every K1 instance (call once per
 // device before launching or capturing).
