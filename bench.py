@@ -64,6 +64,9 @@ CONFIGS = {
                              "M=8192 (configs[2])"},
     "cfg1": {"layers": [(1024, 1024)], "m": 128, "s": 0.75, "g": 128, "delta": 0.0,
              "workload": "single 1024x1024 weight, TW 75% G=128, M=128 (configs[0])"},
+    "big": {"layers": [(16384, 16384)], "m": 8192, "s": 0.75, "g": 128, "delta": 0.0,
+            "workload": "16384x16384 TW 75% G=128, M=8192; column tiles sharded over the "
+                        "ranks + NCCL all-gather of C'^T (configs[4])"},
 }
 N_ROTATE = 4
 
@@ -497,6 +500,148 @@ def run_ours(args, cfg, rank: int, world: int) -> None:
     print(json.dumps(line))
 
 
+# ----------------------------------------------------------------------------
+# configs[4]: one large layer, column tiles sharded across ranks (strong scaling)
+# ----------------------------------------------------------------------------
+
+def run_big(args, cfg, rank: int, world: int) -> None:
+    """16384^2 TW layer, M=8192.  Rank r owns a contiguous, MAC-balanced group
+    of column tiles (distributed.column_shards), runs K1 on it and one
+    all_gather_into_tensor assembles the full C'^T (N' x M).  A step = K1 on
+    the shard + the all-gather; value = the WHOLE layer's surviving FLOPs /
+    max-over-ranks step time (strong scaling).  Inputs (268 MB A^T, 134 MB
+    payload, 134 MB output per rank) exceed L2, so there is no rotation."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2402_10876_b200 as tw
+    from paper_2402_10876_b200 import distributed as D
+
+    dev = torch.device("cuda", torch.cuda.current_device())
+    (k, n), m = cfg["layers"][0], cfg["m"]
+    w = tw.round_to(tw.synthetic_matrix(0, k, n, tw.STREAM_WEIGHTS), "fp16")
+    _, tsm = tw.prune_tw(w, cfg["s"], cfg["g"])
+    enc = tw.encode_cto(tsm)
+    shards = D.column_shards(enc, world)
+    rows = D.shard_rows(enc, shards)
+    lo, hi = shards[rank]
+    plan = tw.TwPlan(D.shard_encoding(enc, lo, hi), compute_dtype="fp16")
+    flops_total = tw.sparse_flops(tsm, m)
+    flops_local = plan.flops(m)
+    a_host = tw.round_to(tw.synthetic_matrix(0, m, k, tw.STREAM_INPUT), "fp16")
+    a_dev = torch.from_numpy(a_host).to(dev, torch.float16)
+    at = plan.prepare(a_dev)
+    r0, r1 = rows[rank]
+    tallest = max(b - a for a, b in rows)
+    local = torch.empty((tallest, m), dtype=torch.float16, device=dev)
+    full = torch.empty((tallest * world, m), dtype=torch.float16, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def step(i: int = 0):
+        plan.run(at, out=local[: r1 - r0])
+        if world > 1:
+            dist.all_gather_into_tensor(full, local)
+
+    def timed(fn, steps):
+        for i in range(args.warmup):
+            fn(i)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for i in range(steps):
+            fn(i)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t = torch.tensor([e0.elapsed_time(e1) / steps], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        t_soak = time.time()
+        while time.time() - t_soak < 1.0:
+            step()
+            torch.cuda.synchronize()
+        ms_step = timed(step, args.steps)
+    value = flops_total / (ms_step * 1e-3) / 1e12
+
+    # K1 alone on this rank's shard (roofline) and the all-gather alone
+    ms_k1 = timed(lambda i: plan.run(at, out=local[: r1 - r0]), args.steps)
+    ms_ag = timed(lambda i: dist.all_gather_into_tensor(full, local), args.steps) if world > 1 else 0.0
+
+    # dense cuBLAS on the same column share (N/world columns of W, same A^T)
+    c0 = n * rank // world
+    c1 = n * (rank + 1) // world
+    wt = torch.from_numpy(np.ascontiguousarray(w[:, c0:c1].T)).to(dev, torch.float16)
+    at_plain = tw.prepare_activations(a_dev)
+    dense_out = torch.empty((c1 - c0, m), dtype=torch.float16, device=dev)
+    ms_dense = timed(lambda i: torch.matmul(wt, at_plain, out=dense_out), args.steps)
+    del wt, dense_out
+
+    # e2e through the public API: pinned host A (M x K) -> H2D -> K4 -> K1 ->
+    # all-gather -> D2H of the full fp16 C'^T
+    a_pin = torch.from_numpy(a_host).to(torch.float16).pin_memory()
+    c_pin = torch.empty((tallest * world if world > 1 else r1 - r0, m),
+                        dtype=torch.float16).pin_memory()
+
+    def e2e(i: int = 0):
+        a_dev.copy_(a_pin, non_blocking=True)
+        x = plan.prepare(a_dev)
+        plan.run(x, out=local[: r1 - r0])
+        if world > 1:
+            dist.all_gather_into_tensor(full, local)
+            c_pin.copy_(full, non_blocking=True)
+        else:
+            c_pin.copy_(local[: r1 - r0], non_blocking=True)
+
+    ms_e2e = timed(e2e, max(2, args.steps // 4))
+    if rank != 0:
+        return
+    pk = peaks()
+    tf_k1 = flops_local / (ms_k1 * 1e-3) / 1e12
+    roofline = {"bound": "tensor", "achieved": tf_k1, "peak": pk["tc"], "unit": "TFLOP/s",
+                "frac": tf_k1 / pk["tc"], "traffic": None, "kernel": "tw_gemm_kernel",
+                "peak_source": pk["source"],
+                "arithmetic_intensity": flops_total / tw.algorithmic_bytes(tsm, m),
+                "k1_ms": ms_k1, "allgather_ms": ms_ag}
+    # CPU baseline: the reference algorithm on one tile over 64 tokens, scaled
+    from oracle import tilesparse_oracle as orc
+    t = tsm.tiles[0]
+    a_s = a_host[:64]
+    t0 = time.perf_counter()
+    orc.execute_batched(a_s, [(t.kept_rows.kept, t.payload)], os.cpu_count() or 1, "lpt")
+    cpu_s = time.perf_counter() - t0
+    cpu_rate = 2 * 64 * t.width * t.kept_rows.n_kept / cpu_s / 1e12
+    line = {
+        "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "fp16",
+        "data": "synthetic (Philox seed 0, fp16-rounded)",
+        "config": {"workload": cfg["workload"], "m_tokens": m, "sparsity": cfg["s"],
+                   "g": cfg["g"], "parallelism": f"column tiles / {world} ranks + all-gather",
+                   "l2": "inputs > L2 (268 MB A^T, 134 MB payload, 134 MB C'^T)"},
+        "speedup_vs_cublas": ms_dense / ms_k1,
+        "cublas": {"ms_per_step": ms_dense, "columns_per_rank": c1 - c0,
+                   "tflops_dense": 2 * m * k * (c1 - c0) / (ms_dense * 1e-3) / 1e12},
+        "frac_of_dense_peak": tf_k1 / pk["tc"],
+        "e2e": {"value": flops_total / (ms_e2e * 1e-3) / 1e12, "unit": "TFLOP/s",
+                "ms_per_step": ms_e2e, "h2d_bytes_per_step": a_pin.numel() * 2,
+                "d2h_bytes_per_step": c_pin.numel() * 2,
+                "path": "pinned host fp16 A -> H2D -> K4 -> K1 -> all-gather -> D2H"},
+        "roofline": roofline,
+        "cpu_baseline": {"value": cpu_rate, "unit": "TFLOP/s", "cores": os.cpu_count() or 1,
+                         "kind": "port", "sample": f"tile 0 (K'={t.kept_rows.n_kept}) x 64 tokens "
+                                                   f"({cpu_s:.1f} s, one lane: one tile)"},
+        "gpu_launches": args.steps,
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line))
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -524,7 +669,10 @@ def main() -> None:
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     try:
-        run_ours(args, cfg, rank, world)
+        if args.config == "big":
+            run_big(args, cfg, rank, world)
+        else:
+            run_ours(args, cfg, rank, world)
     finally:
         if world > 1:
             dist.destroy_process_group()

@@ -559,7 +559,22 @@ static int run_tw(const tw_plan* p, const void* x, int64_t m, int64_t ld_x, void
   // on the SMs; otherwise 256-token units strided over the CTAs.
   int grid;
   WorkTable work;
-  if (p->owner && !env_int("TW_STRIDED", 0)) {
+  bool owner = p->owner && !env_int("TW_STRIDED", 0);
+  if (owner && !p->resident && !env_int("TW_OWNER", 0)) {
+    // Streamed payload: both modes re-stream a sub-tile's payload per unit,
+    // so pick the one whose busiest CTA does less (k-steps x tokens).
+    int64_t own = 0, max_steps = 0;
+    for (int sidx = 0; sidx < p->n_sub; ++sidx) {
+      const int c = p->cta_first[sidx + 1] - p->cta_first[sidx];
+      const int64_t toks = ((m + c - 1) / c + 63) / 64 * 64;
+      own = std::max<int64_t>(own, (int64_t)p->subtiles[sidx].kp_steps * toks);
+      max_steps = std::max<int64_t>(max_steps, p->subtiles[sidx].kp_steps);
+    }
+    const int64_t units = (int64_t)p->n_sub * ((m + kTN - 1) / kTN);
+    const int64_t strided = (units + p->sm_count - 1) / p->sm_count * kTN * max_steps;
+    if (strided < own) owner = false;
+  }
+  if (owner) {
     a.owner = 1;
     int gran = env_int("TW_GRAN", 64);
     if (gran != 16 && gran != 32 && gran != 64) gran = 64;

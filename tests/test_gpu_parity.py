@@ -50,6 +50,11 @@ def _oracle_tw(a, tsm):
     (300, 700, 130, 0.5, 300),    # g > 256: tiles split into UMMA-N slices
     (50, 64, 64, 0.0, 8),         # nothing pruned
     (40, 400, 64, 0.9, 1),        # g = 1: 40 width-1 tiles
+    # VGG-16 im2col shapes (configs[3]) at reduced M: K = 9 * C_in
+    (27, 64, 4096, 0.5, 64),      # conv1_1: K = 27, one 64-wide tile
+    (576, 128, 4096, 0.9, 256),   # conv2_1 at 90%: K' down to a few rows
+    (2304, 512, 2048, 0.75, 128), # conv4_1
+    (4608, 512, 1536, 0.9, 64),   # conv4_2 at 90%, G = 64
 ])
 def test_tw_matches_oracle(k, n, m, s, g):
     w, a, plan, tsm = _problem(k, n, m, s, g, seed=k * 31 + n)
@@ -201,3 +206,36 @@ def test_stream_k_matches_oracle_and_is_deterministic(k, n, m, g, s):
     o2 = tw.gemm_tile_sparse(a, tsm).condensed.cpu().numpy()
     assert o1.tobytes() == o2.tobytes()
     assert tw.relative_error(o1, _oracle_tw(a, tsm)) <= TOL["fp32"]
+
+
+@pytest.mark.parametrize("mode", ["owner", "strided"])
+def test_streamed_modes_match_oracle(mode, monkeypatch):
+    """K' > 448 (streamed payload) through both work decompositions."""
+    monkeypatch.setenv("TW_OWNER" if mode == "owner" else "TW_STRIDED", "1")
+    w, a, plan, tsm = _problem(2048, 1024, 1536, 0.75, 128, seed=7)
+    out = tw.TwPlan(tw.encode_cto(tsm)).run(tw.prepare_activations(a)).t()
+    assert tw.relative_error(out, _oracle_tw(a, tsm)) <= TOL["fp32"]
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_column_shards_concatenate_bit_identical(world):
+    """configs[4] partition on one GPU: every rank's shard plan writes its
+    contiguous rows of C'^T; stacked in rank order they equal the unsharded
+    product bit for bit (what the NCCL all-gather assembles)."""
+    import torch
+
+    from paper_2402_10876_b200 import distributed as D
+
+    w, a, plan, tsm = _problem(1024, 2048, 1024, 0.75, 128, seed=world)
+    enc = tw.encode_cto(tsm)
+    full = tw.TwPlan(enc).run(tw.prepare_activations(a))
+    shards = D.column_shards(enc, world)
+    rows = D.shard_rows(enc, shards)
+    parts = []
+    for (lo, hi), (r0, r1) in zip(shards, rows):
+        p = tw.TwPlan(D.shard_encoding(enc, lo, hi))
+        part = p.run(p.prepare(a))
+        assert part.shape[0] == r1 - r0
+        parts.append(part)
+    stacked = torch.cat(parts, dim=0)
+    assert torch.equal(stacked, full)
