@@ -34,136 +34,204 @@ __device__ __forceinline__ void store_from_float(void* p, int32_t dtype, int64_t
 
 // K2 -- TEW overlay SpMM, C'^T[urow(c)] (+)= sum_{(r, v) in column c} v * A^T[r].
 //
-// Every overlay row r of A^T is shared by many overlay columns (nnz/col is
-// 11-46 at the BERT shapes while K is 768-3072), so reading A^T rows per nnz
-// from L2 would move nnz * M * 2 bytes (580 MB for BERT 768x3072) through the
-// SMs.  Instead a CTA stages the A^T block of its T tokens for ALL K rows in
-// shared memory (16-bit, K * T * 2 bytes) together with the packed
-// (row, value) list of its column group (4 bytes per nnz: row << 16 | 16-bit
-// value in the compute dtype, the same rounding the TW payload gets), and
-// walks the columns from there: a group of T/4 lanes per column, 4 tokens per
-// lane, per nnz one broadcast 4-byte list load, one 8-byte A^T load, two
-// conversions and two packed fma.rn.f32x2.  Columns are visited in
-// descending-nnz order (host-sorted) so the lane groups of a warp finish
-// together.  Each column's list is in ascending row order (CSC order of
-// patterns.py:145-214); fp32 accumulation, then one coalesced
-// read-modify-write of the TW result (accumulate = 1) or a plain store
-// (residual-only column).  Geometry (T, column groups) comes from
-// residual_geometry(); shapes that do not fit fall back to the direct kernel.
-constexpr int kResThreads = 512;
+// Replaces the per-column overlay loop of gemm_tew (executor.py:196-203).
+// Every overlay row of A^T is shared by many overlay columns (nnz/col is
+// 11-46 at the BERT shapes while K is 768-3072, and the overlay covers every
+// row), so a CTA stages the A^T block of T tokens for ALL K rows in shared
+// memory (16-bit, K * T * 2 bytes) and serves every overlay column of its
+// column range from there: 2 bytes of shared-memory traffic per FMA and ~1x
+// A^T of L2 reads for the staging.
+//
+// Grid = (token blocks, column splits); several small CTAs per SM give the
+// occupancy that hides the list loads.  After one barrier the warps walk
+// their columns independently: a lane group of L = T / 8 lanes per column
+// (8 tokens per lane, one 16-byte shared load per entry), 32 / L columns per
+// warp step, columns in descending-nnz order (host) so the groups of a warp
+// finish together.  Each lane group fetches L packed entries (row << 16 |
+// 16-bit value, rounded like the TW payload) per global load, one chunk
+// ahead, and broadcasts them with shuffles; one fma.rn.f32.f16 (FHFMA: 16-bit
+// operands, fp32 accumulator, no conversions) per token, fp32 accumulation in ascending row order (CSC order of
+// patterns.py:145-214), then one read-modify-write of the TW result
+// (accumulate = 1) or a plain store (residual-only column).
+constexpr int kResThreads = 256;
 constexpr int kResWarps = kResThreads / 32;
-constexpr int kResSmem = 200 * 1024;
-
-__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
-  float2 d;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;"
-      : "=l"(reinterpret_cast<uint64_t&>(d))
-      : "l"(reinterpret_cast<const uint64_t&>(a)), "l"(reinterpret_cast<const uint64_t&>(b)),
-        "l"(reinterpret_cast<const uint64_t&>(c)));
-  return d;
-}
+constexpr int kResCtasPerSm = 4;  // register budget: 64 per thread
 
 __device__ __forceinline__ float2 h2_to_f2(uint32_t u, bool bf) {
   if (bf) return make_float2(__uint_as_float(u << 16), __uint_as_float(u & 0xFFFF0000u));
   return __half22float2(*reinterpret_cast<const __half2*>(&u));
 }
 
-__device__ __forceinline__ float h_to_f(uint32_t h16, bool bf) {
-  return bf ? __uint_as_float(h16 << 16) : __half2float(__ushort_as_half(static_cast<uint16_t>(h16)));
+// acc + a * v with 16-bit a, v and fp32 accumulation (FHFMA: the product is
+// exact in fp32, one rounding -- identical to widening first).
+template <bool kBf>
+__device__ __forceinline__ float fma_h(uint16_t a, uint16_t v, float acc) {
+  float d;
+  if (kBf)
+    asm("fma.rn.f32.bf16 %0, %1, %2, %3;" : "=f"(d) : "h"(a), "h"(v), "f"(acc));
+  else
+    asm("fma.rn.f32.f16 %0, %1, %2, %3;" : "=f"(d) : "h"(a), "h"(v), "f"(acc));
+  return d;
 }
 
-template <int T>
-__global__ void __launch_bounds__(kResThreads)
-    tw_residual_kernel(const ResidualArgs args, int col_groups) {
+// acc[0..7] += 8 packed 16-bit a (uint4) * v
+template <bool kBf>
+__device__ __forceinline__ void fma8(float (&acc)[8], const uint4& a, uint16_t v) {
+  const uint32_t w[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    uint16_t lo, hi;
+    asm("mov.b32 {%0, %1}, %2;" : "=h"(lo), "=h"(hi) : "r"(w[i]));
+    acc[2 * i] = fma_h<kBf>(lo, v, acc[2 * i]);
+    acc[2 * i + 1] = fma_h<kBf>(hi, v, acc[2 * i + 1]);
+  }
+}
+
+
+// 4 outputs at out[bs..bs+3] (+)= o, 16-bit or fp32, tail-masked by n.
+__device__ __forceinline__ void residual_store4(const ResidualArgs& args, int64_t bs, int n,
+                                                bool accum, float o0, float o1, float o2,
+                                                float o3) {
+  const bool obf = args.out_dtype == kBF16;
+  if (n >= 4 && bs % 4 == 0) {
+    if (args.out_dtype != kF32) {
+      uint2* p = reinterpret_cast<uint2*>(static_cast<uint16_t*>(args.out) + bs);
+      const uint2 prev = accum ? *p : make_uint2(0u, 0u);
+      const float2 lo2 = h2_to_f2(prev.x, obf), hi2 = h2_to_f2(prev.y, obf);
+      const float f0 = lo2.x + o0, f1 = lo2.y + o1, f2 = hi2.x + o2, f3 = hi2.y + o3;
+      uint2 w;
+      if (!obf) {
+        const __half2 x = __floats2half2_rn(f0, f1), y = __floats2half2_rn(f2, f3);
+        w = make_uint2(*reinterpret_cast<const uint32_t*>(&x), *reinterpret_cast<const uint32_t*>(&y));
+      } else {
+        const __nv_bfloat162 x = __floats2bfloat162_rn(f0, f1);
+        const __nv_bfloat162 y = __floats2bfloat162_rn(f2, f3);
+        w = make_uint2(*reinterpret_cast<const uint32_t*>(&x), *reinterpret_cast<const uint32_t*>(&y));
+      }
+      *p = w;
+    } else {
+      float4* p = reinterpret_cast<float4*>(static_cast<float*>(args.out) + bs);
+      const float4 prev = accum ? *p : make_float4(0.f, 0.f, 0.f, 0.f);
+      *p = make_float4(prev.x + o0, prev.y + o1, prev.z + o2, prev.w + o3);
+    }
+    return;
+  }
+  const float o[4] = {o0, o1, o2, o3};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    if (i < n) {
+      float w = o[i];
+      if (accum) w += load_as_float(args.out, args.out_dtype, bs + i);
+      store_from_float(args.out, args.out_dtype, bs + i, w);
+    }
+  }
+}
+
+template <int T, bool kBf>
+__global__ void __launch_bounds__(kResThreads, kResCtasPerSm)
+    tw_residual_kernel(const __grid_constant__ ResidualArgs args) {
   extern __shared__ __align__(16) uint8_t res_smem[];
-  uint16_t* sA = reinterpret_cast<uint16_t*>(res_smem);                  // [K][T]
-  uint32_t* sRV = reinterpret_cast<uint32_t*>(res_smem + args.K * T * 2);  // group's list
-  constexpr int kLanesPerCol = T / 4;
-  constexpr int kColsPerWarp = 32 / kLanesPerCol;
-  const int64_t t0 = static_cast<int64_t>(blockIdx.x) * T;
+  uint16_t* sA = reinterpret_cast<uint16_t*>(res_smem);  // [K][T]
+  constexpr int L = T / 8;        // lanes per column (8 tokens each)
+  constexpr int kCols = 32 / L;   // columns per warp step
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint16_t* at = static_cast<const uint16_t*>(args.at);
   const int K = args.K;
-  const bool bf = args.in_dtype == kBF16;
+  const int sub = lane / L;
+  const int tl = lane - sub * L;
+  const int tok = tl * 8;
+  const int gbase = sub * L;
+  const int64_t t0 = static_cast<int64_t>(blockIdx.x) * T;
   const int64_t rem = args.M - t0;
   const int ntok = rem < T ? static_cast<int>(rem) : T;
-  // column group g: processed columns [c0, c1), nnz [e0, e1)
-  const int g = blockIdx.y;
-  const int c0 = static_cast<int>(static_cast<int64_t>(g) * args.n_cols / col_groups);
-  const int c1 = static_cast<int>(static_cast<int64_t>(g + 1) * args.n_cols / col_groups);
-  const int e0 = __ldg(args.col_start + c0), e1 = __ldg(args.col_start + c1);
-  // stage the (row, value) list and A^T[:, t0:t0+T] (zero past M) with
-  // cp.async so every load of the CTA is in flight at once
+  // this CTA's columns: split y of the descending-nnz order (by nnz)
+  const int c0 = args.group_first[blockIdx.y], c1 = args.group_first[blockIdx.y + 1];
   {
-    const int n4 = (e1 - e0);
-    const bool al = ((e0 & 3) == 0);
-    const int nvec = al ? n4 / 4 : 0;
-    for (int i = threadIdx.x; i < nvec; i += kResThreads)
-      cp_async_16(smem_u32(sRV + 4 * i), args.rv + e0 + 4 * i, 16);
-    for (int i = 4 * nvec + threadIdx.x; i < n4; i += kResThreads) sRV[i] = __ldg(args.rv + e0 + i);
-  }
-  if (T % 8 == 0 && args.ld_at % 8 == 0) {
     constexpr int per_row = T / 8;
-    for (int i = threadIdx.x; i < K * per_row; i += kResThreads) {
+    // row K stays zero: padding entries (row K, value 0) add exactly 0
+    for (int i = threadIdx.x; i < (K + 1) * per_row; i += kResThreads) {
       const int r = i / per_row, j = (i - r * per_row) * 8;
-      const int valid = ntok - j;
+      const int valid = r < K ? ntok - j : 0;
       const uint32_t bytes = valid >= 8 ? 16u : (valid > 0 ? static_cast<uint32_t>(valid) * 2 : 0u);
       cp_async_16(smem_u32(sA + r * T + j), bytes ? at + r * args.ld_at + t0 + j : at, bytes);
     }
-  } else {
-    for (int i = threadIdx.x; i < K * T; i += kResThreads) {
-      const int r = i / T, j = i - r * T;
-      sA[i] = j < ntok ? at[r * args.ld_at + t0 + j] : static_cast<uint16_t>(0);
-    }
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncthreads();
   }
-  cp_async_commit();
-  cp_async_wait<0>();
-  __syncthreads();
-  const int sub = lane / kLanesPerCol;
-  const int tok = (lane - sub * kLanesPerCol) * 4;
   const uint16_t* sAt = sA + tok;
-  for (int col = c0 + warp * kColsPerWarp + sub; col < c1; col += kResWarps * kColsPerWarp) {
-    const int lo = __ldg(args.col_start + col) - e0, hi = __ldg(args.col_start + col + 1) - e0;
-    float2 acc0 = make_float2(0.f, 0.f), acc1 = make_float2(0.f, 0.f);
-#pragma unroll 4
-    for (int e = lo; e < hi; ++e) {
-      const uint32_t q = sRV[e];
-      const uint2 a = *reinterpret_cast<const uint2*>(sAt + (q >> 16) * T);
-      const float v = h_to_f(q & 0xFFFFu, bf);
-      const float2 vv = make_float2(v, v);
-      acc0 = fma2(h2_to_f2(a.x, bf), vv, acc0);
-      acc1 = fma2(h2_to_f2(a.y, bf), vv, acc1);
-    }
-    if (tok >= ntok) continue;
-    const int64_t base = static_cast<int64_t>(__ldg(args.out_rows + col)) * args.ld_out + t0 + tok;
-    const bool accum = __ldg(args.accumulate + col) != 0;
-    const float o[4] = {acc0.x, acc0.y, acc1.x, acc1.y};
-    if (args.out_dtype != kF32 && tok + 4 <= ntok && base % 4 == 0) {
-      // 8-byte read-modify-write of 4 16-bit outputs
-      uint2* p = reinterpret_cast<uint2*>(static_cast<uint16_t*>(args.out) + base);
-      uint2 cur = accum ? *p : make_uint2(0u, 0u);
-      float f[4];
-      const float2 lo2 = h2_to_f2(cur.x, args.out_dtype == kBF16);
-      const float2 hi2 = h2_to_f2(cur.y, args.out_dtype == kBF16);
-      f[0] = lo2.x + o[0]; f[1] = lo2.y + o[1]; f[2] = hi2.x + o[2]; f[3] = hi2.y + o[3];
-      if (args.out_dtype == kF16) {
-        const __half2 x = __floats2half2_rn(f[0], f[1]), y = __floats2half2_rn(f[2], f[3]);
-        cur = make_uint2(*reinterpret_cast<const uint32_t*>(&x), *reinterpret_cast<const uint32_t*>(&y));
-      } else {
-        const __nv_bfloat162 x = __floats2bfloat162_rn(f[0], f[1]);
-        const __nv_bfloat162 y = __floats2bfloat162_rn(f[2], f[3]);
-        cur = make_uint2(*reinterpret_cast<const uint32_t*>(&x), *reinterpret_cast<const uint32_t*>(&y));
-      }
-      *p = cur;
-      continue;
-    }
+  // One column per lane group per step; the next step's metadata is
+  // prefetched one step ahead.
+  constexpr int kStep = kCols * kResWarps;
+  constexpr int G = 4 * L;  // entries per group (4 per lane, one 16-byte load)
+  const uint32_t zrow = static_cast<uint32_t>(K) << 16;
+  const uint4 zero4 = make_uint4(zrow, zrow, zrow, zrow);
+  const uint8_t* sAb = reinterpret_cast<const uint8_t*>(sAt);
+  const bool fast = args.out_dtype != kF32 && args.ld_out % 8 == 0;
+  int cs = c0 + warp * kCols;
+  // columns past c1 read the (zero-row) padding at the start of the lists
+  int4 m = cs + sub < c1 ? __ldg(args.meta + cs + sub) : make_int4(0, 0, 0, 0);
+  for (; cs < c1; cs += kStep) {
+    const int col = cs + sub;
+    const int4 mn = col + kStep < c1 ? __ldg(args.meta + col + kStep) : make_int4(0, 0, 0, 0);
+    const bool live = col < c1 && tok < ntok;
+    const int64_t bs = static_cast<int64_t>(m.z) * args.ld_out + t0 + tok;
+    // current output of a TW-kept column, consumed after the sum
+    uint4 prev = make_uint4(0u, 0u, 0u, 0u);
+    const bool vec = fast && ntok - tok >= 8;
+    if (live && vec && m.w)
+      prev = *reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(args.out) + bs);
+    const int maxlen = __reduce_max_sync(0xffffffffu, m.y);
+    float ac[8];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      if (tok + i >= ntok) break;
-      float w = o[i];
-      if (accum) w += load_as_float(args.out, args.out_dtype, base + i);
-      store_from_float(args.out, args.out_dtype, base + i, w);
+    for (int i = 0; i < 8; ++i) ac[i] = 0.f;
+    // entry groups: lane tl holds entries 4 tl .. 4 tl + 3 of a group;
+    // groups gi + 1, gi + 2 are in flight while gi is consumed.  Lists are
+    // padded to whole groups with zero-row entries (row K of the block is
+    // zero) and a lane group past its list substitutes them, so the entry
+    // loop has no branches.
+    const uint4* lp = reinterpret_cast<const uint4*>(args.rv + m.x) + tl;
+    uint4 c = __ldg(lp), n1 = __ldg(lp + L);
+    for (int eo = 0; eo < maxlen; eo += G) {
+      const uint4 f = __ldg(lp + 2 * L);
+      lp += L;
+      if (eo >= m.y) c = zero4;
+      const uint32_t w[4] = {c.x, c.y, c.z, c.w};
+#pragma unroll
+      for (int j = 0; j < G; ++j) {
+        const uint32_t q = L == 1 ? w[j & 3] : __shfl_sync(0xffffffffu, w[j & 3], gbase + (j >> 2));
+        fma8<kBf>(ac, *reinterpret_cast<const uint4*>(sAb + (q >> 16) * (T * 2)),
+                  static_cast<uint16_t>(q & 0xFFFFu));
+      }
+      c = n1;
+      n1 = f;
     }
+    if (live) {
+      if (vec) {
+        // 16-byte read-modify-write of 8 16-bit outputs
+        const bool obf = args.out_dtype == kBF16;
+        const uint32_t pw[4] = {prev.x, prev.y, prev.z, prev.w};
+        uint32_t o[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float2 fp = h2_to_f2(pw[i], obf);
+          const float f0 = fp.x + ac[2 * i], f1 = fp.y + ac[2 * i + 1];
+          if (!obf) {
+            const __half2 h = __floats2half2_rn(f0, f1);
+            o[i] = *reinterpret_cast<const uint32_t*>(&h);
+          } else {
+            const __nv_bfloat162 h = __floats2bfloat162_rn(f0, f1);
+            o[i] = *reinterpret_cast<const uint32_t*>(&h);
+          }
+        }
+        *reinterpret_cast<uint4*>(static_cast<uint16_t*>(args.out) + bs) = make_uint4(o[0], o[1], o[2], o[3]);
+      } else {
+        residual_store4(args, bs, ntok - tok, m.w != 0, ac[0], ac[1], ac[2], ac[3]);
+        if (tok + 4 < ntok)
+          residual_store4(args, bs + 4, ntok - tok - 4, m.w != 0, ac[4], ac[5], ac[6], ac[7]);
+      }
+    }
+    m = mn;
   }
 }
 
@@ -221,41 +289,43 @@ __global__ void build_payload_kernel(const PayloadArgs args) {
 
 }  // namespace
 
-bool residual_geometry(int32_t K, int64_t max_group_nnz_bytes_per_group1, int* T_out,
-                       int* groups_out) {
-  // largest T whose A^T block leaves room for the (row, value) list split into
-  // as few column groups as possible (list bytes = 4 * nnz)
-  for (int T : {64, 32, 16, 8}) {
-    const int64_t a_bytes = static_cast<int64_t>(K) * T * 2;
-    if (a_bytes > kResSmem / 2) continue;
-    const int64_t budget = kResSmem - a_bytes;
-    const int64_t groups = (max_group_nnz_bytes_per_group1 + budget - 1) / budget;
-    *T_out = T;
-    *groups_out = static_cast<int>(std::max<int64_t>(1, groups));
-    return true;
+int residual_block_tokens(int32_t K, int* ctas_per_sm) {
+  // T tokens per CTA (8 per lane): the A^T block (K + 1) * T * 2 bytes
+  // stays <= 56 KB so four 256-thread CTAs share an SM; T = 16 before 32
+  // keeps >= 3 CTAs per SM in flight at M = 8192
+  constexpr int64_t kMaxBlock = 56 * 1024;
+  for (int T : {16, 8}) {
+    const int64_t bytes = static_cast<int64_t>(K + 1) * T * 2;
+    if (bytes <= kMaxBlock) {
+      *ctas_per_sm = static_cast<int>(std::min<int64_t>(kResCtasPerSm, (220 * 1024) / (bytes + 1024)));
+      return T;
+    }
   }
-  return false;
+  *ctas_per_sm = 0;
+  return 0;
+}
+
+template <int T, bool kBf>
+static cudaError_t launch_res_t(const ResidualArgs& args, cudaStream_t stream) {
+  const size_t smem = static_cast<size_t>(args.K + 1) * T * 2;
+  cudaError_t e = cudaFuncSetAttribute(tw_residual_kernel<T, kBf>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  dim3 grid(static_cast<unsigned>(args.n_blocks), static_cast<unsigned>(args.n_groups));
+  tw_residual_kernel<T, kBf><<<grid, kResThreads, smem, stream>>>(args);
+  return cudaGetLastError();
 }
 
 template <int T>
 static cudaError_t launch_res(const ResidualArgs& args, cudaStream_t stream) {
-  const int blocks = static_cast<int>((args.M + T - 1) / T);
-  // smem: A^T block + the largest column group's list (host-checked bound)
-  const size_t smem = static_cast<size_t>(args.K) * T * 2 + static_cast<size_t>(args.max_group_nnz) * 4;
-  cudaError_t e = cudaFuncSetAttribute(tw_residual_kernel<T>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem));
-  if (e != cudaSuccess) return e;
-  dim3 grid(static_cast<unsigned>(blocks), static_cast<unsigned>(args.col_groups));
-  tw_residual_kernel<T><<<grid, kResThreads, smem, stream>>>(args, args.col_groups);
-  return cudaGetLastError();
+  return args.in_dtype == kBF16 ? launch_res_t<T, true>(args, stream)
+                                : launch_res_t<T, false>(args, stream);
 }
 
 cudaError_t launch_tw_residual(const ResidualArgs& args, cudaStream_t stream) {
   if (args.n_cols <= 0 || args.M <= 0) return cudaSuccess;
   switch (args.rv ? args.block_tokens : 0) {
-    case 64: return launch_res<64>(args, stream);
-    case 32: return launch_res<32>(args, stream);
     case 16: return launch_res<16>(args, stream);
     case 8: return launch_res<8>(args, stream);
     default: break;

@@ -158,13 +158,15 @@ struct tw_plan {
   float* d_ov_vals = nullptr;
   int32_t* d_ov_out = nullptr;
   int32_t* d_ov_acc = nullptr;
+  int4* d_ov_meta = nullptr;          // K2 per column: {first entry, entries, out row, accumulate}
   uint32_t* d_ov_rv = nullptr;         // K2 lists: row << 16 | 16-bit value
-  int32_t ov_block_tokens = 0, ov_col_groups = 1, ov_max_group_nnz = 0;
+  int32_t ov_block_tokens = 0, ov_ctas_per_sm = 0;
+  std::vector<int32_t> ov_start;       // host copy of the K2 column pointers
 
   ~tw_plan() {
     for (void* p : {(void*)d_subtiles, (void*)d_gidx, d_payload,
                     (void*)d_union_rowmap, (void*)d_ov_start, (void*)d_ov_rows, (void*)d_ov_vals,
-                    (void*)d_ov_out, (void*)d_ov_acc, (void*)d_ov_rv})
+                    (void*)d_ov_out, (void*)d_ov_acc, (void*)d_ov_rv, (void*)d_ov_meta})
       if (p) cudaFree(p);
   }
 };
@@ -426,45 +428,48 @@ int tw_plan_attach_overlay(tw_plan* p, int32_t k, int32_t n, int64_t nnz, const 
   }
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   for (void* q : {(void*)p->d_union_rowmap, (void*)p->d_ov_start, (void*)p->d_ov_rows,
-                  (void*)p->d_ov_vals, (void*)p->d_ov_out, (void*)p->d_ov_acc, (void*)p->d_ov_rv})
+                  (void*)p->d_ov_vals, (void*)p->d_ov_out, (void*)p->d_ov_acc, (void*)p->d_ov_rv,
+                  (void*)p->d_ov_meta})
     if (q) cudaFree(q);
   p->d_ov_rv = nullptr;
   p->d_union_rowmap = nullptr;
   p->d_ov_start = p->d_ov_rows = p->d_ov_out = p->d_ov_acc = nullptr;
   p->d_ov_vals = nullptr;
+  p->d_ov_meta = nullptr;
   if (int st = upload(&p->d_union_rowmap, rowmap, s)) return st;
   if (int st = upload(&p->d_ov_start, start, s)) return st;
   if (int st = upload(&p->d_ov_rows, rows, s)) return st;
   if (int st = upload(&p->d_ov_vals, vals, s)) return st;
   if (int st = upload(&p->d_ov_out, out_rows, s)) return st;
   if (int st = upload(&p->d_ov_acc, acc, s)) return st;
-  // K2 geometry: A^T block of T tokens + the column group's packed list in
-  // shared memory; split columns into more groups until the largest fits.
+  // K2 geometry: A^T block of T tokens for all K rows in shared memory;
+  // packed (row, value) lists need row < 2^16.  Each column's list starts on
+  // a 16-byte boundary and is zero-padded to whole groups of 4 * L entries
+  // (L = T / 8 lanes per column), so every lane fetches its next 4 entries
+  // with one 16-byte load.
   p->ov_block_tokens = 0;
-  const int64_t n_ov = (int64_t)ov_cols.size();
-  int T = 0, groups = 1;
-  if (k <= 65535 && n_ov > 0 && !env_int("TW_RESIDUAL_DIRECT", 0) &&
-      residual_geometry(k, (int64_t)rows.size() * 4, &T, &groups)) {
-    const int64_t limit = 227 * 1024 - (int64_t)k * T * 2;
-    for (;; ++groups) {
-      int64_t worst = 0;
-      for (int g = 0; g < groups; ++g) {
-        const int64_t c0 = (int64_t)g * n_ov / groups, c1 = (int64_t)(g + 1) * n_ov / groups;
-        worst = std::max<int64_t>(worst, start[c1] - start[c0]);
-      }
-      if (worst * 4 <= limit || groups >= n_ov) {
-        p->ov_max_group_nnz = (int32_t)worst;
-        break;
-      }
-    }
-    if ((int64_t)p->ov_max_group_nnz * 4 <= limit) {
+  p->ov_ctas_per_sm = 0;
+  p->ov_start = start;
+  if (k < 65535 && !ov_cols.empty() && !env_int("TW_RESIDUAL_DIRECT", 0)) {
+    int cps = 0;
+    const int T = residual_block_tokens(k, &cps);
+    if (T > 0) {
       p->ov_block_tokens = T;
-      p->ov_col_groups = groups;
-      std::vector<uint32_t> rv(rows.size());
-      for (size_t e = 0; e < rows.size(); ++e)
-        rv[e] = ((uint32_t)rows[e] << 16) |
-                (p->dtype == kBF16 ? float_to_bf16_bits(vals[e]) : float_to_half_bits(vals[e]));
+      p->ov_ctas_per_sm = cps;
+      const int G = 4 * (T / 8);
+      std::vector<uint32_t> rv;
+      std::vector<int4> meta(ov_cols.size());
+      for (size_t i = 0; i < ov_cols.size(); ++i) {
+        const int32_t n = start[i + 1] - start[i];
+        meta[i] = make_int4((int32_t)rv.size(), n, out_rows[i], acc[i]);
+        for (int32_t e = start[i]; e < start[i + 1]; ++e)
+          rv.push_back(((uint32_t)rows[e] << 16) |
+                       (p->dtype == kBF16 ? float_to_bf16_bits(vals[e]) : float_to_half_bits(vals[e])));
+        while (rv.size() % G) rv.push_back((uint32_t)k << 16);  // zero row, value 0
+      }
+      rv.resize(rv.size() + 2 * G, (uint32_t)k << 16);  // the pipeline fetches two groups ahead
       if (int st = upload(&p->d_ov_rv, rv, s)) return st;
+      if (int st = upload(&p->d_ov_meta, meta, s)) return st;
     }
   }
   TW_CUDA(cudaStreamSynchronize(s));
@@ -646,6 +651,7 @@ int tw_gemm_tew(const tw_plan* p, const void* x, int64_t m, int64_t ld_x, void* 
   r.rows = p->d_ov_rows;
   r.vals = p->d_ov_vals;
   r.out_rows = p->d_ov_out;
+  r.meta = p->d_ov_meta;
   r.accumulate = p->d_ov_acc;
   r.out = ct;
   r.ld_out = ld_ct;
@@ -655,8 +661,38 @@ int tw_gemm_tew(const tw_plan* p, const void* x, int64_t m, int64_t ld_x, void* 
   r.K = p->k;
   r.rv = p->d_ov_rv;
   r.block_tokens = p->ov_block_tokens;
-  r.col_groups = p->ov_col_groups;
-  r.max_group_nnz = p->ov_max_group_nnz;
+  if (r.block_tokens > 0) {
+    // grid = token blocks x column splits; splits (nnz-balanced runs of the
+    // descending-nnz column order) are added only to round the number of
+    // CTAs up to whole waves of resident CTAs
+    const int T = r.block_tokens;
+    const int64_t sms = p->sm_count;
+    r.n_blocks = (int32_t)((m + T - 1) / T);
+    int best = 1;
+    double best_eff = 0.0;
+    for (int ng = 1; ng <= 4 && ng <= p->n_ov_cols; ++ng) {
+      // CTAs are scheduled as slots free, so the busiest SM does about
+      // ceil(ctas / SMs) CTAs of 1 / ng of a block's work; each extra split
+      // re-stages the A^T block
+      const int64_t ctas = (int64_t)r.n_blocks * ng;
+      const int64_t per_sm = (ctas + sms - 1) / sms;
+      const double eff = (double)ctas / (double)(per_sm * sms) / (1.0 + 0.1 * (ng - 1));
+      if (eff > best_eff + 1e-9) {
+        best_eff = eff;
+        best = ng;
+      }
+    }
+    r.n_groups = best;
+    const int64_t total = p->ov_start.back();
+    int c = 0;
+    r.group_first[0] = 0;
+    for (int g = 1; g < r.n_groups; ++g) {
+      const int64_t target = total * g / r.n_groups;
+      while (c < p->n_ov_cols && p->ov_start[c] < target) ++c;
+      r.group_first[g] = std::max(c, r.group_first[g - 1]);
+    }
+    r.group_first[r.n_groups] = p->n_ov_cols;
+  }
   TW_CUDA(launch_tw_residual(r, s));
   return TW_OK;
 }

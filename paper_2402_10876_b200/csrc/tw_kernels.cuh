@@ -83,30 +83,33 @@ cudaError_t launch_tw_gemm(const CUtensorMap& map_pay, const CUtensorMap& map_ou
 cudaError_t configure_gemm_kernels();
 
 // K2: TEW residual, C'^T[urow(c)] (+)= sum_r A^T[r] * v over overlay column c.
+constexpr int kMaxColGroups = 64;
 struct ResidualArgs {
   const void* at;           // activations A^T [K][ld_at]
   int64_t ld_at;
   int32_t in_dtype;
-  const int32_t* col_start; // [n_cols + 1] CSC pointers into rows / vals
-  const int32_t* rows;      // [nnz] K rows
-  const float* vals;        // [nnz]
+  const int32_t* col_start; // [n_cols + 1] CSC pointers (columns in descending-nnz order)
+  const int32_t* rows;      // [nnz] K rows            (direct kernel)
+  const float* vals;        // [nnz]                   (direct kernel)
+  const uint32_t* rv;       // [nnz] row << 16 | 16-bit value; nullptr = direct kernel
   const int32_t* out_rows;  // [n_cols] output row (union position)
   const int32_t* accumulate;// [n_cols] 1 = add onto TW result, 0 = overwrite
+  const int4* meta;         // [n_cols] {first entry, entries, out row, accumulate}
   void* out;
   int64_t ld_out;
   int32_t out_dtype;
   int32_t M;
   int32_t n_cols;
   int32_t K;                // rows of A^T
-  const uint32_t* rv;       // [nnz] row << 16 | 16-bit value; nullptr = direct kernel
-  int32_t block_tokens;     // T of the staged A^T block
-  int32_t col_groups;       // column groups (contiguous in processing order)
-  int32_t max_group_nnz;    // largest group's nnz (shared-memory list size)
+  int32_t block_tokens;     // T: tokens of the staged A^T block (0 = direct kernel)
+  int32_t n_blocks;         // ceil(M / T): grid.x
+  int32_t n_groups;         // nnz-balanced column splits: grid.y
+  int32_t group_first[kMaxColGroups + 1];  // first column of every split
 };
 cudaError_t launch_tw_residual(const ResidualArgs& args, cudaStream_t stream);
-// Staged-block geometry of the overlay SpMM for K rows and a list of
-// `list_bytes` bytes: tokens per block and column groups; false = direct path.
-bool residual_geometry(int32_t K, int64_t list_bytes, int* T, int* groups);
+// Token-block size of the staged SpMM for K rows (0 = direct kernel) and the
+// number of resident CTAs per SM it allows.
+int residual_block_tokens(int32_t K, int* ctas_per_sm);
 
 // K4: A (M x K, row-major, lda) -> A^T (K x M, ld_at) with a dtype cast.
 cudaError_t launch_transpose_cast(const void* a, int32_t a_dtype, int64_t M, int64_t K,
