@@ -33,16 +33,17 @@
 // residency removes the payload re-reads, and the balanced split keeps the
 // busiest SM close to the mean.
 //
-// Roles (1 CTA per SM, 768 threads):
+// Roles (1 CTA per SM, 896 threads; 16 gather warps measured ~7% faster than
+// 12 and equal to 20):
 //   warp 0      payload producer (TMA 2-D boxes of 128 cols x 64 k, SW128).
 //   warp 1      TMEM allocator (2 x 256 columns: double-buffered accumulators)
 //               and MMA issuer: one thread, tcgen05.mma.kind::f16 M=128 N=n K=16.
-//   warps 4-15  gather producers: each stage is 64 kept A^T rows x n tokens as
+//   warps 4-19  gather producers: each stage is 64 kept A^T rows x n tokens as
 //               16-byte cp.async into the 128-B swizzled MN-major layout; row
 //               indices are prefetched one stage ahead in registers; every
 //               thread's copies arrive on the stage barrier asynchronously
 //               (cp.async.mbarrier.arrive.noinc).  A^T is read where it lies.
-//   warps 16-23 epilogue: warp w owns TMEM lanes 32*(w%4).. (output columns)
+//   warps 20-27 epilogue: warp w owns TMEM lanes 32*(w%4).. (output columns)
 //               and one 128-token half; tcgen05.ld -> fp16/bf16 -> swizzled
 //               smem -> TMA 2-D store per 32 x 32 block (16-byte stores for the
 //               TEW row scatter, ragged sub-tiles, partial blocks, fp32 out).
@@ -59,7 +60,7 @@ namespace {
 constexpr int kPayloadWarp = 0;
 constexpr int kMmaWarp = 1;
 constexpr int kGatherWarp0 = 4;
-constexpr int kGatherWarps = 12;
+constexpr int kGatherWarps = 16;
 constexpr int kGatherThreads = 32 * kGatherWarps;
 constexpr int kEpilogueWarp0 = kGatherWarp0 + kGatherWarps;
 constexpr int kEpilogueWarps = 8;
