@@ -42,20 +42,20 @@ __device__ __forceinline__ void store_from_float(void* p, int32_t dtype, int64_t
 // column range from there: 2 bytes of shared-memory traffic per FMA and ~1x
 // A^T of L2 reads for the staging.
 //
-// Grid = (token blocks, column splits); several small CTAs per SM give the
-// occupancy that hides the list loads.  After one barrier the warps walk
+// Grid = (token blocks, column splits), one 32-warp CTA per SM; T is as
+// large as shared memory allows so the column lists (re-read per block) are
+// amortised.  After one barrier the warps walk
 // their columns independently: a lane group of L = T / 8 lanes per column
 // (8 tokens per lane, one 16-byte shared load per entry), 32 / L columns per
 // warp step, columns in descending-nnz order (host) so the groups of a warp
-// finish together.  Each lane group fetches L packed entries (row << 16 |
-// 16-bit value, rounded like the TW payload) per global load, one chunk
+// finish together.  Each lane group fetches 2 L packed entries (row << 16 |
+// 16-bit value, rounded like the TW payload) per 8-byte load, two groups
 // ahead, and broadcasts them with shuffles; one fma.rn.f32.f16 (FHFMA: 16-bit
 // operands, fp32 accumulator, no conversions) per token, fp32 accumulation in ascending row order (CSC order of
 // patterns.py:145-214), then one read-modify-write of the TW result
 // (accumulate = 1) or a plain store (residual-only column).
-constexpr int kResThreads = 256;
+constexpr int kResThreads = 1024;  // 32 warps: one CTA per SM, 64 registers per thread
 constexpr int kResWarps = kResThreads / 32;
-constexpr int kResCtasPerSm = 4;  // register budget: 64 per thread
 
 __device__ __forceinline__ float2 h2_to_f2(uint32_t u, bool bf) {
   if (bf) return make_float2(__uint_as_float(u << 16), __uint_as_float(u & 0xFFFF0000u));
@@ -128,7 +128,7 @@ __device__ __forceinline__ void residual_store4(const ResidualArgs& args, int64_
 }
 
 template <int T, bool kBf>
-__global__ void __launch_bounds__(kResThreads, kResCtasPerSm)
+__global__ void __launch_bounds__(kResThreads, 1)
     tw_residual_kernel(const __grid_constant__ ResidualArgs args) {
   extern __shared__ __align__(16) uint8_t res_smem[];
   uint16_t* sA = reinterpret_cast<uint16_t*>(res_smem);  // [K][T]
@@ -163,9 +163,8 @@ __global__ void __launch_bounds__(kResThreads, kResCtasPerSm)
   // One column per lane group per step; the next step's metadata is
   // prefetched one step ahead.
   constexpr int kStep = kCols * kResWarps;
-  constexpr int G = 4 * L;  // entries per group (4 per lane, one 16-byte load)
+  constexpr int G = 2 * L;  // entries per group (2 per lane, one 8-byte load)
   const uint32_t zrow = static_cast<uint32_t>(K) << 16;
-  const uint4 zero4 = make_uint4(zrow, zrow, zrow, zrow);
   const uint8_t* sAb = reinterpret_cast<const uint8_t*>(sAt);
   const bool fast = args.out_dtype != kF32 && args.ld_out % 8 == 0;
   int cs = c0 + warp * kCols;
@@ -185,21 +184,21 @@ __global__ void __launch_bounds__(kResThreads, kResCtasPerSm)
     float ac[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) ac[i] = 0.f;
-    // entry groups: lane tl holds entries 4 tl .. 4 tl + 3 of a group;
+    // entry groups: lane tl holds entries 2 tl, 2 tl + 1 of a group;
     // groups gi + 1, gi + 2 are in flight while gi is consumed.  Lists are
     // padded to whole groups with zero-row entries (row K of the block is
     // zero) and a lane group past its list substitutes them, so the entry
     // loop has no branches.
-    const uint4* lp = reinterpret_cast<const uint4*>(args.rv + m.x) + tl;
-    uint4 c = __ldg(lp), n1 = __ldg(lp + L);
+    const uint2* lp = reinterpret_cast<const uint2*>(args.rv + m.x) + tl;
+    uint2 c = __ldg(lp), n1 = __ldg(lp + L);
     for (int eo = 0; eo < maxlen; eo += G) {
-      const uint4 f = __ldg(lp + 2 * L);
+      const uint2 f = __ldg(lp + 2 * L);
       lp += L;
-      if (eo >= m.y) c = zero4;
-      const uint32_t w[4] = {c.x, c.y, c.z, c.w};
+      if (eo >= m.y) c = make_uint2(zrow, zrow);
+      const uint32_t w[2] = {c.x, c.y};
 #pragma unroll
       for (int j = 0; j < G; ++j) {
-        const uint32_t q = L == 1 ? w[j & 3] : __shfl_sync(0xffffffffu, w[j & 3], gbase + (j >> 2));
+        const uint32_t q = L == 1 ? w[j & 1] : __shfl_sync(0xffffffffu, w[j & 1], gbase + (j >> 1));
         fma8<kBf>(ac, *reinterpret_cast<const uint4*>(sAb + (q >> 16) * (T * 2)),
                   static_cast<uint16_t>(q & 0xFFFFu));
       }
@@ -290,14 +289,15 @@ __global__ void build_payload_kernel(const PayloadArgs args) {
 }  // namespace
 
 int residual_block_tokens(int32_t K, int* ctas_per_sm) {
-  // T tokens per CTA (8 per lane): the A^T block (K + 1) * T * 2 bytes
-  // stays <= 56 KB so four 256-thread CTAs share an SM; T = 16 before 32
-  // keeps >= 3 CTAs per SM in flight at M = 8192
-  constexpr int64_t kMaxBlock = 56 * 1024;
-  for (int T : {16, 8}) {
+  // T tokens per CTA (8 per lane): the largest block (K + 1) * T * 2 bytes
+  // of at most ~200 KB, so the column lists (re-read once per block) are
+  // amortised over as many tokens as shared memory allows; one 32-warp CTA
+  // per SM hides the list loads
+  constexpr int64_t kMaxBlock = 200 * 1024;
+  for (int T : {64, 32, 16}) {
     const int64_t bytes = static_cast<int64_t>(K + 1) * T * 2;
     if (bytes <= kMaxBlock) {
-      *ctas_per_sm = static_cast<int>(std::min<int64_t>(kResCtasPerSm, (220 * 1024) / (bytes + 1024)));
+      *ctas_per_sm = 1;
       return T;
     }
   }
@@ -326,8 +326,9 @@ static cudaError_t launch_res(const ResidualArgs& args, cudaStream_t stream) {
 cudaError_t launch_tw_residual(const ResidualArgs& args, cudaStream_t stream) {
   if (args.n_cols <= 0 || args.M <= 0) return cudaSuccess;
   switch (args.rv ? args.block_tokens : 0) {
+    case 64: return launch_res<64>(args, stream);
+    case 32: return launch_res<32>(args, stream);
     case 16: return launch_res<16>(args, stream);
-    case 8: return launch_res<8>(args, stream);
     default: break;
   }
   dim3 grid(static_cast<unsigned>((args.M + 255) / 256), static_cast<unsigned>(args.n_cols));
