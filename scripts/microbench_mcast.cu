@@ -131,7 +131,7 @@ int main() {
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
-  for (int share : {1, -1, -2}) for (int csz : {1}) {
+  for (int share : {1, -1, -2}) for (int csz : {1, 2, 4}) {
     for (int mode : {0, 1}) {
       if (mode == 1 && csz == 1) continue;
       if (share > 1 && mode == 1) continue;
