@@ -402,32 +402,60 @@ def run_ours(args, cfg, rank: int, world: int) -> None:
     prep_ms = p0.elapsed_time(p1) / args.steps
     del prep_graphs
 
-    # ---- e2e through the public API from pinned host memory
+    # ---- e2e through the public API from pinned host memory: per layer
+    # H2D of A (M x K fp16, the reference layout) -> prepare (K4) -> run (K1
+    # [+ K2]) -> D2H of the native C'^T.  Three streams pipeline the layers:
+    # the copy engines (H2D, D2H: full duplex) overlap each other and the
+    # kernels; events order every reuse of a device buffer.
     host_a = [torch.from_numpy(activations(cfg, L["k"], li, rank)).to(torch.float16)
               .pin_memory() for li, L in enumerate(layers)]
-    host_c = [torch.empty((s[2].shape[1], s[2].shape[0]), dtype=torch.float16).pin_memory()
+    host_c = [torch.empty(tuple(s[2].shape), dtype=torch.float16).pin_memory()
               for s in sets[0]]
-    dev_a = [torch.empty(h.shape, dtype=torch.float16, device=dev) for h in host_a]
+    dev_a = [[torch.empty(h.shape, dtype=torch.float16, device=dev) for h in host_a]
+             for _ in range(2)]
     h2d = sum(h.numel() * h.element_size() for h in host_a)
     d2h = sum(h.numel() * h.element_size() for h in host_c)
+    s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
+    nl = len(layers)
+    ev = lambda: torch.cuda.Event()  # noqa: E731
+    ev_in = [[ev() for _ in range(nl)] for _ in range(2)]
+    ev_comp = [[ev() for _ in range(nl)] for _ in range(2)]
+    ev_out = [[ev() for _ in range(nl)] for _ in range(N_ROTATE)]
+    for e_list in ev_comp + ev_out:
+        for e_ in e_list:
+            e_.record(stream)
 
     def e2e_step(i: int):
-        for li, (plan, _, ct) in enumerate(sets[i % N_ROTATE]):
-            dev_a[li].copy_(host_a[li], non_blocking=True)
-            at = plan.prepare(dev_a[li])
+        p, r = i % 2, i % N_ROTATE
+        for li in range(nl):
+            s_in.wait_event(ev_comp[p][li])        # dev_a[p][li] consumed two steps ago
+            with torch.cuda.stream(s_in):
+                dev_a[p][li].copy_(host_a[li], non_blocking=True)
+                ev_in[p][li].record(s_in)
+        for li, (plan, _, ct) in enumerate(sets[r]):
+            stream.wait_event(ev_in[p][li])
+            stream.wait_event(ev_out[r][li])       # ct's previous D2H is done
+            at = plan.prepare(dev_a[p][li])
             if tew:
                 plan.run_tew(at, out=ct)
             else:
                 plan.run(at, out=ct)
-            host_c[li].copy_(ct.t(), non_blocking=True)
+            ev_comp[p][li].record(stream)
+            s_out.wait_event(ev_comp[p][li])
+            with torch.cuda.stream(s_out):
+                host_c[li].copy_(ct, non_blocking=True)
+                ev_out[r][li].record(s_out)
 
     for i in range(args.warmup):
         e2e_step(i)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
+    s_in.wait_event(e0)
+    s_out.wait_event(e0)
     for i in range(args.steps):
         e2e_step(i)
+    stream.wait_stream(s_out)
     e1.record(stream)
     torch.cuda.synchronize()
     te = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
@@ -488,7 +516,9 @@ def run_ours(args, cfg, rank: int, world: int) -> None:
         "frac_of_dense_peak": value / world / pk["tc"],
         "e2e": {"value": e2e_value, "unit": "TFLOP/s", "ms_per_step": e2e_ms,
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "path": "pinned host fp16 A (M x K) -> H2D -> tw_transpose_cast -> tw_gemm -> D2H fp16"},
+                "path": "pinned host fp16 A (M x K) -> H2D -> TwPlan.prepare (K4) -> TwPlan.run "
+                        "(K1) -> D2H of the fp16 C'^T; layers pipelined over H2D / compute / "
+                        "D2H streams"},
         "roofline": roofline,
         "cpu_baseline": {"value": cpu_rate, "unit": "TFLOP/s", "cores": workers, "kind": "port",
                          "sample": f"{m_sample} of {m} tokens through every layer "

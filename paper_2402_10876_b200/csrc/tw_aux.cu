@@ -250,7 +250,7 @@ __global__ void __launch_bounds__(256)
   store_from_float(args.out, args.out_dtype, base, acc);
 }
 
-// 32 x 32 shared-memory transpose with dtype conversion.
+// 32 x 32 shared-memory transpose with dtype conversion (general fallback).
 __global__ void transpose_cast_kernel(const void* a, int32_t a_dtype, int64_t M, int64_t K,
                                       int64_t lda, void* at, int32_t at_dtype, int64_t ld_at) {
   __shared__ float tile[32][33];
@@ -264,6 +264,45 @@ __global__ void transpose_cast_kernel(const void* a, int32_t a_dtype, int64_t M,
   for (int i = threadIdx.y; i < 32; i += blockDim.y) {
     const int64_t k = k0 + i, m = m0 + threadIdx.x;
     if (k < K && m < M) store_from_float(at, at_dtype, k * ld_at + m, tile[threadIdx.x][i]);
+  }
+}
+
+// 16-bit -> 16-bit (same type) 64 x 64 tile transpose with 16-byte loads and
+// stores: each thread reads 8 consecutive k of a row of A and writes 8
+// consecutive m of a row of A^T.  Needs M, K, lda, ld_at multiples of 8 and
+// 16-byte aligned bases.
+__global__ void __launch_bounds__(256) transpose16_kernel(const uint16_t* a, int64_t M, int64_t K,
+                                                          int64_t lda, uint16_t* at,
+                                                          int64_t ld_at) {
+  // [m][k] with the 8-element k-chunk index XOR-swizzled by (m / 8) % 8, so
+  // the column reads of the second phase hit 8 different banks
+  __shared__ __align__(16) uint16_t tile[64][64];
+  const int64_t k0 = static_cast<int64_t>(blockIdx.x) * 64;
+  const int64_t m0 = static_cast<int64_t>(blockIdx.y) * 64;
+  const int t = threadIdx.x;
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    const int idx = t + r * 256;
+    const int mi = idx >> 3, kc = idx & 7;
+    const int64_t m = m0 + mi, k = k0 + kc * 8;
+    uint4 v = make_uint4(0u, 0u, 0u, 0u);
+    if (m < M && k < K) v = *reinterpret_cast<const uint4*>(a + m * lda + k);
+    *reinterpret_cast<uint4*>(&tile[mi][(kc ^ ((mi >> 3) & 7)) * 8]) = v;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    const int idx = t + r * 256;
+    const int ki = idx >> 3, mc = idx & 7;
+    const int64_t k = k0 + ki, m = m0 + mc * 8;
+    if (k >= K || m >= M) continue;
+    const int col = ((ki >> 3) ^ mc) * 8 + (ki & 7);
+    uint32_t w[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      w[j] = static_cast<uint32_t>(tile[mc * 8 + 2 * j][col]) |
+             (static_cast<uint32_t>(tile[mc * 8 + 2 * j + 1][col]) << 16);
+    *reinterpret_cast<uint4*>(at + k * ld_at + m) = make_uint4(w[0], w[1], w[2], w[3]);
   }
 }
 
@@ -340,6 +379,15 @@ cudaError_t launch_transpose_cast(const void* a, int32_t a_dtype, int64_t M, int
                                   int64_t lda, void* at, int32_t at_dtype, int64_t ld_at,
                                   cudaStream_t stream) {
   if (M <= 0 || K <= 0) return cudaSuccess;
+  const bool fast = a_dtype == at_dtype && a_dtype != kF32 && M % 8 == 0 && K % 8 == 0 &&
+                    lda % 8 == 0 && ld_at % 8 == 0 &&
+                    reinterpret_cast<uintptr_t>(a) % 16 == 0 && reinterpret_cast<uintptr_t>(at) % 16 == 0;
+  if (fast) {
+    dim3 grid(static_cast<unsigned>((K + 63) / 64), static_cast<unsigned>((M + 63) / 64));
+    transpose16_kernel<<<grid, 256, 0, stream>>>(static_cast<const uint16_t*>(a), M, K, lda,
+                                                  static_cast<uint16_t*>(at), ld_at);
+    return cudaGetLastError();
+  }
   dim3 grid(static_cast<unsigned>((K + 31) / 32), static_cast<unsigned>((M + 31) / 32));
   dim3 block(32, 8);
   transpose_cast_kernel<<<grid, block, 0, stream>>>(a, a_dtype, M, K, lda, at, at_dtype, ld_at);

@@ -239,3 +239,22 @@ def test_column_shards_concatenate_bit_identical(world):
         parts.append(part)
     stacked = torch.cat(parts, dim=0)
     assert torch.equal(stacked, full)
+
+
+@pytest.mark.parametrize("m,k,src,dst", [
+    (8192, 768, "fp16", "fp16"),    # 16-byte tile path
+    (136, 72, "bf16", "bf16"),      # 16-byte tile path, partial tiles
+    (77, 50, "fp16", "fp16"),       # ragged: general path
+    (64, 96, "fp32", "fp16"),       # cast: general path
+    (40, 24, "fp32", "bf16"),
+])
+def test_transpose_cast_exact(m, k, src, dst):
+    """K4 (A -> A^T + cast) equals torch's transpose + rounding bit for bit."""
+    import torch
+
+    dt = {"fp16": torch.float16, "bf16": torch.bfloat16, "fp32": torch.float32}
+    g = torch.Generator(device="cuda").manual_seed(m + k)
+    a = torch.randn((m, k), device="cuda", generator=g).to(dt[src])
+    at = tw.prepare_activations(a, dst)
+    assert tuple(at.shape) == (k, m)
+    assert torch.equal(at, a.t().to(dt[dst]))
