@@ -109,6 +109,16 @@ class TwPlan:
             self.attach_overlay(overlay)
         self._refresh_info()
 
+    @classmethod
+    def from_cto1(cls, path, overlay: Optional[SparseOverlay] = None,
+                  compute_dtype: str = "fp16", schedule: str = "lpt") -> "TwPlan":
+        """Device plan straight from a CTO1 artifact: the file
+        is read and validated like reference read_cto1 (formats.py:259-304)
+        and the GPU weight format is built from it without re-pruning."""
+        from .formats import read_cto1
+
+        return cls(read_cto1(path), overlay, compute_dtype, schedule)
+
     # -- metadata -------------------------------------------------------
     def _refresh_info(self) -> None:
         lib = _native.load_library()

@@ -1,0 +1,100 @@
+"""Layer chaining in the condensed C'^T layout and CTO1 ->
+device plans (8f-2).
+
+CPU: the chained encoding of layer l+1 applied to layer l's condensed output
+equals layer l+1 applied to the expanded output (zeros at pruned columns),
+exactly (the oracle sums in fp64 in ascending row order; the dropped terms are
+products with exact zeros).  GPU: the chained plan consumes layer l's C'^T
+buffer directly.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import paper_2402_10876_b200 as tw
+from oracle import tilesparse_oracle as orc
+
+
+def _layers(seed=0, k=256, n1=512, n2=192, s1=0.75, s2=0.6, g=64):
+    rng = np.random.default_rng(seed)
+    w1 = tw.round_to(rng.normal(size=(k, n1)).astype(np.float32), "fp16")
+    w2 = tw.round_to(rng.normal(size=(n1, n2)).astype(np.float32), "fp16")
+    _, t1 = tw.prune_tw(w1, s1, g)
+    _, t2 = tw.prune_tw(w2, s2, g)
+    return tw.encode_cto(t1), t1, tw.encode_cto(t2), t2
+
+
+def test_chain_encoding_equals_expanded_product():
+    e1, t1, e2, t2 = _layers()
+    rng = np.random.default_rng(1)
+    a = tw.round_to(rng.normal(size=(40, 256)).astype(np.float32), "fp16")
+    h = orc.c_gemm_cto_enc(a, e1).astype(np.float32)          # condensed M x N1'
+    full = np.zeros((h.shape[0], e2.original_dims[0]), dtype=np.float32)
+    full[:, t1.column_mask.kept] = h                           # GemmOutput.expand
+    ref = orc.c_gemm_cto_enc(full, e2)
+    chained = tw.chain_encoding(e2, t1.column_mask.kept)
+    assert chained.original_dims == (t1.n_condensed, e2.original_dims[1])
+    out = orc.c_gemm_cto_enc(h, chained)
+    assert np.array_equal(out, ref)
+    # only MACs on surviving inputs remain
+    assert int(chained.row_counts.sum()) <= int(e2.row_counts.sum())
+
+
+def test_chain_tile_with_no_surviving_rows_outputs_zero():
+    rng = np.random.default_rng(3)
+    w2 = tw.round_to(rng.normal(size=(64, 16)).astype(np.float32), "fp16")
+    _, t2 = tw.prune_tw(w2, 0.5, 8)
+    e2 = tw.encode_cto(t2)
+    # previous layer kept only rows no tile of layer 2 uses
+    used = set()
+    for i in range(e2.tile_count):
+        used.update(e2.tile_rows(i).tolist())
+    unused = [r for r in range(64) if r not in used]
+    prev = unused if unused else [0]
+    chained = tw.chain_encoding(e2, prev)
+    h = rng.normal(size=(5, len(prev))).astype(np.float32)
+    out = orc.c_gemm_cto_enc(h, chained)
+    full = np.zeros((5, 64), dtype=np.float32)
+    full[:, prev] = h
+    assert np.array_equal(out, orc.c_gemm_cto_enc(full, e2))
+
+
+def test_chain_rejects_bad_columns():
+    _, _, e2, _ = _layers()
+    with pytest.raises(tw.InvalidInputError):
+        tw.chain_encoding(e2, [3, 2])
+    with pytest.raises(tw.InvalidInputError):
+        tw.chain_encoding(e2, [0, e2.original_dims[0]])
+
+
+@pytest.mark.gpu
+def test_chained_plans_on_gpu():
+    """layer 1 -> C'^T (fp16) -> chained layer 2 reads it in place."""
+    import torch
+
+    e1, t1, e2, t2 = _layers(seed=5, k=768, n1=3072, n2=768, s1=0.75, s2=0.75, g=128)
+    rng = np.random.default_rng(6)
+    a = tw.round_to(rng.normal(size=(1000, 768)).astype(np.float32), "fp16")
+    p1 = tw.TwPlan(e1)
+    p2 = tw.TwPlan(tw.chain_encoding(e2, p1.condensed_columns))
+    h = p1.run(p1.prepare(a), out_dtype="fp16")               # N1' x M, the next A^T
+    out = p2.run(h)                                             # no expand / transpose
+    hh = h.t().float().cpu().numpy()
+    full = np.zeros((1000, 3072), dtype=np.float32)
+    full[:, t1.column_mask.kept] = hh
+    ref = orc.c_gemm_cto_enc(full, e2)
+    assert tw.relative_error(out.t(), ref) <= 1e-5
+    torch.cuda.synchronize()
+
+
+@pytest.mark.gpu
+def test_plan_from_cto1_file(tmp_path):
+    e1, t1, _, _ = _layers(seed=7)
+    path = tmp_path / "w.cto1"
+    tw.write_cto1(path, e1)
+    a = tw.round_to(np.random.default_rng(8).normal(size=(64, 256)).astype(np.float32), "fp16")
+    p = tw.TwPlan.from_cto1(path)
+    out = p.run(p.prepare(a))
+    assert tw.relative_error(out.t(), orc.c_gemm_cto_enc(a, e1)) <= 1e-5
