@@ -82,8 +82,12 @@ struct Cfg {
   static constexpr int kPayloadRegion = kRes ? kResSteps * kPBytes : 0;
   static constexpr int kBarrierBytes = 256;
   static constexpr int kSubBytes = kRes ? 0 : kMaxSmemSub * static_cast<int>(sizeof(SubTile));
+  // owner mode: the owned sub-tile's whole gather list, staged once
+  static constexpr int kIdxCap = kRes ? kResSteps * kBK : 60 * kBK;
+  static constexpr int kIdxBytes = kIdxCap * 4;
   static constexpr int kSmemBytes = kStages * kStageBytes + kPayloadRegion +
-                                    kEpilogueWarps * kStgBytes + kBarrierBytes + kSubBytes + 1024;
+                                    kEpilogueWarps * kStgBytes + kBarrierBytes + kSubBytes +
+                                    kIdxBytes + 1024;
   static_assert(kSmemBytes <= 227 * 1024, "shared memory budget");
   static_assert(2 * kStages + kResSteps + 4 + 1 <= kBarrierBytes / 8, "barrier region");
 };
@@ -267,6 +271,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* pfull = tempty + 2;  // resident payload, one barrier per k-step
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pfull + kResSteps);
   SubTile* sub_smem = reinterpret_cast<SubTile*>(bar_region + C::kBarrierBytes);
+  int32_t* sIdx = reinterpret_cast<int32_t*>(bar_region + C::kBarrierBytes + C::kSubBytes);
   long long* trace = args.trace ? args.trace + static_cast<int64_t>(blockIdx.x) * 4096 : nullptr;
 
   const int warp = threadIdx.x >> 5;
@@ -376,12 +381,28 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     };
     auto unit_n = [](const Seg& g) { return (g.ue - g.ub + 15) & ~15; };
-    auto load_idx = [&](const Seg& g, int ks, int (&idx)[kMaxItems]) {
-      const int32_t* src = args.gidx + static_cast<int64_t>(g.d.idx_row) * args.kp + ks * kBK;
-#pragma unroll
-      for (int i = 0; i < kMaxItems; ++i) idx[i] = slot_row[i] >= 0 ? __ldg(src + slot_row[i]) : -1;
-    };
+    // Owner mode: the owned sub-tile's gather list is staged in shared
+    // memory once (plan constants: before the dependency wait), so a stage's
+    // row indices are a shared load away -- with indices prefetched from
+    // global only one stage ahead, their L2 latency paced the whole gather.
     bool have = walk.next(args, sg);
+    const bool idx_smem = args.owner && have && sg.d.kp_steps * kBK <= C::kIdxCap;
+    if (idx_smem) {
+      const int32_t* src = args.gidx + static_cast<int64_t>(sg.d.idx_row) * args.kp;
+      for (int i = gt; i < sg.d.kp_steps * kBK; i += kGatherThreads) sIdx[i] = __ldg(src + i);
+      named_bar_sync(1, kGatherThreads);
+    }
+    auto load_idx = [&](const Seg& g, int ks, int (&idx)[kMaxItems]) {
+      if (idx_smem) {
+        const int32_t* src = sIdx + ks * kBK;
+#pragma unroll
+        for (int i = 0; i < kMaxItems; ++i) idx[i] = slot_row[i] >= 0 ? src[slot_row[i]] : -1;
+      } else {
+        const int32_t* src = args.gidx + static_cast<int64_t>(g.d.idx_row) * args.kp + ks * kBK;
+#pragma unroll
+        for (int i = 0; i < kMaxItems; ++i) idx[i] = slot_row[i] >= 0 ? __ldg(src + slot_row[i]) : -1;
+      }
+    };
     int ks = 0;
     int idx[kMaxItems];
     if (have) {
