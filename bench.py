@@ -263,7 +263,10 @@ def run_ours(args, cfg, rank: int, world: int) -> None:
     for r in range(N_ROTATE):
         layer_set = []
         for li, L in enumerate(layers):
-            plan = tw.TwPlan(L["enc"], L["ov"], compute_dtype="fp16")
+            # TW layers take their activations in the plan's row-run layout
+            # (prepare() writes it); TEW plans keep the natural order
+            plan = tw.TwPlan(L["enc"], L["ov"], compute_dtype="fp16",
+                             row_layout="natural" if tew else "runs")
             a = activations(cfg, L["k"], li, rank)
             at = plan.prepare(torch.from_numpy(a).to(dev))
             rows = plan.info.n_union if tew else plan.info.n_condensed
@@ -390,7 +393,7 @@ def run_ours(args, cfg, rank: int, world: int) -> None:
 
     def prep_set(r: int):
         for li, (plan, at, _) in enumerate(sets[r]):
-            tw.prepare_activations(a_dev[li], plan.compute_dtype, out=at)
+            plan.prepare(a_dev[li], out=at)
 
     prep_graphs = [capture_graph(lambda r=r: prep_set(r)) for r in range(N_ROTATE)]
     p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -506,7 +509,7 @@ def run_ours(args, cfg, rank: int, world: int) -> None:
                    "l2": f"{N_ROTATE} rotating buffer sets (weights, A^T, C^T) > 2x L2"},
         "speedup_vs_cublas": dense_ms / ms_step,
         "transpose": {"ms_per_step": prep_ms,
-                 "what": "A (M x K fp16, device, row-major) -> A^T per layer (tw_transpose_cast); "
+                 "what": "A (M x K fp16, device, row-major) -> A^T per layer (TwPlan.prepare: K4 + row order); "
                          "only for row-major callers (a TW layer's C'^T output is already the "
                          "next layer's A^T); inside e2e",
                  "value_incl_transpose": world * flops_step / ((ms_step + prep_ms) * 1e-3) / 1e12,

@@ -51,6 +51,10 @@ extern "C" {
 #define TW_F16 1
 #define TW_BF16 2
 
+/* Activation row layouts (tw_gemm_ex). */
+#define TW_LAYOUT_NATURAL 0        /* A^T rows in original K order             */
+#define TW_LAYOUT_PLAN 1           /* the plan's row order (tw_plan_prepare)   */
+
 /* Sub-tile visiting order inside each token block
  * (executor.py:206-227 schedule_tiles strategies). */
 #define TW_SCHEDULE_LPT 0          /* descending surviving K'             */
@@ -71,6 +75,8 @@ typedef struct tw_plan_info {
   int64_t kept_macs_per_token;/* sum_i width_i * K'_i (+ nnz for TEW)    */
   int32_t sm_count;           /* SMs of the plan's device                */
   int32_t has_overlay;
+  int32_t row_runs;           /* 1: the plan has a permuted row layout in
+                                 which every tile's kept rows form runs     */
 } tw_plan_info;
 
 /* Build a device plan from a CTO encoding held in host memory.
@@ -82,12 +88,15 @@ typedef struct tw_plan_info {
  *   row_offsets: n_tiles x max_rows u32, col_offsets: n_tiles x max_cols u32,
  *   payload: sum(row_counts[i]*col_counts[i]) fp32, per tile transposed
  *            (width x kept rows, kept rows contiguous; formats.py:200).
+ * row_runs = 1 lets the plan choose a permuted row layout in which every
+ * tile's kept rows form runs (tiles' K' then follow that order; see
+ * tw_plan_prepare / tw_gemm_ex); 0 keeps ascending kept-row order.
  * Synchronises `stream` before returning. */
 TW_API int tw_plan_create_cto(tw_plan** out, int32_t k, int32_t n, int32_t g, int32_t n_tiles,
                        const uint32_t* row_counts, const uint32_t* col_counts,
                        const uint32_t* row_offsets, int32_t max_rows,
                        const uint32_t* col_offsets, int32_t max_cols, const float* payload,
-                       int32_t compute_dtype, int32_t schedule, void* stream);
+                       int32_t compute_dtype, int32_t schedule, int32_t row_runs, void* stream);
 
 /* Attach a TEW overlay (CSC, int64 like patterns.SparseOverlay,
  * patterns.py:145-214).  Replaces the overlap/dims checks of
@@ -111,6 +120,24 @@ TW_API int tw_plan_union_columns(const tw_plan* plan, int32_t* out_cols);
  * are bit-identical on the GPU as in the reference. */
 TW_API int tw_gemm(const tw_plan* plan, const void* at, int64_t m, int64_t ld_at, void* ct,
                    int64_t ld_ct, int32_t out_dtype, void* stream);
+
+/* tw_gemm with the activation row layout given: TW_LAYOUT_NATURAL (A^T rows
+ * in K order, kept rows gathered with cp.async) or TW_LAYOUT_PLAN (A^T as
+ * tw_plan_prepare writes it; on plans with row_runs, every stage is a few
+ * dense TMA boxes).  Both layouts give bit-identical results. */
+TW_API int tw_gemm_ex(const tw_plan* plan, const void* at, int64_t m, int64_t ld_at, void* ct,
+                      int64_t ld_ct, int32_t out_dtype, int32_t at_layout, void* stream);
+
+/* A (m x k row-major, pitch lda, any dtype) -> A^T in the plan's row layout and
+ * compute dtype (k x m, pitch ld_at): tw_transpose_cast plus the plan's row
+ * permutation.  Replaces the as_matrix / astype copies (core.py:32-43,
+ * executor.py:158) for inputs of this plan. */
+TW_API int tw_plan_prepare(const tw_plan* plan, const void* a, int32_t a_dtype, int64_t m,
+                           int64_t lda, void* at, int64_t ld_at, void* stream);
+
+/* Original K row held at each position of the plan's row layout (host buffer
+ * of k entries; the identity when row_runs == 0). */
+TW_API int tw_plan_row_order(const tw_plan* plan, int32_t* out_rows);
 
 /* TEW product over the union columns: ct[|union| x M].
  * Replaces: executor.gemm_tew (executor.py:180-203). */

@@ -16,6 +16,7 @@ from .errors import DeviceError, raise_for_status
 LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libtwgemm.so"
 
 TW_F32, TW_F16, TW_BF16 = 0, 1, 2
+TW_LAYOUT_NATURAL, TW_LAYOUT_PLAN = 0, 1
 SCHEDULES = {"lpt": 0, "round_robin": 1}
 
 _c_int = ctypes.c_int
@@ -32,18 +33,21 @@ class PlanInfo(ctypes.Structure):
     _fields_ = [("k", _i32), ("n", _i32), ("g", _i32), ("n_tiles", _i32), ("n_sub", _i32),
                 ("bn", _i32), ("kp", _i32), ("n_condensed", _i32), ("n_union", _i32),
                 ("compute_dtype", _i32), ("nnz", _i64), ("kept_macs_per_token", _i64),
-                ("sm_count", _i32), ("has_overlay", _i32)]
+                ("sm_count", _i32), ("has_overlay", _i32), ("row_runs", _i32)]
 
 
 # name -> (restype, argtypes); must match include/tw_gemm.h exactly
 SIGNATURES = {
     "tw_plan_create_cto": (_c_int, [ctypes.POINTER(_vp), _i32, _i32, _i32, _i32, _u32p, _u32p,
-                                    _u32p, _i32, _u32p, _i32, _f32p, _i32, _i32, _vp]),
+                                    _u32p, _i32, _u32p, _i32, _f32p, _i32, _i32, _i32, _vp]),
     "tw_plan_attach_overlay": (_c_int, [_vp, _i32, _i32, _i64, _i64p, _i64p, _f32p, _vp]),
     "tw_plan_get_info": (_c_int, [_vp, ctypes.POINTER(PlanInfo)]),
     "tw_plan_condensed_columns": (_c_int, [_vp, _i32p]),
     "tw_plan_union_columns": (_c_int, [_vp, _i32p]),
     "tw_gemm": (_c_int, [_vp, _vp, _i64, _i64, _vp, _i64, _i32, _vp]),
+    "tw_gemm_ex": (_c_int, [_vp, _vp, _i64, _i64, _vp, _i64, _i32, _i32, _vp]),
+    "tw_plan_prepare": (_c_int, [_vp, _vp, _i32, _i64, _i64, _vp, _i64, _vp]),
+    "tw_plan_row_order": (_c_int, [_vp, _i32p]),
     "tw_gemm_tew": (_c_int, [_vp, _vp, _i64, _i64, _vp, _i64, _i32, _vp]),
     "tw_transpose_cast": (_c_int, [_vp, _i32, _i64, _i64, _i64, _vp, _i32, _i64, _vp]),
     "tw_plan_destroy": (None, [_vp]),

@@ -252,7 +252,8 @@ __global__ void __launch_bounds__(256)
 
 // 32 x 32 shared-memory transpose with dtype conversion (general fallback).
 __global__ void transpose_cast_kernel(const void* a, int32_t a_dtype, int64_t M, int64_t K,
-                                      int64_t lda, void* at, int32_t at_dtype, int64_t ld_at) {
+                                      int64_t lda, void* at, int32_t at_dtype, int64_t ld_at,
+                                      const int32_t* out_row) {
   __shared__ float tile[32][33];
   const int64_t k0 = static_cast<int64_t>(blockIdx.x) * 32;
   const int64_t m0 = static_cast<int64_t>(blockIdx.y) * 32;
@@ -263,7 +264,10 @@ __global__ void transpose_cast_kernel(const void* a, int32_t a_dtype, int64_t M,
   __syncthreads();
   for (int i = threadIdx.y; i < 32; i += blockDim.y) {
     const int64_t k = k0 + i, m = m0 + threadIdx.x;
-    if (k < K && m < M) store_from_float(at, at_dtype, k * ld_at + m, tile[threadIdx.x][i]);
+    if (k < K && m < M) {
+      const int64_t ko = out_row ? __ldg(out_row + k) : k;
+      store_from_float(at, at_dtype, ko * ld_at + m, tile[threadIdx.x][i]);
+    }
   }
 }
 
@@ -273,7 +277,7 @@ __global__ void transpose_cast_kernel(const void* a, int32_t a_dtype, int64_t M,
 // 16-byte aligned bases.
 __global__ void __launch_bounds__(256) transpose16_kernel(const uint16_t* a, int64_t M, int64_t K,
                                                           int64_t lda, uint16_t* at,
-                                                          int64_t ld_at) {
+                                                          int64_t ld_at, const int32_t* out_row) {
   // [m][k] with the 8-element k-chunk index XOR-swizzled by (m / 8) % 8, so
   // the column reads of the second phase hit 8 different banks
   __shared__ __align__(16) uint16_t tile[64][64];
@@ -297,12 +301,13 @@ __global__ void __launch_bounds__(256) transpose16_kernel(const uint16_t* a, int
     const int64_t k = k0 + ki, m = m0 + mc * 8;
     if (k >= K || m >= M) continue;
     const int col = ((ki >> 3) ^ mc) * 8 + (ki & 7);
+    const int64_t ko = out_row ? __ldg(out_row + k) : k;
     uint32_t w[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j)
       w[j] = static_cast<uint32_t>(tile[mc * 8 + 2 * j][col]) |
              (static_cast<uint32_t>(tile[mc * 8 + 2 * j + 1][col]) << 16);
-    *reinterpret_cast<uint4*>(at + k * ld_at + m) = make_uint4(w[0], w[1], w[2], w[3]);
+    *reinterpret_cast<uint4*>(at + ko * ld_at + m) = make_uint4(w[0], w[1], w[2], w[3]);
   }
 }
 
@@ -377,7 +382,7 @@ cudaError_t launch_tw_residual(const ResidualArgs& args, cudaStream_t stream) {
 
 cudaError_t launch_transpose_cast(const void* a, int32_t a_dtype, int64_t M, int64_t K,
                                   int64_t lda, void* at, int32_t at_dtype, int64_t ld_at,
-                                  cudaStream_t stream) {
+                                  const int32_t* out_row, cudaStream_t stream) {
   if (M <= 0 || K <= 0) return cudaSuccess;
   const bool fast = a_dtype == at_dtype && a_dtype != kF32 && M % 8 == 0 && K % 8 == 0 &&
                     lda % 8 == 0 && ld_at % 8 == 0 &&
@@ -385,12 +390,13 @@ cudaError_t launch_transpose_cast(const void* a, int32_t a_dtype, int64_t M, int
   if (fast) {
     dim3 grid(static_cast<unsigned>((K + 63) / 64), static_cast<unsigned>((M + 63) / 64));
     transpose16_kernel<<<grid, 256, 0, stream>>>(static_cast<const uint16_t*>(a), M, K, lda,
-                                                  static_cast<uint16_t*>(at), ld_at);
+                                                  static_cast<uint16_t*>(at), ld_at, out_row);
     return cudaGetLastError();
   }
   dim3 grid(static_cast<unsigned>((K + 31) / 32), static_cast<unsigned>((M + 31) / 32));
   dim3 block(32, 8);
-  transpose_cast_kernel<<<grid, block, 0, stream>>>(a, a_dtype, M, K, lda, at, at_dtype, ld_at);
+  transpose_cast_kernel<<<grid, block, 0, stream>>>(a, a_dtype, M, K, lda, at, at_dtype, ld_at,
+                                                     out_row);
   return cudaGetLastError();
 }
 

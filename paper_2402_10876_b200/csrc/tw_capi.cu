@@ -142,8 +142,17 @@ struct tw_plan {
   bool owner = false;                    // n_sub <= SMs: one sub-tile per CTA
   bool resident = false;                 // owner and every payload fits in smem
   std::vector<int32_t> cta_first;        // owner mode: [n_sub + 1]
+  // row-run layout: A^T rows permuted so each tile's kept rows form a few
+  // runs; position p holds original row perm[p] (empty = not used)
+  bool runs = false;
+  std::vector<int32_t> perm, inv;
+  int32_t box_stride = 0;                // stages per tile + 1
   // device
   SubTile* d_subtiles = nullptr;
+  int32_t* d_perm = nullptr;             // [k] position -> original row
+  int32_t* d_inv = nullptr;              // [k] original row -> position
+  int32_t* d_box_first = nullptr;        // [n_tiles][box_stride] first box of every stage
+  uint32_t* d_boxes = nullptr;           // slot | log2(rows) << 6 | position << 9
   int32_t* d_gidx = nullptr;  // [n_tiles][kp] kept rows, -1 padded
   void* d_payload = nullptr;
   CUtensorMap map_pay;
@@ -164,7 +173,8 @@ struct tw_plan {
   std::vector<int32_t> ov_start;       // host copy of the K2 column pointers
 
   ~tw_plan() {
-    for (void* p : {(void*)d_subtiles, (void*)d_gidx, d_payload,
+    for (void* p : {(void*)d_subtiles, (void*)d_gidx, d_payload, (void*)d_perm, (void*)d_inv,
+                    (void*)d_box_first, (void*)d_boxes,
                     (void*)d_union_rowmap, (void*)d_ov_start, (void*)d_ov_rows, (void*)d_ov_vals,
                     (void*)d_ov_out, (void*)d_ov_acc, (void*)d_ov_rv, (void*)d_ov_meta})
       if (p) cudaFree(p);
@@ -175,13 +185,13 @@ extern "C" {
 
 const char* tw_last_error(void) { return g_last_error.c_str(); }
 
-int32_t tw_abi_version(void) { return 300; }
+int32_t tw_abi_version(void) { return 400; }
 
 int tw_plan_create_cto(tw_plan** out, int32_t k, int32_t n, int32_t g, int32_t n_tiles,
                        const uint32_t* row_counts, const uint32_t* col_counts,
                        const uint32_t* row_offsets, int32_t max_rows,
                        const uint32_t* col_offsets, int32_t max_cols, const float* payload,
-                       int32_t compute_dtype, int32_t schedule, void* stream) {
+                       int32_t compute_dtype, int32_t schedule, int32_t row_runs, void* stream) {
   g_last_error.clear();
   if (!out) return fail(TW_ERR_INVALID_INPUT, "out is null");
   *out = nullptr;
@@ -262,6 +272,104 @@ int tw_plan_create_cto(tw_plan** out, int32_t k, int32_t n, int32_t g, int32_t n
   int32_t kp = kBK;
   for (int i = 0; i < n_tiles; ++i) kp = std::max(kp, round_up((int32_t)row_counts[i], kBK));
   plan->kp = kp;
+
+  // Row-run layout.  With few tiles, ordering the rows of A^T by their
+  // tile-membership signature (Gray-code order of the n_tiles-bit set of
+  // tiles that keep the row) turns every tile's kept rows into a handful of
+  // runs of consecutive positions, which dense TMA boxes fetch at the full
+  // TMA rate instead of 16-byte cp.async gathers.  The tiles' K' order
+  // becomes position order (payload columns reordered to match), so the
+  // natural-layout cp.async path and the run path accumulate in the same
+  // order and stay bit-identical.  Enabled when the boxes per 64-row stage
+  // stay few.
+  const float* pay_src = payload;
+  std::vector<float> pay_re;
+  std::vector<int32_t> box_first;
+  std::vector<uint32_t> boxes;
+  if (row_runs && n_tiles <= 6 && k < (1 << 23) && !env_int("TW_NO_RUNS", 0)) {
+    std::vector<int32_t> sig(k, 0);
+    for (int i = 0; i < n_tiles; ++i)
+      for (int32_t r : rows[i]) sig[r] |= 1 << i;
+    std::vector<int32_t> gray_rank(1 << n_tiles);
+    for (int v = 0; v < (1 << n_tiles); ++v) gray_rank[v ^ (v >> 1)] = v;
+    std::vector<int32_t> perm(k), inv(k);
+    std::iota(perm.begin(), perm.end(), 0);
+    std::stable_sort(perm.begin(), perm.end(),
+                     [&](int32_t a, int32_t b) { return gray_rank[sig[a]] < gray_rank[sig[b]]; });
+    for (int32_t p = 0; p < k; ++p) inv[perm[p]] = p;
+    const int stride = kp / kBK + 1;
+    std::vector<std::vector<int32_t>> order(n_tiles);
+    std::vector<int32_t> bf((size_t)n_tiles * stride, 0);
+    std::vector<uint32_t> bx;
+    int64_t stages = 0;
+    for (int i = 0; i < n_tiles; ++i) {
+      const int32_t h = (int32_t)rows[i].size();
+      order[i].resize(h);
+      std::iota(order[i].begin(), order[i].end(), 0);
+      std::stable_sort(order[i].begin(), order[i].end(),
+                       [&](int32_t a, int32_t b) { return inv[rows[i][a]] < inv[rows[i][b]]; });
+      const int nst = round_up(h, kBK) / kBK;
+      for (int st = 0; st < nst; ++st) {
+        bf[(size_t)i * stride + st] = (int32_t)bx.size();
+        // slots [64 st, 64 st + 64): maximal runs of consecutive positions,
+        // then the padding (positions >= k: zero-filled by the TMA); each run
+        // is cut into power-of-two boxes
+        int slot = st * kBK;
+        const int end = st * kBK + kBK;
+        while (slot < end) {
+          int len = 1;
+          int32_t p0 = slot < h ? inv[rows[i][order[i][slot]]] : k;
+          if (slot < h) {
+            while (slot + len < end && slot + len < h &&
+                   inv[rows[i][order[i][slot + len]]] == p0 + len)
+              ++len;
+          } else {
+            len = end - slot;
+          }
+          int done = 0;
+          while (done < len) {
+            int hb = 64;
+            while (hb > len - done) hb >>= 1;
+            int code = 0;
+            while ((1 << code) < hb) ++code;
+            bx.push_back((uint32_t)((slot + done) - st * kBK) | ((uint32_t)code << 6) |
+                         ((uint32_t)(p0 + done) << 9));
+            done += hb;
+          }
+          slot += len;
+        }
+        ++stages;
+      }
+      bf[(size_t)i * stride + nst] = (int32_t)bx.size();
+      for (int st = nst + 1; st < stride; ++st) bf[(size_t)i * stride + st] = (int32_t)bx.size();
+    }
+    const double per_stage = stages ? (double)bx.size() / (double)stages : 1e9;
+    if (per_stage <= 4.0) {
+      plan->runs = true;
+      plan->perm = perm;
+      plan->inv = inv;
+      plan->box_stride = stride;
+      box_first.swap(bf);
+      boxes.swap(bx);
+      // K' order = position order: rows and payload columns follow
+      pay_re.resize(std::max<int64_t>(1, 0));
+      int64_t total = 0;
+      for (int i = 0; i < n_tiles; ++i) total += (int64_t)row_counts[i] * col_counts[i];
+      pay_re.resize(total);
+      int64_t base = 0;
+      for (int i = 0; i < n_tiles; ++i) {
+        const int32_t h = (int32_t)row_counts[i], w = (int32_t)col_counts[i];
+        std::vector<int32_t> r2(h);
+        for (int32_t j = 0; j < h; ++j) r2[j] = rows[i][order[i][j]];
+        rows[i].swap(r2);
+        for (int32_t c = 0; c < w; ++c)
+          for (int32_t j = 0; j < h; ++j)
+            pay_re[base + (int64_t)c * h + j] = payload[base + (int64_t)c * h + order[i][j]];
+        base += (int64_t)h * w;
+      }
+      pay_src = pay_re.data();
+    }
+  }
   std::vector<int32_t> gidx((size_t)n_tiles * kp, -1);
   for (int i = 0; i < n_tiles; ++i)
     std::copy(rows[i].begin(), rows[i].end(), gidx.begin() + (size_t)i * kp);
@@ -349,6 +457,12 @@ int tw_plan_create_cto(tw_plan** out, int32_t k, int32_t n, int32_t g, int32_t n
 
   if (int st = upload(&plan->d_subtiles, plan->subtiles, s)) return st;
   if (int st = upload(&plan->d_gidx, gidx, s)) return st;
+  if (plan->runs) {
+    if (int st = upload(&plan->d_perm, plan->perm, s)) return st;
+    if (int st = upload(&plan->d_inv, plan->inv, s)) return st;
+    if (int st = upload(&plan->d_box_first, box_first, s)) return st;
+    if (int st = upload(&plan->d_boxes, boxes, s)) return st;
+  }
 
   int64_t* d_src_base = nullptr;
   int32_t* d_src_ld = nullptr;
@@ -356,7 +470,7 @@ int tw_plan_create_cto(tw_plan** out, int32_t k, int32_t n, int32_t g, int32_t n
   if (int st = upload(&d_src_base, base2, s)) return st;
   if (int st = upload(&d_src_ld, ld2, s)) return st;
   TW_CUDA(cudaMalloc(&d_src, std::max<int64_t>(pbase, 1) * sizeof(float)));
-  TW_CUDA(cudaMemcpyAsync(d_src, payload, pbase * sizeof(float), cudaMemcpyHostToDevice, s));
+  TW_CUDA(cudaMemcpyAsync(d_src, pay_src, pbase * sizeof(float), cudaMemcpyHostToDevice, s));
   const size_t pay_bytes = (size_t)plan->n_sub * bn * kp * 2;
   TW_CUDA(cudaMalloc(&plan->d_payload, pay_bytes));
   PayloadArgs pa{d_src, d_src_base, d_src_ld, plan->d_subtiles, plan->d_payload,
@@ -496,6 +610,7 @@ int tw_plan_get_info(const tw_plan* p, tw_plan_info* info) {
   info->kept_macs_per_token = p->kept_macs + p->nnz;
   info->sm_count = p->sm_count;
   info->has_overlay = p->has_overlay ? 1 : 0;
+  info->row_runs = p->runs ? 1 : 0;
   return TW_OK;
 }
 
@@ -532,7 +647,7 @@ static int check_io(const tw_plan* p, const void* x, int64_t m, int64_t ld_x, co
 
 static int run_tw(const tw_plan* p, const void* x, int64_t m, int64_t ld_x, void* ct,
                   int64_t ld_ct, int32_t out_dtype, const int32_t* rowmap, int64_t out_rows,
-                  cudaStream_t s) {
+                  cudaStream_t s, bool plan_layout = false) {
   GemmArgs a{};
   a.subtiles = p->d_subtiles;
   a.x = x;
@@ -618,7 +733,21 @@ static int run_tw(const tw_plan* p, const void* x, int64_t m, int64_t ld_x, void
     grid = std::min(a.n_units, p->sm_count);
   }
   const bool resident = a.owner && p->resident;
-  TW_CUDA(launch_tw_gemm(p->map_pay, map_out, a, work, resident, grid, s));
+  // row-run path: x is in the plan's permuted row layout
+  RunMaps run_maps;
+  std::memset(&run_maps, 0, sizeof(run_maps));
+  a.runs = 0;
+  if (plan_layout && p->runs) {
+    a.runs = 1;
+    a.box_first = p->d_box_first;
+    a.boxes = p->d_boxes;
+    a.box_stride = p->box_stride;
+    for (int c = 0; c < kRunMaps && a.runs; ++c)
+      if (make_map_2d(&run_maps.m[c], x, p->dtype, (uint64_t)m, (uint64_t)p->k, (uint64_t)ld_x,
+                      64, 1u << c, 128) != TW_OK)
+        return TW_ERR_INVALID_INPUT;
+  }
+  TW_CUDA(launch_tw_gemm(p->map_pay, map_out, run_maps, a, work, resident, grid, s));
   return TW_OK;
 }
 
@@ -628,6 +757,33 @@ int tw_gemm(const tw_plan* p, const void* x, int64_t m, int64_t ld_x, void* ct, 
   if (int st = check_io(p, x, m, ld_x, ct, ld_ct, out_dtype)) return st;
   return run_tw(p, x, m, ld_x, ct, ld_ct, out_dtype, nullptr, p->n_cond,
                 static_cast<cudaStream_t>(stream));
+}
+
+int tw_gemm_ex(const tw_plan* p, const void* x, int64_t m, int64_t ld_x, void* ct, int64_t ld_ct,
+               int32_t out_dtype, int32_t x_layout, void* stream) {
+  g_last_error.clear();
+  if (int st = check_io(p, x, m, ld_x, ct, ld_ct, out_dtype)) return st;
+  if (x_layout != TW_LAYOUT_NATURAL && x_layout != TW_LAYOUT_PLAN)
+    return fail(TW_ERR_INVALID_INPUT, "unknown activation layout %d", x_layout);
+  return run_tw(p, x, m, ld_x, ct, ld_ct, out_dtype, nullptr, p->n_cond,
+                static_cast<cudaStream_t>(stream), x_layout == TW_LAYOUT_PLAN);
+}
+
+int tw_plan_prepare(const tw_plan* p, const void* a, int32_t a_dtype, int64_t m, int64_t lda,
+                    void* at, int64_t ld_at, void* stream) {
+  g_last_error.clear();
+  if (!p || !a || !at) return fail(TW_ERR_INVALID_INPUT, "null argument");
+  if (m < 1 || lda < p->k || ld_at < m) return fail(TW_ERR_INVALID_INPUT, "bad prepare geometry");
+  if (int st = check_dtype(a_dtype)) return st;
+  TW_CUDA(launch_transpose_cast(a, a_dtype, m, p->k, lda, at, p->dtype, ld_at,
+                                p->runs ? p->d_inv : nullptr, static_cast<cudaStream_t>(stream)));
+  return TW_OK;
+}
+
+int tw_plan_row_order(const tw_plan* p, int32_t* out_rows) {
+  if (!p || !out_rows) return fail(TW_ERR_INVALID_INPUT, "null argument");
+  for (int32_t i = 0; i < p->k; ++i) out_rows[i] = p->runs ? p->perm[i] : i;
+  return TW_OK;
 }
 
 int tw_gemm_tew(const tw_plan* p, const void* x, int64_t m, int64_t ld_x, void* ct,
@@ -705,7 +861,7 @@ int tw_transpose_cast(const void* a, int32_t a_dtype, int64_t m, int64_t k, int6
     return fail(TW_ERR_INVALID_INPUT, "bad transpose geometry");
   if (int st = check_dtype(a_dtype)) return st;
   if (int st = check_dtype(at_dtype)) return st;
-  TW_CUDA(launch_transpose_cast(a, a_dtype, m, k, lda, at, at_dtype, ld_at,
+  TW_CUDA(launch_transpose_cast(a, a_dtype, m, k, lda, at, at_dtype, ld_at, nullptr,
                                 static_cast<cudaStream_t>(stream)));
   return TW_OK;
 }

@@ -251,7 +251,8 @@ __device__ __forceinline__ void epilogue_rows(const GemmArgs& args, const CUtens
 template <bool kRes>
 __global__ void __launch_bounds__(kThreads, 1)
     tw_gemm_kernel(const __grid_constant__ CUtensorMap map_pay,
-                   const __grid_constant__ CUtensorMap map_out, const __grid_constant__ GemmArgs args,
+                   const __grid_constant__ CUtensorMap map_out,
+                   const __grid_constant__ RunMaps run_maps, const __grid_constant__ GemmArgs args,
                    const __grid_constant__ WorkTable work) {
   using C = Cfg<kRes>;
   constexpr int kStages = C::kStages;
@@ -291,7 +292,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int s = 0; s < kStages; ++s) {
       // streamed: payload TMA (expect_tx arrival); both: one cp.async
       // arrival per gather thread
-      mbar_init(&full[s], (kRes ? 0 : 1) + kGatherThreads);
+      // streamed: payload TMA (expect_tx arrival); cp.async path: one
+      // arrival per gather thread; run path: the box issuer's one arrival
+      mbar_init(&full[s], args.runs ? 1 : (kRes ? 0 : 1) + kGatherThreads);
       mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
@@ -306,6 +309,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     tma_prefetch_desc(&map_pay);
     if (args.use_tma_store) tma_prefetch_desc(&map_out);
   }
+  if (args.runs && warp == kPayloadWarp && lane < kRunMaps) tma_prefetch_desc(&run_maps.m[lane]);
   if (warp == kMmaWarp) {
     tmem_alloc(tmem_slot, kTmemCols);
     tmem_relinquish();
@@ -326,32 +330,70 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == kPayloadWarp) {
     // ---------------------------------------------------- payload producer
-    if (lane == 0) {
-      if (kRes) {
-        // the owned sub-tile's whole payload, once, paced with the first
-        // unit's activation stages (k-step ks is requested when stage ks may
-        // be filled) so the first stages are not queued behind all of it
-        if (walk.next(args, sg)) {
-          for (int ks = 0; ks < sg.d.kp_steps; ++ks) {
-            mbar_wait(&empty[ks % kStages], ((ks / kStages) & 1) ^ 1u);
-            mbar_arrive_expect_tx(&pfull[ks], kPBytes);
-            tma_load_2d(sP + ks * kPBytes, &map_pay, &pfull[ks], ks * kBK, sg.d.pay_row);
-          }
-        }
-      } else {
-        int gs = 0;
-        while (walk.next(args, sg)) {
-          for (int ks = 0; ks < sg.d.kp_steps; ++ks, ++gs) {
-            const int stage = gs % kStages;
-            mbar_wait(&empty[stage], ((gs / kStages) & 1) ^ 1u);
-            if (trace && gs < 1024) trace[gs] = clock64();
-            mbar_arrive_expect_tx(&full[stage], kPBytes);
-            tma_load_2d(sP + stage * kPBytes, &map_pay, &full[stage], ks * kBK, sg.d.pay_row);
-          }
+    if (kRes && lane == 0) {
+      // the owned sub-tile's whole payload, once, paced with the first
+      // unit's activation stages (k-step ks is requested when stage ks may
+      // be filled) so the first stages are not queued behind all of it; on
+      // the run path this warp also fills the stages, so no pacing
+      Walker w0 = walk;
+      Seg s0;
+      if (w0.next(args, s0)) {
+        for (int ks = 0; ks < s0.d.kp_steps; ++ks) {
+          if (!args.runs) mbar_wait(&empty[ks % kStages], ((ks / kStages) & 1) ^ 1u);
+          mbar_arrive_expect_tx(&pfull[ks], kPBytes);
+          tma_load_2d(sP + ks * kPBytes, &map_pay, &pfull[ks], ks * kBK, s0.d.pay_row);
         }
       }
     }
-  } else if (warp >= kGatherWarp0 && warp < kEpilogueWarp0) {
+    if (args.runs) {
+      // Run path: each stage is a few dense TMA boxes of consecutive A^T
+      // rows (plan row layout) x 64 tokens, one box per lane; lane 0 also
+      // streams the payload slice (streamed kernel).
+      grid_dependency_wait();  // A^T may be written by the previous kernel
+      int gs = 0;
+      while (walk.next(args, sg)) {
+        const int n = (sg.ue - sg.ub + 15) & ~15;
+        const int chunks = (n + 63) >> 6;
+        const int32_t* bf = args.box_first + static_cast<int64_t>(sg.d.idx_row) * args.box_stride;
+        int b0 = __ldg(bf), b1 = __ldg(bf + 1);
+        for (int ks = 0; ks < sg.d.kp_steps; ++ks, ++gs) {
+          const int stage = gs % kStages;
+          const int nb0 = ks + 1 < sg.d.kp_steps ? __ldg(bf + ks + 1) : 0;
+          const int nb1 = ks + 1 < sg.d.kp_steps ? __ldg(bf + ks + 2) : 0;
+          const uint32_t e = b0 + lane < b1 ? __ldg(args.boxes + b0 + lane) : 0u;
+          mbar_wait(&empty[stage], ((gs / kStages) & 1) ^ 1u);
+          if (lane == 0) {
+            mbar_arrive_expect_tx(&full[stage], (kRes ? 0u : static_cast<uint32_t>(kPBytes)) +
+                                                    static_cast<uint32_t>(chunks * kBK * 128));
+            if (!kRes)
+              tma_load_2d(sP + stage * kPBytes, &map_pay, &full[stage], ks * kBK, sg.d.pay_row);
+          }
+          __syncwarp();
+          for (int j = b0 + lane, jj = 0; j < b1; j += 32, jj += 32) {
+            const uint32_t ej = jj == 0 ? e : __ldg(args.boxes + j);
+            const int slot = static_cast<int>(ej & 63u), code = static_cast<int>((ej >> 6) & 7u);
+            const int32_t pos = static_cast<int32_t>(ej >> 9);
+            uint8_t* dst = sX + stage * kXBytes + slot * 128;
+            for (int c = 0; c < chunks; ++c)
+              tma_load_2d(dst + c * kChunkBytes, &run_maps.m[code], &full[stage], sg.ub + c * 64, pos);
+          }
+          b0 = nb0;
+          b1 = nb1;
+        }
+      }
+    } else if (!kRes && lane == 0) {
+      int gs = 0;
+      while (walk.next(args, sg)) {
+        for (int ks = 0; ks < sg.d.kp_steps; ++ks, ++gs) {
+          const int stage = gs % kStages;
+          mbar_wait(&empty[stage], ((gs / kStages) & 1) ^ 1u);
+          if (trace && gs < 1024) trace[gs] = clock64();
+          mbar_arrive_expect_tx(&full[stage], kPBytes);
+          tma_load_2d(sP + stage * kPBytes, &map_pay, &full[stage], ks * kBK, sg.d.pay_row);
+        }
+      }
+    }
+  } else if (warp >= kGatherWarp0 && warp < kEpilogueWarp0 && !args.runs) {
     // ----------------------------------------------------- gather producers
     // A stage is kBK kept rows x n tokens = kBK * n / 8 16-byte items; item i
     // is row i / cpr, 16-byte chunk i % cpr (cpr = n / 8), so every lane is
@@ -458,7 +500,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(&full[stage], (gs / kStages) & 1);
           if (trace && gs < 1024) trace[1024 + gs] = clock64();
           tc_fence_after();
-          fence_proxy_async_smem();  // cp.async (generic proxy) writes -> tcgen05 reads
+          if (!args.runs) fence_proxy_async_smem();  // cp.async (generic proxy) writes -> tcgen05 reads
           const uint32_t p0 = smem_u32(sP + (kRes ? ks : stage) * kPBytes);
           const uint32_t x0 = smem_u32(sX + stage * kXBytes);
           if (!(flags & kFlagSkipMma)) {
@@ -539,8 +581,8 @@ cudaError_t configure_gemm_kernels() {
 }
 
 cudaError_t launch_tw_gemm(const CUtensorMap& map_pay, const CUtensorMap& map_out,
-                           const GemmArgs& args, const WorkTable& work, bool resident, int grid,
-                           cudaStream_t stream) {
+                           const RunMaps& run_maps, const GemmArgs& args, const WorkTable& work,
+                           bool resident, int grid, cudaStream_t stream) {
   if (grid <= 0) return cudaSuccess;
   if (resident && !args.owner) return cudaErrorInvalidValue;
   if (args.owner && grid > kMaxCtas) return cudaErrorInvalidValue;
@@ -555,8 +597,8 @@ cudaError_t launch_tw_gemm(const CUtensorMap& map_pay, const CUtensorMap& map_ou
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   if (resident)
-    return cudaLaunchKernelEx(&cfg, tw_gemm_kernel<true>, map_pay, map_out, args, work);
-  return cudaLaunchKernelEx(&cfg, tw_gemm_kernel<false>, map_pay, map_out, args, work);
+    return cudaLaunchKernelEx(&cfg, tw_gemm_kernel<true>, map_pay, map_out, run_maps, args, work);
+  return cudaLaunchKernelEx(&cfg, tw_gemm_kernel<false>, map_pay, map_out, run_maps, args, work);
 }
 
 }  // namespace tw

@@ -63,6 +63,19 @@ struct GemmArgs {
   int32_t vec_ok;           // output rows 16-byte aligned: vector stores allowed
   int32_t use_tma_store;    // map_out valid (16-bit output): 32 x 16 blocks via TMA stores
   long long* trace;         // optional per-CTA clock64 trace (4096 entries per CTA)
+  // row-run path (x in the plan's permuted row layout): activation stages are
+  // dense TMA boxes listed per (tile, stage) instead of cp.async gathers
+  int32_t runs;
+  const int32_t* box_first; // [n_tiles][box_stride]
+  const uint32_t* boxes;    // slot | log2(rows) << 6 | position << 9
+  int32_t box_stride;
+};
+
+// Tensor maps over the permuted A^T for box heights 1, 2, 4, ..., 64 rows
+// (64 tokens wide, 128-byte swizzle).
+constexpr int kRunMaps = 7;
+struct RunMaps {
+  CUtensorMap m[kRunMaps];
 };
 
 // Diagnostic switches (profiling only; results are wrong when set).
@@ -75,8 +88,8 @@ constexpr int32_t kFlagSkipMma = 4;     // do not issue tcgen05.mma
 //   map_out : C'^T (16-bit), box {16 tokens, 32 rows}, 32-B swizzle
 //   resident: payload held in shared memory (owner mode, kp_steps <= kResSteps)
 cudaError_t launch_tw_gemm(const CUtensorMap& map_pay, const CUtensorMap& map_out,
-                           const GemmArgs& args, const WorkTable& work, bool resident, int grid,
-                           cudaStream_t stream);
+                           const RunMaps& run_maps, const GemmArgs& args, const WorkTable& work,
+                           bool resident, int grid, cudaStream_t stream);
 
 // Raise the dynamic shared-memory limit of every K1 instance (call once per
 // device before launching or capturing).
@@ -112,9 +125,10 @@ cudaError_t launch_tw_residual(const ResidualArgs& args, cudaStream_t stream);
 int residual_block_tokens(int32_t K, int* ctas_per_sm);
 
 // K4: A (M x K, row-major, lda) -> A^T (K x M, ld_at) with a dtype cast.
+// out_row (optional, [K]): A column k lands in A^T row out_row[k] (plan row layout).
 cudaError_t launch_transpose_cast(const void* a, int32_t a_dtype, int64_t M, int64_t K,
                                   int64_t lda, void* at, int32_t at_dtype, int64_t ld_at,
-                                  cudaStream_t stream);
+                                  const int32_t* out_row, cudaStream_t stream);
 
 // Payload build: packed transposed fp32 CTO payload -> padded [n_sub*kBN][Kp] fp16/bf16
 // (kept-row order, as formats.py:200 stores it).

@@ -76,11 +76,15 @@ class TwPlan:
     """
 
     def __init__(self, enc: CtoEncoding, overlay: Optional[SparseOverlay] = None,
-                 compute_dtype: str = "fp16", schedule: str = "lpt"):
+                 compute_dtype: str = "fp16", schedule: str = "lpt",
+                 row_layout: str = "natural"):
         torch = _torch()
         lib = _native.load_library()
         if schedule not in _native.SCHEDULES:
             raise InvalidInputError(f"unknown strategy {schedule!r}")
+        if row_layout not in ("natural", "runs"):
+            raise InvalidInputError(f"row_layout must be 'natural' or 'runs', got {row_layout!r}")
+        self.row_layout = row_layout
         self.compute_dtype = _dtype_name(compute_dtype)
         if self.compute_dtype == "fp32":
             raise InvalidInputError("compute_dtype must be fp16 or bf16 (tensor-core inputs)")
@@ -100,7 +104,8 @@ class TwPlan:
             _native.ptr(ro, _native.ctypes.c_uint32), ro.shape[1],
             _native.ptr(co, _native.ctypes.c_uint32), co.shape[1],
             _native.ptr(pl, _native.ctypes.c_float), _DTYPE_CODES[self.compute_dtype],
-            _native.SCHEDULES[schedule], _native.stream_handle()))
+            _native.SCHEDULES[schedule], 1 if row_layout == "runs" else 0,
+            _native.stream_handle()))
         self._handle = handle
         self._finalizer = weakref.finalize(self, lib.tw_plan_destroy, handle)
         self.per_tile_kept = [int(h) for h in rc]
@@ -111,13 +116,14 @@ class TwPlan:
 
     @classmethod
     def from_cto1(cls, path, overlay: Optional[SparseOverlay] = None,
-                  compute_dtype: str = "fp16", schedule: str = "lpt") -> "TwPlan":
+                  compute_dtype: str = "fp16", schedule: str = "lpt",
+                  row_layout: str = "natural") -> "TwPlan":
         """Device plan straight from a CTO1 artifact: the file
         is read and validated like reference read_cto1 (formats.py:259-304)
         and the GPU weight format is built from it without re-pruning."""
         from .formats import read_cto1
 
-        return cls(read_cto1(path), overlay, compute_dtype, schedule)
+        return cls(read_cto1(path), overlay, compute_dtype, schedule, row_layout)
 
     # -- metadata -------------------------------------------------------
     def _refresh_info(self) -> None:
@@ -133,6 +139,17 @@ class TwPlan:
                                                 _native.ptr(uni, _native.ctypes.c_int32)))
         self.condensed_columns = cond.astype(np.int64)
         self.union_columns = uni.astype(np.int64)
+        order = np.empty(info.k, dtype=np.int32)
+        _native.check(lib.tw_plan_row_order(self._handle, _native.ptr(order, _native.ctypes.c_int32)))
+        self.row_order = order.astype(np.int64)  # position -> original K row
+        self._row_order_dev = None
+
+    @property
+    def uses_row_runs(self) -> bool:
+        """True when run()'s input is in this plan's permuted row layout
+        (row_layout='runs', the library found few-run row orders, no overlay)."""
+        return (self.row_layout == "runs" and bool(self.info.row_runs)
+                and not bool(self.info.has_overlay))
 
     @property
     def has_overlay(self) -> bool:
@@ -162,16 +179,18 @@ class TwPlan:
         return 2 * int(m) * int(macs)
 
     # -- activations ------------------------------------------------------
-    def prepare(self, a=None, *, at=None, stream=None):
+    def prepare(self, a=None, *, at=None, stream=None, out=None):
         """Activations -> the A^T operand of :meth:`run` (K x M, compute dtype).
 
         ``a`` is the reference-layout activation matrix (M x K: numpy, nested
-        list, CPU or CUDA tensor), transposed and cast on the GPU (K4);
-        alternatively ``at`` is a CUDA A^T (K x M), returned as is when it is
-        already in the compute dtype with unit token stride, a token pitch
-        that is a multiple of 8 and a 16-byte aligned base (the layout
-        :meth:`run` writes, so one layer's output feeds the next), else
-        copied into that layout.
+        list, CPU or CUDA tensor), transposed and cast on the GPU (K4) -- into
+        the plan's permuted row order when :attr:`uses_row_runs`.
+        Alternatively ``at`` is a CUDA A^T (K x M) in the original row order,
+        returned as is when it already is the operand (compute dtype, unit
+        token stride, token pitch a multiple of 8, 16-byte aligned base: the
+        layout :meth:`run` writes, so one layer's output feeds the next), else
+        copied (and row-permuted) into it.  ``out`` (with ``a``): a K x M
+        CUDA view to write into.
         """
         torch = _torch()
         k = self.original_dims[0]
@@ -182,19 +201,50 @@ class TwPlan:
             if len(m_k) != 2 or m_k[1] != k:
                 raise InvalidInputError(
                     f"inner dims disagree: a has {m_k[-1]} cols, weights have K={k}")
-            return prepare_activations(a, self.compute_dtype, stream=stream)
+            if not self.uses_row_runs:
+                return prepare_activations(a, self.compute_dtype, stream=stream, out=out)
+            return self._prepare_runs(a, stream, out)
         if not isinstance(at, torch.Tensor) or not at.is_cuda or at.dim() != 2:
             raise InvalidInputError("at must be a 2-D CUDA tensor (K x M)")
         if at.shape[0] != k:
             raise InvalidInputError(f"inner dims disagree: at has {at.shape[0]} rows, "
                                     f"weights have K={k}")
+        if self.uses_row_runs:
+            if self._row_order_dev is None:
+                self._row_order_dev = torch.tensor(self.row_order, device=at.device)
+            at = at.index_select(0, self._row_order_dev)
         if _at_ready(at, self.compute_dtype):
             return at
         m = int(at.shape[1])
         ld = (m + 7) // 8 * 8
-        out = torch.zeros((k, ld), dtype=_torch_dtype(self.compute_dtype), device=at.device)
-        out[:, :m].copy_(at)
-        return out[:, :m]
+        buf = torch.zeros((k, ld), dtype=_torch_dtype(self.compute_dtype), device=at.device)
+        buf[:, :m].copy_(at)
+        return buf[:, :m]
+
+    def _prepare_runs(self, a, stream, out):
+        torch = _torch()
+        k = self.original_dims[0]
+        if isinstance(a, torch.Tensor):
+            src = a if a.is_cuda else a.cuda(non_blocking=True)
+            if src.dtype not in (torch.float32, torch.float16, torch.bfloat16):
+                src = src.float()
+            if src.stride(1) != 1:
+                src = src.contiguous()
+        else:
+            src = torch.from_numpy(as_matrix(a)).cuda()
+        m = int(src.shape[0])
+        if out is not None:
+            if tuple(out.shape) != (k, m) or not _at_ready(out, self.compute_dtype):
+                raise InvalidInputError("out must be a K x M A^T view in the compute dtype")
+            at, ld = out, (out.stride(0) if k > 1 else (m + 7) // 8 * 8)
+        else:
+            ld = (m + 7) // 8 * 8
+            at = torch.empty((k, ld), dtype=_torch_dtype(self.compute_dtype), device=src.device)
+        lib = _native.load_library()
+        _native.check(lib.tw_plan_prepare(self._handle, src.data_ptr(),
+                                          _DTYPE_CODES[_dtype_name(src.dtype)], m, src.stride(0),
+                                          at.data_ptr(), ld, _native.stream_handle(stream)))
+        return at if out is not None else at[:, :m]
 
     # -- launches -------------------------------------------------------
     def _check_x(self, x):
@@ -222,14 +272,21 @@ class TwPlan:
             raise InvalidInputError("out must be a (rows x M) CUDA tensor with unit token stride")
         return out
 
-    def run(self, x, out=None, out_dtype="fp32", stream=None):
-        """C'^T (N' x M) = TW product of x = A^T (K x M); K1 only."""
+    def run(self, x, out=None, out_dtype="fp32", stream=None, x_layout=None):
+        """C'^T (N' x M) = TW product of x = A^T (K x M); K1 only.  x is in
+        the plan's row layout: the original order for row_layout='natural',
+        the permuted order :meth:`prepare` writes for row_layout='runs'
+        (``x_layout='natural'`` overrides: original-order rows, gathered)."""
         m, ld = self._check_x(x)
         ct = self._out(self.info.n_condensed, m, out, out_dtype)
         lib = _native.load_library()
-        _native.check(lib.tw_gemm(self._handle, x.data_ptr(), m, ld, ct.data_ptr(),
-                                  ct.stride(0), _DTYPE_CODES[_dtype_name(ct.dtype)],
-                                  _native.stream_handle(stream)))
+        if x_layout not in (None, "natural", "plan"):
+            raise InvalidInputError(f"unknown x_layout {x_layout!r}")
+        use_plan = self.uses_row_runs if x_layout is None else x_layout == "plan"
+        layout = _native.TW_LAYOUT_PLAN if use_plan else _native.TW_LAYOUT_NATURAL
+        _native.check(lib.tw_gemm_ex(self._handle, x.data_ptr(), m, ld, ct.data_ptr(),
+                                     ct.stride(0), _DTYPE_CODES[_dtype_name(ct.dtype)], layout,
+                                     _native.stream_handle(stream)))
         return ct
 
     def run_tew(self, x, out=None, out_dtype="fp32", stream=None):
@@ -305,7 +362,8 @@ _PLAN_CACHE: dict = {}
 
 
 def plan_for(b: Union[TileSparseMatrix, CtoEncoding], overlay: Optional[SparseOverlay] = None,
-             compute_dtype: str = "fp16", schedule: str = "lpt") -> TwPlan:
+             compute_dtype: str = "fp16", schedule: str = "lpt",
+             row_layout: str = "runs") -> TwPlan:
     """Cached :class:`TwPlan` for a tile matrix / encoding (+ overlay).
 
     The reference structures are frozen, so a plan is keyed by the identity
@@ -313,11 +371,12 @@ def plan_for(b: Union[TileSparseMatrix, CtoEncoding], overlay: Optional[SparseOv
     """
     torch = _torch()
     watched = [b] if overlay is None else [b, overlay]
-    key = tuple(id(o) for o in watched) + (torch.cuda.current_device(), compute_dtype, schedule)
+    key = tuple(id(o) for o in watched) + (torch.cuda.current_device(), compute_dtype, schedule,
+                                          row_layout)
     plan = _PLAN_CACHE.get(key)
     if plan is None:
         enc = b if isinstance(b, CtoEncoding) else encode_cto(b)
-        plan = TwPlan(enc, overlay, compute_dtype, schedule)
+        plan = TwPlan(enc, overlay, compute_dtype, schedule, row_layout)
         _PLAN_CACHE[key] = plan
         for o in watched:
             weakref.finalize(o, _PLAN_CACHE.pop, key, None)

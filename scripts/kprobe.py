@@ -71,7 +71,7 @@ def main():
                 pl.run = pl.run_tew
         else:
             _, tsm = tw.prune_tw(w, 0.75, args.g)
-            plans = [tw.TwPlan(tw.encode_cto(tsm)) for _ in range(4)]
+            plans = [tw.TwPlan(tw.encode_cto(tsm), row_layout=os.environ.get('TW_ROW_LAYOUT', 'runs')) for _ in range(4)]
         a = tw.round_to(tw.synthetic_matrix(0, args.m, k, 1), "fp16")
         ats = [pl.prepare(torch.from_numpy(a).cuda()) for pl in plans]
         if args.pad:

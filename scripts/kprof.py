@@ -34,7 +34,7 @@ def main():
     for k, n in LAYERS:
         w = tw.round_to(tw.synthetic_matrix(0, k, n, 0), "fp16")
         _, tsm = tw.prune_tw(w, 0.75, args.g)
-        plans.append([tw.TwPlan(tw.encode_cto(tsm)) for _ in range(4)])
+        plans.append([tw.TwPlan(tw.encode_cto(tsm), row_layout=os.environ.get('TW_ROW_LAYOUT', 'runs')) for _ in range(4)])
         a = tw.round_to(tw.synthetic_matrix(0, args.m, k, 1), "fp16")
         ats.append([pl.prepare(torch.from_numpy(a).cuda()) for pl in plans[-1]])
         outs.append([torch.empty((tsm.n_condensed, args.m), dtype=torch.float16, device="cuda")

@@ -29,7 +29,7 @@ def main():
     k, n = LAYERS[args.layer]
     w = tw.round_to(tw.synthetic_matrix(0, k, n, 0), "fp16")
     _, tsm = tw.prune_tw(w, 0.75, 128)
-    plan = tw.TwPlan(tw.encode_cto(tsm))
+    plan = tw.TwPlan(tw.encode_cto(tsm), row_layout=os.environ.get('TW_ROW_LAYOUT', 'runs'))
     a = tw.round_to(tw.synthetic_matrix(0, args.m, k, 1), "fp16")
     at = plan.prepare(torch.from_numpy(a).cuda())
     out = torch.empty((tsm.n_condensed, args.m), dtype=torch.float16, device="cuda")
