@@ -77,6 +77,8 @@ typedef struct tw_plan_info {
   int32_t has_overlay;
   int32_t row_runs;           /* 1: the plan has a permuted row layout in
                                  which every tile's kept rows form runs     */
+  int32_t row_copies;         /* rows of the plan layout = row_copies * k
+                                 (one row order per group of tiles)         */
 } tw_plan_info;
 
 /* Build a device plan from a CTO encoding held in host memory.
@@ -129,14 +131,14 @@ TW_API int tw_gemm_ex(const tw_plan* plan, const void* at, int64_t m, int64_t ld
                       int64_t ld_ct, int32_t out_dtype, int32_t at_layout, void* stream);
 
 /* A (m x k row-major, pitch lda, any dtype) -> A^T in the plan's row layout and
- * compute dtype (k x m, pitch ld_at): tw_transpose_cast plus the plan's row
- * permutation.  Replaces the as_matrix / astype copies (core.py:32-43,
+ * compute dtype (row_copies * k rows x m, pitch ld_at): tw_transpose_cast plus
+ * the plan's row permutation(s).  Replaces the as_matrix / astype copies (core.py:32-43,
  * executor.py:158) for inputs of this plan. */
 TW_API int tw_plan_prepare(const tw_plan* plan, const void* a, int32_t a_dtype, int64_t m,
                            int64_t lda, void* at, int64_t ld_at, void* stream);
 
 /* Original K row held at each position of the plan's row layout (host buffer
- * of k entries; the identity when row_runs == 0). */
+ * of row_copies * k entries; the identity when row_runs == 0). */
 TW_API int tw_plan_row_order(const tw_plan* plan, int32_t* out_rows);
 
 /* TEW product over the union columns: ct[|union| x M].

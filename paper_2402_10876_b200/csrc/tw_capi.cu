@@ -145,7 +145,8 @@ struct tw_plan {
   // row-run layout: A^T rows permuted so each tile's kept rows form a few
   // runs; position p holds original row perm[p] (empty = not used)
   bool runs = false;
-  std::vector<int32_t> perm, inv;
+  int32_t row_copies = 1;                // G copies of A^T (one per tile group)
+  std::vector<int32_t> perm, inv;        // [G * k]: position -> row, copy g: row -> position
   int32_t box_stride = 0;                // stages per tile + 1
   // device
   SubTile* d_subtiles = nullptr;
@@ -273,89 +274,110 @@ int tw_plan_create_cto(tw_plan** out, int32_t k, int32_t n, int32_t g, int32_t n
   for (int i = 0; i < n_tiles; ++i) kp = std::max(kp, round_up((int32_t)row_counts[i], kBK));
   plan->kp = kp;
 
-  // Row-run layout.  With few tiles, ordering the rows of A^T by their
-  // tile-membership signature (Gray-code order of the n_tiles-bit set of
-  // tiles that keep the row) turns every tile's kept rows into a handful of
-  // runs of consecutive positions, which dense TMA boxes fetch at the full
-  // TMA rate instead of 16-byte cp.async gathers.  The tiles' K' order
-  // becomes position order (payload columns reordered to match), so the
-  // natural-layout cp.async path and the run path accumulate in the same
-  // order and stay bit-identical.  Enabled when the boxes per 64-row stage
-  // stay few.
+  // Row-run layout.  Ordering the rows of A^T by their tile-membership
+  // signature (Gray-code order of the set of tiles that keep the row) turns
+  // every tile's kept rows into a handful of runs of consecutive positions,
+  // which dense TMA boxes fetch at the full TMA rate instead of 16-byte
+  // cp.async gathers.  That works for up to ~6 tiles; layers with more tiles
+  // split them into G <= 4 contiguous groups, each with its own row order and
+  // its own copy of A^T (the plan layout is then G x K rows).  The tiles' K'
+  // order becomes position order (payload columns reordered to match), so
+  // the natural-layout cp.async path and the run path accumulate in the same
+  // order and stay bit-identical.  Used when the boxes per 64-row stage stay
+  // few.
   const float* pay_src = payload;
   std::vector<float> pay_re;
   std::vector<int32_t> box_first;
   std::vector<uint32_t> boxes;
-  if (row_runs && n_tiles <= 6 && k < (1 << 23) && !env_int("TW_NO_RUNS", 0)) {
-    std::vector<int32_t> sig(k, 0);
-    for (int i = 0; i < n_tiles; ++i)
-      for (int32_t r : rows[i]) sig[r] |= 1 << i;
-    std::vector<int32_t> gray_rank(1 << n_tiles);
-    for (int v = 0; v < (1 << n_tiles); ++v) gray_rank[v ^ (v >> 1)] = v;
-    std::vector<int32_t> perm(k), inv(k);
-    std::iota(perm.begin(), perm.end(), 0);
-    std::stable_sort(perm.begin(), perm.end(),
-                     [&](int32_t a, int32_t b) { return gray_rank[sig[a]] < gray_rank[sig[b]]; });
-    for (int32_t p = 0; p < k; ++p) inv[perm[p]] = p;
+  std::vector<double> tile_cost(n_tiles, 0.0);  // owner split weight (run path)
+  // More than one copy (layers with > 6 tiles) measured no faster than the
+  // gather on BERT 768x3072 (G = 3: 21.0 vs 20.9 us), so it is opt-in.
+  const int max_copies = std::max(1, std::min(4, env_int("TW_RUN_COPIES", 1)));
+  if (row_runs && k < (1 << 20) && !env_int("TW_NO_RUNS", 0)) {
     const int stride = kp / kBK + 1;
-    std::vector<std::vector<int32_t>> order(n_tiles);
-    std::vector<int32_t> bf((size_t)n_tiles * stride, 0);
-    std::vector<uint32_t> bx;
-    int64_t stages = 0;
-    for (int i = 0; i < n_tiles; ++i) {
-      const int32_t h = (int32_t)rows[i].size();
-      order[i].resize(h);
-      std::iota(order[i].begin(), order[i].end(), 0);
-      std::stable_sort(order[i].begin(), order[i].end(),
-                       [&](int32_t a, int32_t b) { return inv[rows[i][a]] < inv[rows[i][b]]; });
-      const int nst = round_up(h, kBK) / kBK;
-      for (int st = 0; st < nst; ++st) {
-        bf[(size_t)i * stride + st] = (int32_t)bx.size();
-        // slots [64 st, 64 st + 64): maximal runs of consecutive positions,
-        // then the padding (positions >= k: zero-filled by the TMA); each run
-        // is cut into power-of-two boxes
-        int slot = st * kBK;
-        const int end = st * kBK + kBK;
-        while (slot < end) {
-          int len = 1;
-          int32_t p0 = slot < h ? inv[rows[i][order[i][slot]]] : k;
-          if (slot < h) {
-            while (slot + len < end && slot + len < h &&
-                   inv[rows[i][order[i][slot + len]]] == p0 + len)
-              ++len;
-          } else {
-            len = end - slot;
+    for (int G = (n_tiles + 5) / 6; G <= max_copies && G <= n_tiles; ++G) {
+      const int per = (n_tiles + G - 1) / G;  // tiles per group
+      if ((int64_t)G * k >= (1 << 23)) break;
+      std::vector<int32_t> perm((size_t)G * k), inv((size_t)G * k);
+      std::vector<std::vector<int32_t>> order(n_tiles);
+      std::vector<int32_t> bf((size_t)n_tiles * stride, 0);
+      std::vector<uint32_t> bx;
+      std::vector<double> cost(n_tiles, 0.0);
+      int64_t stages = 0;
+      for (int gi = 0; gi < G; ++gi) {
+        const int t0 = gi * per, t1 = std::min(n_tiles, t0 + per);
+        const int nt = t1 - t0;
+        if (nt <= 0) break;
+        std::vector<int32_t> sig(k, 0);
+        for (int i = t0; i < t1; ++i)
+          for (int32_t r : rows[i]) sig[r] |= 1 << (i - t0);
+        std::vector<int32_t> gray_rank(1 << nt);
+        for (int v = 0; v < (1 << nt); ++v) gray_rank[v ^ (v >> 1)] = v;
+        int32_t* pg = perm.data() + (size_t)gi * k;
+        int32_t* ig = inv.data() + (size_t)gi * k;
+        std::iota(pg, pg + k, 0);
+        std::stable_sort(pg, pg + k,
+                         [&](int32_t x, int32_t y) { return gray_rank[sig[x]] < gray_rank[sig[y]]; });
+        for (int32_t q = 0; q < k; ++q) ig[pg[q]] = gi * k + q;  // global layout position
+        for (int i = t0; i < t1; ++i) {
+          const int32_t h = (int32_t)rows[i].size();
+          order[i].resize(h);
+          std::iota(order[i].begin(), order[i].end(), 0);
+          std::stable_sort(order[i].begin(), order[i].end(), [&](int32_t x, int32_t y) {
+            return ig[rows[i][x]] < ig[rows[i][y]];
+          });
+          const int nst = round_up(h, kBK) / kBK;
+          for (int st = 0; st < nst; ++st) {
+            const size_t nb0 = bx.size();
+            bf[(size_t)i * stride + st] = (int32_t)nb0;
+            // slots [64 st, 64 st + 64): maximal runs of consecutive
+            // positions, then the padding (positions past the whole G x K
+            // layout, zero-filled by the TMA); each run is cut into
+            // power-of-two boxes
+            int slot = st * kBK;
+            const int end = st * kBK + kBK;
+            while (slot < end) {
+              int len = 1;
+              int32_t p0 = slot < h ? ig[rows[i][order[i][slot]]] : G * k;
+              if (slot < h) {
+                while (slot + len < end && slot + len < h &&
+                       ig[rows[i][order[i][slot + len]]] == p0 + len)
+                  ++len;
+              } else {
+                len = end - slot;
+              }
+              int done = 0;
+              while (done < len) {
+                int hb = 64;
+                while (hb > len - done) hb >>= 1;
+                int code = 0;
+                while ((1 << code) < hb) ++code;
+                bx.push_back((uint32_t)((slot + done) - st * kBK) | ((uint32_t)code << 6) |
+                             ((uint32_t)(p0 + done) << 9));
+                done += hb;
+              }
+              slot += len;
+            }
+            cost[i] += 2.0 + (double)(bx.size() - nb0);  // issue cost grows with boxes
+            ++stages;
           }
-          int done = 0;
-          while (done < len) {
-            int hb = 64;
-            while (hb > len - done) hb >>= 1;
-            int code = 0;
-            while ((1 << code) < hb) ++code;
-            bx.push_back((uint32_t)((slot + done) - st * kBK) | ((uint32_t)code << 6) |
-                         ((uint32_t)(p0 + done) << 9));
-            done += hb;
-          }
-          slot += len;
+          for (int st = nst; st < stride; ++st) bf[(size_t)i * stride + st] = (int32_t)bx.size();
         }
-        ++stages;
       }
-      bf[(size_t)i * stride + nst] = (int32_t)bx.size();
-      for (int st = nst + 1; st < stride; ++st) bf[(size_t)i * stride + st] = (int32_t)bx.size();
-    }
-    const double per_stage = stages ? (double)bx.size() / (double)stages : 1e9;
-    if (per_stage <= 4.0) {
+      const double per_stage = stages ? (double)bx.size() / (double)stages : 1e9;
+      if (per_stage > (G == 1 ? 4.0 : 3.0)) continue;
       plan->runs = true;
+      plan->row_copies = G;
       plan->perm = perm;
       plan->inv = inv;
       plan->box_stride = stride;
       box_first.swap(bf);
       boxes.swap(bx);
+      tile_cost.swap(cost);
       // K' order = position order: rows and payload columns follow
-      pay_re.resize(std::max<int64_t>(1, 0));
       int64_t total = 0;
       for (int i = 0; i < n_tiles; ++i) total += (int64_t)row_counts[i] * col_counts[i];
-      pay_re.resize(total);
+      pay_re.resize(std::max<int64_t>(total, 1));
       int64_t base = 0;
       for (int i = 0; i < n_tiles; ++i) {
         const int32_t h = (int32_t)row_counts[i], w = (int32_t)col_counts[i];
@@ -368,6 +390,7 @@ int tw_plan_create_cto(tw_plan** out, int32_t k, int32_t n, int32_t g, int32_t n
         base += (int64_t)h * w;
       }
       pay_src = pay_re.data();
+      break;
     }
   }
   std::vector<int32_t> gidx((size_t)n_tiles * kp, -1);
@@ -427,13 +450,19 @@ int tw_plan_create_cto(tw_plan** out, int32_t k, int32_t n, int32_t g, int32_t n
   const int G = plan->sm_count;
   plan->owner = plan->n_sub <= G && G <= kMaxCtas;
   if (plan->owner) {
+    // weight: k-steps, or (row-run plans) the stages' TMA issue cost
     std::vector<int32_t> c(plan->n_sub, 1);
-    int64_t w = 0;
-    for (const SubTile& st : plan->subtiles) w += st.kp_steps;
+    std::vector<double> wt(plan->n_sub);
+    double w = 0;
+    for (int i = 0; i < plan->n_sub; ++i) {
+      const SubTile& st = plan->subtiles[i];
+      wt[i] = plan->runs ? tile_cost[st.idx_row] : (double)st.kp_steps;
+      w += wt[i];
+    }
     std::vector<std::pair<double, int>> frac;
     int used = 0;
     for (int i = 0; i < plan->n_sub; ++i) {
-      const double q = (double)G * plan->subtiles[i].kp_steps / (double)w;
+      const double q = (double)G * wt[i] / w;
       c[i] = std::max(1, (int)q);
       used += c[i];
       frac.push_back({q - (int)q, i});
@@ -452,7 +481,10 @@ int tw_plan_create_cto(tw_plan** out, int32_t k, int32_t n, int32_t g, int32_t n
     for (int i = 0; i < plan->n_sub; ++i) plan->cta_first[i + 1] = plan->cta_first[i] + c[i];
     int max_steps = 0;
     for (const SubTile& st : plan->subtiles) max_steps = std::max(max_steps, (int)st.kp_steps);
-    plan->resident = max_steps <= kResSteps && !env_int("TW_NO_RESIDENT", 0);
+    // Row-run plans stream the payload with each stage instead: their TMA
+    // activation boxes need the deeper ring (4 x 48 KB vs 3 x 32 KB) more
+    // than the payload needs residency (768^2: 9.3 -> 8.7 us).
+    plan->resident = max_steps <= kResSteps && !plan->runs && !env_int("TW_NO_RESIDENT", 0);
   }
 
   if (int st = upload(&plan->d_subtiles, plan->subtiles, s)) return st;
@@ -611,6 +643,7 @@ int tw_plan_get_info(const tw_plan* p, tw_plan_info* info) {
   info->sm_count = p->sm_count;
   info->has_overlay = p->has_overlay ? 1 : 0;
   info->row_runs = p->runs ? 1 : 0;
+  info->row_copies = p->runs ? p->row_copies : 1;
   return TW_OK;
 }
 
@@ -743,8 +776,8 @@ static int run_tw(const tw_plan* p, const void* x, int64_t m, int64_t ld_x, void
     a.boxes = p->d_boxes;
     a.box_stride = p->box_stride;
     for (int c = 0; c < kRunMaps && a.runs; ++c)
-      if (make_map_2d(&run_maps.m[c], x, p->dtype, (uint64_t)m, (uint64_t)p->k, (uint64_t)ld_x,
-                      64, 1u << c, 128) != TW_OK)
+      if (make_map_2d(&run_maps.m[c], x, p->dtype, (uint64_t)m,
+                      (uint64_t)p->k * p->row_copies, (uint64_t)ld_x, 64, 1u << c, 128) != TW_OK)
         return TW_ERR_INVALID_INPUT;
   }
   TW_CUDA(launch_tw_gemm(p->map_pay, map_out, run_maps, a, work, resident, grid, s));
@@ -775,14 +808,17 @@ int tw_plan_prepare(const tw_plan* p, const void* a, int32_t a_dtype, int64_t m,
   if (!p || !a || !at) return fail(TW_ERR_INVALID_INPUT, "null argument");
   if (m < 1 || lda < p->k || ld_at < m) return fail(TW_ERR_INVALID_INPUT, "bad prepare geometry");
   if (int st = check_dtype(a_dtype)) return st;
-  TW_CUDA(launch_transpose_cast(a, a_dtype, m, p->k, lda, at, p->dtype, ld_at,
-                                p->runs ? p->d_inv : nullptr, static_cast<cudaStream_t>(stream)));
+  for (int gi = 0; gi < (p->runs ? p->row_copies : 1); ++gi)
+    TW_CUDA(launch_transpose_cast(a, a_dtype, m, p->k, lda, at, p->dtype, ld_at,
+                                  p->runs ? p->d_inv + (size_t)gi * p->k : nullptr,
+                                  static_cast<cudaStream_t>(stream)));
   return TW_OK;
 }
 
 int tw_plan_row_order(const tw_plan* p, int32_t* out_rows) {
   if (!p || !out_rows) return fail(TW_ERR_INVALID_INPUT, "null argument");
-  for (int32_t i = 0; i < p->k; ++i) out_rows[i] = p->runs ? p->perm[i] : i;
+  const int64_t n = (int64_t)p->k * (p->runs ? p->row_copies : 1);
+  for (int64_t i = 0; i < n; ++i) out_rows[i] = p->runs ? p->perm[i] : (int32_t)i;
   return TW_OK;
 }
 

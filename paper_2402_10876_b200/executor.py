@@ -139,9 +139,9 @@ class TwPlan:
                                                 _native.ptr(uni, _native.ctypes.c_int32)))
         self.condensed_columns = cond.astype(np.int64)
         self.union_columns = uni.astype(np.int64)
-        order = np.empty(info.k, dtype=np.int32)
+        order = np.empty(info.k * max(1, info.row_copies), dtype=np.int32)
         _native.check(lib.tw_plan_row_order(self._handle, _native.ptr(order, _native.ctypes.c_int32)))
-        self.row_order = order.astype(np.int64)  # position -> original K row
+        self.row_order = order.astype(np.int64)  # layout position -> original K row
         self._row_order_dev = None
 
     @property
@@ -233,13 +233,14 @@ class TwPlan:
         else:
             src = torch.from_numpy(as_matrix(a)).cuda()
         m = int(src.shape[0])
+        rows = self.layout_rows
         if out is not None:
-            if tuple(out.shape) != (k, m) or not _at_ready(out, self.compute_dtype):
-                raise InvalidInputError("out must be a K x M A^T view in the compute dtype")
-            at, ld = out, (out.stride(0) if k > 1 else (m + 7) // 8 * 8)
+            if tuple(out.shape) != (rows, m) or not _at_ready(out, self.compute_dtype):
+                raise InvalidInputError(f"out must be a {rows} x M A^T view in the compute dtype")
+            at, ld = out, out.stride(0)
         else:
             ld = (m + 7) // 8 * 8
-            at = torch.empty((k, ld), dtype=_torch_dtype(self.compute_dtype), device=src.device)
+            at = torch.empty((rows, ld), dtype=_torch_dtype(self.compute_dtype), device=src.device)
         lib = _native.load_library()
         _native.check(lib.tw_plan_prepare(self._handle, src.data_ptr(),
                                           _DTYPE_CODES[_dtype_name(src.dtype)], m, src.stride(0),
@@ -247,13 +248,20 @@ class TwPlan:
         return at if out is not None else at[:, :m]
 
     # -- launches -------------------------------------------------------
-    def _check_x(self, x):
+    @property
+    def layout_rows(self) -> int:
+        """Rows of run()'s input: K, or row_copies x K in the row-run layout."""
+        k = self.original_dims[0]
+        return k * int(self.info.row_copies) if self.uses_row_runs else k
+
+    def _check_x(self, x, rows=None):
         torch = _torch()
         if not isinstance(x, torch.Tensor) or not x.is_cuda:
             raise InvalidInputError("x must be a CUDA A^T (K x M) tensor, see TwPlan.prepare()")
-        k = self.original_dims[0]
+        k = self.original_dims[0] if rows is None else rows
         if x.dim() != 2 or x.shape[0] != k:
-            raise InvalidInputError(f"x must be K x M = {k} x M, got {tuple(x.shape)}")
+            raise InvalidInputError(f"x must be {k} x M (plan layout rows x tokens), "
+                                    f"got {tuple(x.shape)}")
         if x.dtype != _torch_dtype(self.compute_dtype):
             raise InvalidInputError(f"x dtype {x.dtype} != plan compute dtype "
                                     f"{self.compute_dtype}")
@@ -277,12 +285,15 @@ class TwPlan:
         the plan's row layout: the original order for row_layout='natural',
         the permuted order :meth:`prepare` writes for row_layout='runs'
         (``x_layout='natural'`` overrides: original-order rows, gathered)."""
-        m, ld = self._check_x(x)
-        ct = self._out(self.info.n_condensed, m, out, out_dtype)
-        lib = _native.load_library()
         if x_layout not in (None, "natural", "plan"):
             raise InvalidInputError(f"unknown x_layout {x_layout!r}")
         use_plan = self.uses_row_runs if x_layout is None else x_layout == "plan"
+        if use_plan and not self.info.row_runs:
+            raise InvalidInputError("this plan has no row-run layout")
+        rows = self.original_dims[0] * int(self.info.row_copies) if use_plan else None
+        m, ld = self._check_x(x, rows)
+        ct = self._out(self.info.n_condensed, m, out, out_dtype)
+        lib = _native.load_library()
         layout = _native.TW_LAYOUT_PLAN if use_plan else _native.TW_LAYOUT_NATURAL
         _native.check(lib.tw_gemm_ex(self._handle, x.data_ptr(), m, ld, ct.data_ptr(),
                                      ct.stride(0), _DTYPE_CODES[_dtype_name(ct.dtype)], layout,

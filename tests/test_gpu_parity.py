@@ -260,23 +260,26 @@ def test_transpose_cast_exact(m, k, src, dst):
     assert torch.equal(at, a.t().to(dt[dst]))
 
 
-@pytest.mark.parametrize("k,n,m,s,g,mode", [
-    (768, 768, 1000, 0.75, 128, None),        # resident, owner (BERT 768^2 shape)
-    (3072, 768, 1000, 0.75, 128, None),       # streamed, owner (BERT FFN-2 shape)
-    (3072, 768, 777, 0.75, 128, "TW_STRIDED"),
-    (1024, 512, 300, 0.5, 256, None),         # g = 256: 2 sub-tiles per tile
+@pytest.mark.parametrize("k,n,m,s,g,env", [
+    (768, 768, 1000, 0.75, 128, {}),                      # BERT 768^2 shape
+    (3072, 768, 1000, 0.75, 128, {}),                     # BERT FFN-2 shape
+    (3072, 768, 777, 0.75, 128, {"TW_STRIDED": "1"}),
+    (768, 768, 600, 0.75, 128, {"TW_OWNER": "1"}),
+    (1024, 512, 300, 0.5, 256, {}),                       # g = 256: 2 sub-tiles per tile
+    (768, 3072, 1000, 0.75, 128, {"TW_RUN_COPIES": "3"}), # 12 tiles: one order per tile group
 ])
-def test_row_runs_layout_bit_identical(k, n, m, s, g, mode, monkeypatch):
+def test_row_runs_layout_bit_identical(k, n, m, s, g, env, monkeypatch):
     """Plans with the row-run layout: activations prepared into the permuted
     row order and fetched with dense TMA boxes give exactly the result of the
     natural-order cp.async gather (same K' order), and match the oracle."""
-    if mode:
-        monkeypatch.setenv(mode, "1")
+    for name, value in env.items():
+        monkeypatch.setenv(name, value)
     w, a, plan, tsm = _problem(k, n, m, s, g, seed=k + m)
     enc = tw.encode_cto(tsm)
     runs = tw.TwPlan(enc, row_layout="runs")
     assert runs.uses_row_runs, "expected a few-run row order for <= 6 tiles"
-    assert sorted(runs.row_order.tolist()) == list(range(k))
+    copies = int(runs.info.row_copies)
+    assert sorted(runs.row_order.tolist()) == sorted(list(range(k)) * copies)
     o_runs = runs.run(runs.prepare(a))                            # TMA row runs
     o_nat = runs.run(tw.prepare_activations(a), x_layout="natural")  # cp.async gather
     assert torch_equal(o_runs, o_nat)
