@@ -153,6 +153,7 @@ struct tw_plan {
   int32_t* d_perm = nullptr;             // [k] position -> original row
   int32_t* d_inv = nullptr;              // [k] original row -> position
   int32_t* d_box_first = nullptr;        // [n_tiles][box_stride] first box of every stage
+  int32_t* d_gidx_pos = nullptr;         // [n_tiles][kp] kept rows as layout positions
   uint32_t* d_boxes = nullptr;           // slot | log2(rows) << 6 | position << 9
   int32_t* d_gidx = nullptr;  // [n_tiles][kp] kept rows, -1 padded
   void* d_payload = nullptr;
@@ -175,7 +176,7 @@ struct tw_plan {
 
   ~tw_plan() {
     for (void* p : {(void*)d_subtiles, (void*)d_gidx, d_payload, (void*)d_perm, (void*)d_inv,
-                    (void*)d_box_first, (void*)d_boxes,
+                    (void*)d_box_first, (void*)d_boxes, (void*)d_gidx_pos,
                     (void*)d_union_rowmap, (void*)d_ov_start, (void*)d_ov_rows, (void*)d_ov_vals,
                     (void*)d_ov_out, (void*)d_ov_acc, (void*)d_ov_rv, (void*)d_ov_meta})
       if (p) cudaFree(p);
@@ -481,15 +482,21 @@ int tw_plan_create_cto(tw_plan** out, int32_t k, int32_t n, int32_t g, int32_t n
     for (int i = 0; i < plan->n_sub; ++i) plan->cta_first[i + 1] = plan->cta_first[i] + c[i];
     int max_steps = 0;
     for (const SubTile& st : plan->subtiles) max_steps = std::max(max_steps, (int)st.kp_steps);
-    // Row-run plans stream the payload with each stage instead: their TMA
-    // activation boxes need the deeper ring (4 x 48 KB vs 3 x 32 KB) more
-    // than the payload needs residency (768^2: 9.3 -> 8.7 us).
-    plan->resident = max_steps <= kResSteps && !plan->runs && !env_int("TW_NO_RESIDENT", 0);
+    plan->resident = max_steps <= kResSteps && !env_int("TW_NO_RESIDENT", 0);
   }
 
   if (int st = upload(&plan->d_subtiles, plan->subtiles, s)) return st;
   if (int st = upload(&plan->d_gidx, gidx, s)) return st;
   if (plan->runs) {
+    // the same lists as layout positions: the cp.async gather on a
+    // plan-layout A^T (many units per CTA, where TMA boxes lose)
+    std::vector<int32_t> gpos(gidx.size(), -1);
+    for (int i = 0; i < n_tiles; ++i) {
+      const int g = std::min(plan->row_copies - 1, i / ((n_tiles + plan->row_copies - 1) / plan->row_copies));
+      for (size_t j = 0; j < rows[i].size(); ++j)
+        gpos[(size_t)i * kp + j] = plan->inv[(size_t)g * k + rows[i][j]];
+    }
+    if (int st = upload(&plan->d_gidx_pos, gpos, s)) return st;
     if (int st = upload(&plan->d_perm, plan->perm, s)) return st;
     if (int st = upload(&plan->d_inv, plan->inv, s)) return st;
     if (int st = upload(&plan->d_box_first, box_first, s)) return st;
@@ -765,12 +772,35 @@ static int run_tw(const tw_plan* p, const void* x, int64_t m, int64_t ld_x, void
     a.n_units = (int32_t)(p->n_sub * ((m + kTN - 1) / kTN));
     grid = std::min(a.n_units, p->sm_count);
   }
-  const bool resident = a.owner && p->resident;
+  bool resident = a.owner && p->resident;
+  // Plan-layout input: TMA row runs unless a CTA has many units.  Runs win
+  // where the gather is L2->SM-bound (3072x768 21.4 -> 17.3 us; VGG conv4_2
+  // at 6 units per CTA 218 -> 160 us); on long HBM-streaming ranges (VGG
+  // conv1_2: 85 units per CTA) the per-chunk TMA boxes revisit each DRAM row
+  // four times and the cp.async gather by layout position is faster
+  // (545 vs 860 us).  Row runs with <= 2 units per CTA
+  // stream the payload: the TMA boxes need the deeper 4 x 48 KB ring more
+  // than the payload needs residency (768^2: 9.3 -> 8.7 us).
+  bool use_runs = false;
+  if (plan_layout && p->runs) {
+    int64_t max_units = 0;
+    if (a.owner) {
+      for (int i = 0; i < grid; ++i)
+        if (work.w[i].usz > 0)
+          max_units = std::max<int64_t>(
+              max_units, (work.w[i].e - work.w[i].b + work.w[i].usz - 1) / work.w[i].usz);
+    } else {
+      max_units = (a.n_units + grid - 1) / grid;
+    }
+    use_runs = max_units <= env_int("TW_RUN_MAX_UNITS", 16);
+    if (use_runs && max_units <= 2) resident = false;
+    if (!use_runs) a.gidx = p->d_gidx_pos;
+  }
   // row-run path: x is in the plan's permuted row layout
   RunMaps run_maps;
   std::memset(&run_maps, 0, sizeof(run_maps));
   a.runs = 0;
-  if (plan_layout && p->runs) {
+  if (use_runs) {
     a.runs = 1;
     a.box_first = p->d_box_first;
     a.boxes = p->d_boxes;

