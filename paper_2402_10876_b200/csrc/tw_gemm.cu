@@ -423,33 +423,49 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     };
     auto unit_n = [](const Seg& g) { return (g.ue - g.ub + 15) & ~15; };
-    // Owner mode: the owned sub-tile's gather list is staged in shared
-    // memory once (plan constants: before the dependency wait), so a stage's
-    // row indices are a shared load away -- with indices prefetched from
-    // global only one stage ahead, their L2 latency paced the whole gather.
+    // Gather lists live in shared memory, so a stage's row indices are a
+    // shared load away (indices prefetched from global only one stage ahead
+    // let their L2 latency pace the whole gather).  Owner mode with a list
+    // that fits: the owned sub-tile's whole list, staged once (plan
+    // constants: before the dependency wait).  Otherwise chunks of kChunkSt
+    // stages in two alternating buffers, refilled at chunk boundaries; every
+    // gather thread walks the same units and stages, so the named barriers
+    // line up.
+    constexpr int kChunkSt = C::kIdxCap / (2 * kBK);
     bool have = walk.next(args, sg);
-    const bool idx_smem = args.owner && have && sg.d.kp_steps * kBK <= C::kIdxCap;
-    if (idx_smem) {
+    const bool whole = args.owner && have && sg.d.kp_steps * kBK <= C::kIdxCap;
+    auto stage_chunk = [&](const Seg& g, int c) {  // stages [c * kChunkSt, ...) -> buffer c & 1
+      const int first = c * kChunkSt * kBK;
+      const int n = min(kChunkSt, g.d.kp_steps - c * kChunkSt) * kBK;
+      const int32_t* src = args.gidx + static_cast<int64_t>(g.d.idx_row) * args.kp + first;
+      int32_t* dst = sIdx + (c & 1) * kChunkSt * kBK;
+      for (int i = gt; i < n; i += kGatherThreads) dst[i] = __ldg(src + i);
+    };
+    auto begin_unit = [&](const Seg& g) {
+      if (whole) return;
+      named_bar_sync(1, kGatherThreads);  // everyone is done with the old lists
+      stage_chunk(g, 0);
+      if (g.d.kp_steps > kChunkSt) stage_chunk(g, 1);
+      named_bar_sync(1, kGatherThreads);
+    };
+    if (whole) {
       const int32_t* src = args.gidx + static_cast<int64_t>(sg.d.idx_row) * args.kp;
       for (int i = gt; i < sg.d.kp_steps * kBK; i += kGatherThreads) sIdx[i] = __ldg(src + i);
       named_bar_sync(1, kGatherThreads);
     }
-    auto load_idx = [&](const Seg& g, int ks, int (&idx)[kMaxItems]) {
-      if (idx_smem) {
-        const int32_t* src = sIdx + ks * kBK;
+    auto load_idx = [&](int ks, int (&idx)[kMaxItems]) {
+      const int32_t* src =
+          whole ? sIdx + ks * kBK
+                : sIdx + ((ks / kChunkSt) & 1) * kChunkSt * kBK + (ks % kChunkSt) * kBK;
 #pragma unroll
-        for (int i = 0; i < kMaxItems; ++i) idx[i] = slot_row[i] >= 0 ? src[slot_row[i]] : -1;
-      } else {
-        const int32_t* src = args.gidx + static_cast<int64_t>(g.d.idx_row) * args.kp + ks * kBK;
-#pragma unroll
-        for (int i = 0; i < kMaxItems; ++i) idx[i] = slot_row[i] >= 0 ? __ldg(src + slot_row[i]) : -1;
-      }
+      for (int i = 0; i < kMaxItems; ++i) idx[i] = slot_row[i] >= 0 ? src[slot_row[i]] : -1;
     };
     int ks = 0;
     int idx[kMaxItems];
     if (have) {
+      begin_unit(sg);
       layout(unit_n(sg));
-      load_idx(sg, 0, idx);
+      load_idx(0, idx);
     }
     grid_dependency_wait();  // A^T may be written by the previous kernel
     int gs = 0;
@@ -477,9 +493,18 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (++ks >= sg.d.kp_steps) {
         have = walk.next(args, sg);
         ks = 0;
-        if (have) layout(unit_n(sg));
+        if (have) {
+          begin_unit(sg);
+          layout(unit_n(sg));
+        }
+      } else if (!whole && ks % kChunkSt == 0) {
+        // entering chunk c: chunk c - 1 is done everywhere; refill its
+        // buffer with chunk c + 1 (read only after the next boundary's barrier)
+        named_bar_sync(1, kGatherThreads);
+        const int c = ks / kChunkSt;
+        if ((c + 1) * kChunkSt < sg.d.kp_steps) stage_chunk(sg, c + 1);
       }
-      if (have) load_idx(sg, ks, idx);
+      if (have) load_idx(ks, idx);
     }
   } else if (warp == kMmaWarp) {
     // ---------------------------------------------------------- MMA issuer
