@@ -146,6 +146,17 @@ TW_API int tw_plan_row_order(const tw_plan* plan, int32_t* out_rows);
 TW_API int tw_gemm_tew(const tw_plan* plan, const void* at, int64_t m, int64_t ld_at, void* ct,
                        int64_t ld_ct, int32_t out_dtype, void* stream);
 
+/* tw_gemm_tew with a caller-owned workspace of tw_plan_tew_workspace_bytes()
+ * bytes (16-byte aligned): K1 writes the condensed TW result there with its
+ * TMA epilogue and K2 scatters every column to its union row while adding the
+ * residual (faster than K1 scattering union rows itself).  A size of 0 means
+ * the plan does not use one (workspace may then be NULL). */
+TW_API int tw_plan_tew_workspace_bytes(const tw_plan* plan, int64_t m, int32_t out_dtype,
+                                       uint64_t* bytes);
+TW_API int tw_gemm_tew_ws(const tw_plan* plan, const void* at, int64_t m, int64_t ld_at,
+                          void* ct, int64_t ld_ct, int32_t out_dtype, void* workspace,
+                          uint64_t ws_bytes, void* stream);
+
 /* A (m x k row-major, pitch lda, a_dtype) -> A^T (k x m, pitch ld_at, at_dtype).
  * Replaces the float32/float64 carrier copies of core.as_matrix
  * (core.py:32-43) and executor.py:158 on the device; the per-tile column

@@ -88,15 +88,19 @@ __device__ __forceinline__ void fma8(float (&acc)[8], const uint4& a, uint16_t v
 }
 
 
-// 4 outputs at out[bs..bs+3] (+)= o, 16-bit or fp32, tail-masked by n.
+// 4 outputs out[bs..bs+3] = o (+ src[ps..ps+3] when ps >= 0: the TW result),
+// 16-bit or fp32, tail-masked by n.
 __device__ __forceinline__ void residual_store4(const ResidualArgs& args, int64_t bs, int n,
-                                                bool accum, float o0, float o1, float o2,
-                                                float o3) {
+                                                const void* src, int64_t ps, float o0, float o1,
+                                                float o2, float o3) {
   const bool obf = args.out_dtype == kBF16;
-  if (n >= 4 && bs % 4 == 0) {
+  const bool accum = ps >= 0;
+  if (n >= 4 && bs % 4 == 0 && (!accum || ps % 4 == 0)) {
     if (args.out_dtype != kF32) {
       uint2* p = reinterpret_cast<uint2*>(static_cast<uint16_t*>(args.out) + bs);
-      const uint2 prev = accum ? *p : make_uint2(0u, 0u);
+      const uint2 prev =
+          accum ? *reinterpret_cast<const uint2*>(static_cast<const uint16_t*>(src) + ps)
+                : make_uint2(0u, 0u);
       const float2 lo2 = h2_to_f2(prev.x, obf), hi2 = h2_to_f2(prev.y, obf);
       const float f0 = lo2.x + o0, f1 = lo2.y + o1, f2 = hi2.x + o2, f3 = hi2.y + o3;
       uint2 w;
@@ -111,7 +115,9 @@ __device__ __forceinline__ void residual_store4(const ResidualArgs& args, int64_
       *p = w;
     } else {
       float4* p = reinterpret_cast<float4*>(static_cast<float*>(args.out) + bs);
-      const float4 prev = accum ? *p : make_float4(0.f, 0.f, 0.f, 0.f);
+      const float4 prev =
+          accum ? *reinterpret_cast<const float4*>(static_cast<const float*>(src) + ps)
+                : make_float4(0.f, 0.f, 0.f, 0.f);
       *p = make_float4(prev.x + o0, prev.y + o1, prev.z + o2, prev.w + o3);
     }
     return;
@@ -121,7 +127,7 @@ __device__ __forceinline__ void residual_store4(const ResidualArgs& args, int64_
   for (int i = 0; i < 4; ++i) {
     if (i < n) {
       float w = o[i];
-      if (accum) w += load_as_float(args.out, args.out_dtype, bs + i);
+      if (accum) w += load_as_float(src, args.out_dtype, ps + i);
       store_from_float(args.out, args.out_dtype, bs + i, w);
     }
   }
@@ -175,11 +181,16 @@ __global__ void __launch_bounds__(kResThreads, 1)
     const int4 mn = col + kStep < c1 ? __ldg(args.meta + col + kStep) : make_int4(0, 0, 0, 0);
     const bool live = col < c1 && tok < ntok;
     const int64_t bs = static_cast<int64_t>(m.z) * args.ld_out + t0 + tok;
-    // current output of a TW-kept column, consumed after the sum
+    // the TW result of a kept column (workspace row m.w - 1, else the out row
+    // itself), read now and consumed after the sum
+    const void* src = args.src ? args.src : args.out;
+    const int64_t ps = m.w == 0 ? -1
+                       : args.src ? static_cast<int64_t>(m.w - 1) * args.ld_src + t0 + tok
+                                  : bs;
     uint4 prev = make_uint4(0u, 0u, 0u, 0u);
-    const bool vec = fast && ntok - tok >= 8;
-    if (live && vec && m.w)
-      prev = *reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(args.out) + bs);
+    const bool vec = fast && ntok - tok >= 8 && (ps < 0 || ps % 8 == 0);
+    if (live && vec && ps >= 0)
+      prev = *reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(src) + ps);
     const int maxlen = __reduce_max_sync(0xffffffffu, m.y);
     float ac[8];
 #pragma unroll
@@ -225,9 +236,10 @@ __global__ void __launch_bounds__(kResThreads, 1)
         }
         *reinterpret_cast<uint4*>(static_cast<uint16_t*>(args.out) + bs) = make_uint4(o[0], o[1], o[2], o[3]);
       } else {
-        residual_store4(args, bs, ntok - tok, m.w != 0, ac[0], ac[1], ac[2], ac[3]);
+        residual_store4(args, bs, ntok - tok, src, ps, ac[0], ac[1], ac[2], ac[3]);
         if (tok + 4 < ntok)
-          residual_store4(args, bs + 4, ntok - tok - 4, m.w != 0, ac[4], ac[5], ac[6], ac[7]);
+          residual_store4(args, bs + 4, ntok - tok - 4, src, ps < 0 ? -1 : ps + 4, ac[4], ac[5],
+                          ac[6], ac[7]);
       }
     }
     m = mn;

@@ -163,7 +163,8 @@ struct tw_plan {
   int64_t nnz = 0;
   std::vector<int32_t> union_cols;
   int32_t* d_union_rowmap = nullptr;  // condensed col -> union position
-  int32_t n_ov_cols = 0;
+  int32_t n_ov_cols = 0;                // overlay columns with entries (listed first)
+  int32_t n_ov_cols_all = 0;            // + kept columns without entries (workspace mode)
   int32_t* d_ov_start = nullptr;
   int32_t* d_ov_rows = nullptr;
   float* d_ov_vals = nullptr;
@@ -451,13 +452,16 @@ int tw_plan_create_cto(tw_plan** out, int32_t k, int32_t n, int32_t g, int32_t n
   const int G = plan->sm_count;
   plan->owner = plan->n_sub <= G && G <= kMaxCtas;
   if (plan->owner) {
-    // weight: k-steps, or (row-run plans) the stages' TMA issue cost
+    // weight (per token): k-steps, or (row-run plans) the stages' TMA issue
+    // cost, plus a fixed per-unit share for the epilogue and pipeline
+    // fill, which dominates short-K' sub-tiles (TEW 768x3072 keeps K' = 1 on
+    // one tile: proportional-to-k-steps gave it 2 CTAs for all 8192 tokens)
     std::vector<int32_t> c(plan->n_sub, 1);
     std::vector<double> wt(plan->n_sub);
     double w = 0;
     for (int i = 0; i < plan->n_sub; ++i) {
       const SubTile& st = plan->subtiles[i];
-      wt[i] = plan->runs ? tile_cost[st.idx_row] : (double)st.kp_steps;
+      wt[i] = plan->runs ? tile_cost[st.idx_row] + 3 * 16.0 : (double)st.kp_steps + 3.0;
       w += wt[i];
     }
     std::vector<std::pair<double, int>> frac;
@@ -568,7 +572,16 @@ int tw_plan_attach_overlay(tw_plan* p, int32_t k, int32_t n, int64_t nnz, const 
   std::stable_sort(ov_cols.begin(), ov_cols.end(), [&](int32_t a, int32_t b) {
     return col_ptr[a + 1] - col_ptr[a] > col_ptr[b + 1] - col_ptr[b];
   });
-  std::vector<int32_t> start(1, 0), rows, out_rows, acc;
+  // Workspace mode (tw_gemm_tew_ws): K1 writes the condensed TW result to a
+  // scratch C'^T with its fast TMA epilogue and K2 moves every kept column
+  // to its union row, adding the residual; kept columns without overlay
+  // entries ride at the end of the list (0 entries: a plain copy).
+  std::vector<int32_t> cond_of(n, -1);
+  for (int32_t i = 0; i < p->n_cond; ++i) cond_of[p->cond_cols[i]] = i;
+  const int32_t n_with_entries = (int32_t)ov_cols.size();
+  for (int32_t c : p->cond_cols)
+    if (col_ptr[c + 1] == col_ptr[c]) ov_cols.push_back(c);
+  std::vector<int32_t> start(1, 0), rows, out_rows, acc, src_cond;
   std::vector<float> vals;
   for (int32_t c : ov_cols) {
     for (int64_t e = col_ptr[c]; e < col_ptr[c + 1]; ++e) {
@@ -578,6 +591,7 @@ int tw_plan_attach_overlay(tw_plan* p, int32_t k, int32_t n, int64_t nnz, const 
     start.push_back((int32_t)rows.size());
     out_rows.push_back(pos_of[c]);
     acc.push_back(p->tile_of_col[c] >= 0 ? 1 : 0);
+    src_cond.push_back(cond_of[c]);
   }
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   for (void* q : {(void*)p->d_union_rowmap, (void*)p->d_ov_start, (void*)p->d_ov_rows,
@@ -614,7 +628,8 @@ int tw_plan_attach_overlay(tw_plan* p, int32_t k, int32_t n, int64_t nnz, const 
       std::vector<int4> meta(ov_cols.size());
       for (size_t i = 0; i < ov_cols.size(); ++i) {
         const int32_t n = start[i + 1] - start[i];
-        meta[i] = make_int4((int32_t)rv.size(), n, out_rows[i], acc[i]);
+        // w: condensed source row + 1 of a TW-kept column (0: residual only)
+        meta[i] = make_int4((int32_t)rv.size(), n, out_rows[i], src_cond[i] + 1);
         for (int32_t e = start[i]; e < start[i + 1]; ++e)
           rv.push_back(((uint32_t)rows[e] << 16) |
                        (p->dtype == kBF16 ? float_to_bf16_bits(vals[e]) : float_to_half_bits(vals[e])));
@@ -627,7 +642,8 @@ int tw_plan_attach_overlay(tw_plan* p, int32_t k, int32_t n, int64_t nnz, const 
   }
   TW_CUDA(cudaStreamSynchronize(s));
   p->union_cols = uni;
-  p->n_ov_cols = (int32_t)ov_cols.size();
+  p->n_ov_cols = n_with_entries;
+  p->n_ov_cols_all = (int32_t)ov_cols.size();
   p->nnz = nnz;
   p->has_overlay = true;
   return TW_OK;
@@ -852,18 +868,18 @@ int tw_plan_row_order(const tw_plan* p, int32_t* out_rows) {
   return TW_OK;
 }
 
-int tw_gemm_tew(const tw_plan* p, const void* x, int64_t m, int64_t ld_x, void* ct,
-                int64_t ld_ct, int32_t out_dtype, void* stream) {
-  g_last_error.clear();
-  if (int st = check_io(p, x, m, ld_x, ct, ld_ct, out_dtype)) return st;
-  if (!p->has_overlay) return fail(TW_ERR_INVALID_INPUT, "plan has no overlay attached");
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
+static int run_tew(const tw_plan* p, const void* x, int64_t m, int64_t ld_x, void* ct,
+                   int64_t ld_ct, int32_t out_dtype, void* ws, int64_t ld_ws, cudaStream_t s) {
   // TW_TEW_PARTS (diagnostics): 1 = K1 only, 2 = K2 only, otherwise both
   const int parts = env_int("TW_TEW_PARTS", 3);
-  if (parts != 2)
-    if (int st = run_tw(p, x, m, ld_x, ct, ld_ct, out_dtype, p->d_union_rowmap,
-                        (int64_t)p->union_cols.size(), s))
+  if (parts != 2) {
+    if (ws) {
+      if (int st = run_tw(p, x, m, ld_x, ws, ld_ws, out_dtype, nullptr, p->n_cond, s)) return st;
+    } else if (int st = run_tw(p, x, m, ld_x, ct, ld_ct, out_dtype, p->d_union_rowmap,
+                               (int64_t)p->union_cols.size(), s)) {
       return st;
+    }
+  }
   if (parts == 1) return TW_OK;
   ResidualArgs r{};
   r.at = x;
@@ -879,7 +895,9 @@ int tw_gemm_tew(const tw_plan* p, const void* x, int64_t m, int64_t ld_x, void* 
   r.ld_out = ld_ct;
   r.out_dtype = out_dtype;
   r.M = (int32_t)m;
-  r.n_cols = p->n_ov_cols;
+  r.n_cols = ws ? p->n_ov_cols_all : p->n_ov_cols;
+  r.src = ws;
+  r.ld_src = ld_ws;
   r.K = p->k;
   r.rv = p->d_ov_rv;
   r.block_tokens = p->ov_block_tokens;
@@ -892,7 +910,7 @@ int tw_gemm_tew(const tw_plan* p, const void* x, int64_t m, int64_t ld_x, void* 
     r.n_blocks = (int32_t)((m + T - 1) / T);
     int best = 1;
     double best_eff = 0.0;
-    for (int ng = 1; ng <= 4 && ng <= p->n_ov_cols; ++ng) {
+    for (int ng = 1; ng <= 4 && ng <= r.n_cols; ++ng) {
       // CTAs are scheduled as slots free, so the busiest SM does about
       // ceil(ctas / SMs) CTAs of 1 / ng of a block's work; each extra split
       // re-stages the A^T block
@@ -910,13 +928,47 @@ int tw_gemm_tew(const tw_plan* p, const void* x, int64_t m, int64_t ld_x, void* 
     r.group_first[0] = 0;
     for (int g = 1; g < r.n_groups; ++g) {
       const int64_t target = total * g / r.n_groups;
-      while (c < p->n_ov_cols && p->ov_start[c] < target) ++c;
+      while (c < r.n_cols && p->ov_start[c] < target) ++c;
       r.group_first[g] = std::max(c, r.group_first[g - 1]);
     }
-    r.group_first[r.n_groups] = p->n_ov_cols;
+    r.group_first[r.n_groups] = r.n_cols;
   }
   TW_CUDA(launch_tw_residual(r, s));
   return TW_OK;
+}
+
+int tw_gemm_tew(const tw_plan* p, const void* x, int64_t m, int64_t ld_x, void* ct,
+                int64_t ld_ct, int32_t out_dtype, void* stream) {
+  g_last_error.clear();
+  if (int st = check_io(p, x, m, ld_x, ct, ld_ct, out_dtype)) return st;
+  if (!p->has_overlay) return fail(TW_ERR_INVALID_INPUT, "plan has no overlay attached");
+  return run_tew(p, x, m, ld_x, ct, ld_ct, out_dtype, nullptr, 0, static_cast<cudaStream_t>(stream));
+}
+
+int tw_plan_tew_workspace_bytes(const tw_plan* p, int64_t m, int32_t out_dtype, uint64_t* bytes) {
+  if (!p || !bytes) return fail(TW_ERR_INVALID_INPUT, "null argument");
+  if (int st = check_dtype(out_dtype)) return st;
+  const uint64_t ld = (uint64_t)((m + 7) / 8 * 8);
+  *bytes = (p->has_overlay && p->ov_block_tokens > 0)
+               ? (uint64_t)p->n_cond * ld * (out_dtype == kF32 ? 4u : 2u)
+               : 0u;
+  return TW_OK;
+}
+
+int tw_gemm_tew_ws(const tw_plan* p, const void* x, int64_t m, int64_t ld_x, void* ct,
+                   int64_t ld_ct, int32_t out_dtype, void* workspace, uint64_t ws_bytes,
+                   void* stream) {
+  g_last_error.clear();
+  if (int st = check_io(p, x, m, ld_x, ct, ld_ct, out_dtype)) return st;
+  if (!p->has_overlay) return fail(TW_ERR_INVALID_INPUT, "plan has no overlay attached");
+  uint64_t need = 0;
+  if (int st = tw_plan_tew_workspace_bytes(p, m, out_dtype, &need)) return st;
+  void* ws = need ? workspace : nullptr;  // 0 bytes: the scatter path needs none
+  if (need && (!workspace || ws_bytes < need || reinterpret_cast<uintptr_t>(workspace) % 16))
+    return fail(TW_ERR_INVALID_INPUT, "workspace must hold %llu bytes, 16-byte aligned",
+                (unsigned long long)need);
+  return run_tew(p, x, m, ld_x, ct, ld_ct, out_dtype, ws, (m + 7) / 8 * 8,
+                 static_cast<cudaStream_t>(stream));
 }
 
 int tw_transpose_cast(const void* a, int32_t a_dtype, int64_t m, int64_t k, int64_t lda, void* at,

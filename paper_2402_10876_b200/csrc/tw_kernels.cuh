@@ -107,7 +107,9 @@ struct ResidualArgs {
   const uint32_t* rv;       // [nnz] row << 16 | 16-bit value; nullptr = direct kernel
   const int32_t* out_rows;  // [n_cols] output row (union position)
   const int32_t* accumulate;// [n_cols] 1 = add onto TW result, 0 = overwrite
-  const int4* meta;         // [n_cols] {first entry, entries, out row, accumulate}
+  const int4* meta;         // [n_cols] {first entry, entries, out row, source row + 1 (0: none)}
+  const void* src;          // workspace mode: K1's condensed C'^T (source rows), else nullptr
+  int64_t ld_src;           //   (nullptr: the TW result is read back from the out row itself)
   void* out;
   int64_t ld_out;
   int32_t out_dtype;

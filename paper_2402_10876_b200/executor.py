@@ -301,15 +301,28 @@ class TwPlan:
         return ct
 
     def run_tew(self, x, out=None, out_dtype="fp32", stream=None):
-        """C^T over the union columns (|union| x M) = TW + overlay; K1 + K2."""
+        """C^T over the union columns (|union| x M) = TW + overlay; K1 + K2.
+        K1 writes the condensed TW result to a scratch buffer (torch caching
+        allocator, stream-ordered) that K2 scatters to the union rows."""
         if not self.has_overlay:
             raise InvalidInputError("plan has no overlay attached")
+        torch = _torch()
         m, ld = self._check_x(x)
         ct = self._out(self.info.n_union, m, out, out_dtype)
         lib = _native.load_library()
-        _native.check(lib.tw_gemm_tew(self._handle, x.data_ptr(), m, ld, ct.data_ptr(),
-                                      ct.stride(0), _DTYPE_CODES[_dtype_name(ct.dtype)],
-                                      _native.stream_handle(stream)))
+        code = _DTYPE_CODES[_dtype_name(ct.dtype)]
+        need = _native.ctypes.c_uint64()
+        _native.check(lib.tw_plan_tew_workspace_bytes(self._handle, m, code,
+                                                      _native.ctypes.byref(need)))
+        ws = None
+        if need.value:
+            ws = torch.empty(int(need.value), dtype=torch.uint8, device=ct.device)
+            if stream is not None:
+                ws.record_stream(stream)  # freed by the caching allocator after K2 on `stream`
+        _native.check(lib.tw_gemm_tew_ws(self._handle, x.data_ptr(), m, ld, ct.data_ptr(),
+                                         ct.stride(0), code,
+                                         ws.data_ptr() if ws is not None else None,
+                                         int(need.value), _native.stream_handle(stream)))
         return ct
 
 

@@ -295,3 +295,27 @@ def torch_equal(x, y):
     import torch
 
     return torch.equal(x, y)
+
+
+@pytest.mark.parametrize("out_dtype", ["fp32", "fp16"])
+def test_tew_workspace_path_bit_identical(out_dtype):
+    """TEW with the workspace (K1 -> condensed scratch, K2 scatters to union
+    rows) equals the union-row scatter in K1 bit for bit."""
+    import torch
+
+    from paper_2402_10876_b200 import _native
+
+    rng = np.random.default_rng(11)
+    w = tw.round_to(rng.normal(size=(768, 768)).astype(np.float32), "fp16")
+    a = tw.round_to(rng.normal(size=(700, 768)).astype(np.float32), "fp16")
+    _, tsm, ov = tw.prune_tew(w, 0.75, 0.015, 128)
+    plan = tw.TwPlan(tw.encode_cto(tsm), ov)
+    x = plan.prepare(a)
+    o_ws = plan.run_tew(x, out_dtype=out_dtype)
+    o_sc = torch.empty_like(o_ws)
+    lib = _native.load_library()
+    _native.check(lib.tw_gemm_tew(plan._handle, x.data_ptr(), x.shape[1], x.stride(0),
+                                  o_sc.data_ptr(), o_sc.stride(0),
+                                  _native.TW_F32 if out_dtype == "fp32" else _native.TW_F16,
+                                  _native.stream_handle()))
+    assert torch.equal(o_ws, o_sc)
