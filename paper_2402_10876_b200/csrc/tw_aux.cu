@@ -169,7 +169,7 @@ __global__ void __launch_bounds__(kResThreads, 1)
   // One column per lane group per step; the next step's metadata is
   // prefetched one step ahead.
   constexpr int kStep = kCols * kResWarps;
-  constexpr int G = 2 * L;  // entries per group (2 per lane, one 8-byte load)
+  constexpr int G = L;  // entries per group (1 per lane, one 4-byte load)
   const uint32_t zrow = static_cast<uint32_t>(K) << 16;
   const uint8_t* sAb = reinterpret_cast<const uint8_t*>(sAt);
   const bool fast = args.out_dtype != kF32 && args.ld_out % 8 == 0;
@@ -195,21 +195,20 @@ __global__ void __launch_bounds__(kResThreads, 1)
     float ac[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) ac[i] = 0.f;
-    // entry groups: lane tl holds entries 2 tl, 2 tl + 1 of a group;
+    // entry groups: lane tl holds entry tl of a group;
     // groups gi + 1, gi + 2 are in flight while gi is consumed.  Lists are
     // padded to whole groups with zero-row entries (row K of the block is
     // zero) and a lane group past its list substitutes them, so the entry
     // loop has no branches.
-    const uint2* lp = reinterpret_cast<const uint2*>(args.rv + m.x) + tl;
-    uint2 c = __ldg(lp), n1 = __ldg(lp + L);
+    const uint32_t* lp = args.rv + m.x + tl;
+    uint32_t c = __ldg(lp), n1 = __ldg(lp + L);
     for (int eo = 0; eo < maxlen; eo += G) {
-      const uint2 f = __ldg(lp + 2 * L);
+      const uint32_t f = __ldg(lp + 2 * L);
       lp += L;
-      if (eo >= m.y) c = make_uint2(zrow, zrow);
-      const uint32_t w[2] = {c.x, c.y};
+      if (eo >= m.y) c = zrow;
 #pragma unroll
       for (int j = 0; j < G; ++j) {
-        const uint32_t q = L == 1 ? w[j & 1] : __shfl_sync(0xffffffffu, w[j & 1], gbase + (j >> 1));
+        const uint32_t q = L == 1 ? c : __shfl_sync(0xffffffffu, c, gbase + j);
         fma8<kBf>(ac, *reinterpret_cast<const uint4*>(sAb + (q >> 16) * (T * 2)),
                   static_cast<uint16_t>(q & 0xFFFFu));
       }

@@ -611,9 +611,10 @@ int tw_plan_attach_overlay(tw_plan* p, int32_t k, int32_t n, int64_t nnz, const 
   if (int st = upload(&p->d_ov_acc, acc, s)) return st;
   // K2 geometry: A^T block of T tokens for all K rows in shared memory;
   // packed (row, value) lists need row < 2^16.  Each column's list starts on
-  // an 8-byte boundary and is zero-padded to whole groups of 2 * L entries
-  // (L = T / 8 lanes per column), so every lane fetches its next 2 entries
-  // with one 8-byte load.
+  // a group boundary and is zero-padded to whole groups of L entries
+  // (L = T / 8 lanes per column), so every lane fetches its next entry with
+  // one 4-byte load (1 instead of 2 per lane: less padding, 11.5 entries per
+  // column on BERT).
   p->ov_block_tokens = 0;
   p->ov_ctas_per_sm = 0;
   p->ov_start = start;
@@ -623,7 +624,7 @@ int tw_plan_attach_overlay(tw_plan* p, int32_t k, int32_t n, int64_t nnz, const 
     if (T > 0) {
       p->ov_block_tokens = T;
       p->ov_ctas_per_sm = cps;
-      const int G = 2 * (T / 8);
+      const int G = T / 8;
       std::vector<uint32_t> rv;
       std::vector<int4> meta(ov_cols.size());
       for (size_t i = 0; i < ov_cols.size(); ++i) {
