@@ -618,7 +618,7 @@ cudaError_t launch_tw_gemm(const CUtensorMap& map_pay, const CUtensorMap& map_ou
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  attr[0].val.programmaticStreamSerializationAllowed = args.flags & kFlagNoPdl ? 0 : 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   if (resident)

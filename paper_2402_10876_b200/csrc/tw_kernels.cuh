@@ -82,6 +82,7 @@ struct RunMaps {
 constexpr int32_t kFlagSkipA = 1;       // do not load the activations
 constexpr int32_t kFlagSkipStore = 2;   // do not write the output
 constexpr int32_t kFlagSkipMma = 4;     // do not issue tcgen05.mma
+constexpr int32_t kFlagNoPdl = 8;       // launch without programmatic dependent launch (timing only)
 
 // K1: persistent warp-specialised TW GEMM (tcgen05 + TMA + cp.async gather).
 //   map_pay : payload [n_sub * kBN][Kp], box {64 k, kBN rows}, 128-B swizzle
