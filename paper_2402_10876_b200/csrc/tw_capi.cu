@@ -271,9 +271,73 @@ int tw_plan_create_cto(tw_plan** out, int32_t k, int32_t n, int32_t g, int32_t n
   }
   plan->n_cond = (int32_t)plan->cond_cols.size();
 
+  // Narrow tiles (width <= 64) leave most of the 128-row UMMA M idle and
+  // gather their kept rows once per tile.  Consecutive narrow tiles are
+  // therefore merged into 128-column virtual tiles over the UNION of their
+  // kept rows, the payload zero-filled where a tile does not keep a row: one
+  // gather and one full-width MMA serve the whole group (2 x G = 64 at 50 %
+  // rows: 0.75 K rows gathered instead of 2 x 0.5 K, at full M).  The
+  // condensed column order is unchanged; the reference's tile structure
+  // stays in tile_rows / tile_of_col (overlay checks) and kept_macs.
+  int nt = n_tiles;
+  std::vector<uint32_t> rc(row_counts, row_counts + n_tiles), cc(col_counts, col_counts + n_tiles);
+  std::vector<int32_t> tfc = plan->tile_first_cond;
+  const float* pay_in = payload;
+  std::vector<float> pay_merged;
+  {
+    uint32_t wmax = 0;
+    for (int i = 0; i < n_tiles; ++i) wmax = std::max(wmax, col_counts[i]);
+    int gs = 1;
+    while (gs * 2 * (int)wmax <= kBN) gs *= 2;
+    if (gs > 1 && n_tiles > 1 && !env_int("TW_NO_MERGE", 0)) {
+      std::vector<int64_t> pb(n_tiles + 1, 0);
+      for (int i = 0; i < n_tiles; ++i) pb[i + 1] = pb[i] + (int64_t)row_counts[i] * col_counts[i];
+      const int nv = (n_tiles + gs - 1) / gs;
+      std::vector<std::vector<int32_t>> vrows(nv);
+      std::vector<uint32_t> vrc(nv), vcc(nv, 0);
+      std::vector<int32_t> vtfc(nv);
+      std::vector<int32_t> pos(k, -1);
+      for (int v = 0; v < nv; ++v) {
+        const int t0 = v * gs, t1 = std::min(n_tiles, t0 + gs);
+        std::vector<int32_t> u;
+        for (int t = t0; t < t1; ++t) u.insert(u.end(), rows[t].begin(), rows[t].end());
+        std::sort(u.begin(), u.end());
+        u.erase(std::unique(u.begin(), u.end()), u.end());
+        vrows[v] = u;
+        vrc[v] = (uint32_t)u.size();
+        vtfc[v] = plan->tile_first_cond[t0];
+        for (int t = t0; t < t1; ++t) vcc[v] += col_counts[t];
+      }
+      int64_t total = 0;
+      for (int v = 0; v < nv; ++v) total += (int64_t)vrc[v] * vcc[v];
+      pay_merged.assign(total, 0.0f);
+      int64_t base = 0;
+      for (int v = 0; v < nv; ++v) {
+        const int t0 = v * gs, t1 = std::min(n_tiles, t0 + gs);
+        const int32_t hv = (int32_t)vrc[v];
+        for (int32_t j = 0; j < hv; ++j) pos[vrows[v][j]] = j;
+        int32_t col = 0;
+        for (int t = t0; t < t1; ++t) {
+          const int32_t h = (int32_t)row_counts[t], w = (int32_t)col_counts[t];
+          for (int32_t c = 0; c < w; ++c, ++col)
+            for (int32_t j = 0; j < h; ++j)
+              pay_merged[base + (int64_t)col * hv + pos[rows[t][j]]] =
+                  payload[pb[t] + (int64_t)c * h + j];
+        }
+        base += (int64_t)hv * vcc[v];
+      }
+      nt = nv;
+      rc.swap(vrc);
+      cc.swap(vcc);
+      tfc.swap(vtfc);
+      rows.swap(vrows);
+      pay_in = pay_merged.data();
+    }
+  }
+
   // gather lists: each tile's kept rows padded with -1 to whole stages
   int32_t kp = kBK;
-  for (int i = 0; i < n_tiles; ++i) kp = std::max(kp, round_up((int32_t)row_counts[i], kBK));
+  for (int i = 0; i < nt; ++i) kp = std::max(kp, round_up((int32_t)rc[i], kBK));
   plan->kp = kp;
 
   // Row-run layout.  Ordering the rows of A^T by their tile-membership
@@ -287,27 +351,27 @@ int tw_plan_create_cto(tw_plan** out, int32_t k, int32_t n, int32_t g, int32_t n
   // the natural-layout cp.async path and the run path accumulate in the same
   // order and stay bit-identical.  Used when the boxes per 64-row stage stay
   // few.
-  const float* pay_src = payload;
+  const float* pay_src = pay_in;
   std::vector<float> pay_re;
   std::vector<int32_t> box_first;
   std::vector<uint32_t> boxes;
-  std::vector<double> tile_cost(n_tiles, 0.0);  // owner split weight (run path)
+  std::vector<double> tile_cost(nt, 0.0);  // owner split weight (run path)
   // More than one copy (layers with > 6 tiles) measured no faster than the
   // gather on BERT 768x3072 (G = 3: 21.0 vs 20.9 us), so it is opt-in.
   const int max_copies = std::max(1, std::min(4, env_int("TW_RUN_COPIES", 1)));
   if (row_runs && k < (1 << 20) && !env_int("TW_NO_RUNS", 0)) {
     const int stride = kp / kBK + 1;
-    for (int G = (n_tiles + 5) / 6; G <= max_copies && G <= n_tiles; ++G) {
-      const int per = (n_tiles + G - 1) / G;  // tiles per group
+    for (int G = (nt + 5) / 6; G <= max_copies && G <= nt; ++G) {
+      const int per = (nt + G - 1) / G;  // tiles per group
       if ((int64_t)G * k >= (1 << 23)) break;
       std::vector<int32_t> perm((size_t)G * k), inv((size_t)G * k);
-      std::vector<std::vector<int32_t>> order(n_tiles);
-      std::vector<int32_t> bf((size_t)n_tiles * stride, 0);
+      std::vector<std::vector<int32_t>> order(nt);
+      std::vector<int32_t> bf((size_t)nt * stride, 0);
       std::vector<uint32_t> bx;
-      std::vector<double> cost(n_tiles, 0.0);
+      std::vector<double> cost(nt, 0.0);
       int64_t stages = 0;
       for (int gi = 0; gi < G; ++gi) {
-        const int t0 = gi * per, t1 = std::min(n_tiles, t0 + per);
+        const int t0 = gi * per, t1 = std::min(nt, t0 + per);
         const int nt = t1 - t0;
         if (nt <= 0) break;
         std::vector<int32_t> sig(k, 0);
@@ -378,25 +442,25 @@ int tw_plan_create_cto(tw_plan** out, int32_t k, int32_t n, int32_t g, int32_t n
       tile_cost.swap(cost);
       // K' order = position order: rows and payload columns follow
       int64_t total = 0;
-      for (int i = 0; i < n_tiles; ++i) total += (int64_t)row_counts[i] * col_counts[i];
+      for (int i = 0; i < nt; ++i) total += (int64_t)rc[i] * cc[i];
       pay_re.resize(std::max<int64_t>(total, 1));
       int64_t base = 0;
-      for (int i = 0; i < n_tiles; ++i) {
-        const int32_t h = (int32_t)row_counts[i], w = (int32_t)col_counts[i];
+      for (int i = 0; i < nt; ++i) {
+        const int32_t h = (int32_t)rc[i], w = (int32_t)cc[i];
         std::vector<int32_t> r2(h);
         for (int32_t j = 0; j < h; ++j) r2[j] = rows[i][order[i][j]];
         rows[i].swap(r2);
         for (int32_t c = 0; c < w; ++c)
           for (int32_t j = 0; j < h; ++j)
-            pay_re[base + (int64_t)c * h + j] = payload[base + (int64_t)c * h + order[i][j]];
+            pay_re[base + (int64_t)c * h + j] = pay_in[base + (int64_t)c * h + order[i][j]];
         base += (int64_t)h * w;
       }
       pay_src = pay_re.data();
       break;
     }
   }
-  std::vector<int32_t> gidx((size_t)n_tiles * kp, -1);
-  for (int i = 0; i < n_tiles; ++i)
+  std::vector<int32_t> gidx((size_t)nt * kp, -1);
+  for (int i = 0; i < nt; ++i)
     std::copy(rows[i].begin(), rows[i].end(), gidx.begin() + (size_t)i * kp);
 
   // sub-tiles (128-column UMMA-M slices) and payload sources
@@ -406,14 +470,14 @@ int tw_plan_create_cto(tw_plan** out, int32_t k, int32_t n, int32_t g, int32_t n
   std::vector<int64_t> src_base;
   std::vector<int32_t> src_ld;
   int64_t pbase = 0;
-  for (int i = 0; i < n_tiles; ++i) {
-    const int32_t h = (int32_t)row_counts[i], w = (int32_t)col_counts[i];
+  for (int i = 0; i < nt; ++i) {
+    const int32_t h = (int32_t)rc[i], w = (int32_t)cc[i];
     for (int32_t c0 = 0; c0 < w; c0 += bn) {
       SubTile st{};
       st.kp_steps = round_up(h, kBK) / kBK;
       st.idx_row = i;
       st.width = std::min(bn, w - c0);
-      st.out_row = plan->tile_first_cond[i] + c0;
+      st.out_row = tfc[i] + c0;
       st.kept = h;
       subs.push_back(st);
       src_base.push_back(pbase + (int64_t)c0 * h);
@@ -495,8 +559,8 @@ int tw_plan_create_cto(tw_plan** out, int32_t k, int32_t n, int32_t g, int32_t n
     // the same lists as layout positions: the cp.async gather on a
     // plan-layout A^T (many units per CTA, where TMA boxes lose)
     std::vector<int32_t> gpos(gidx.size(), -1);
-    for (int i = 0; i < n_tiles; ++i) {
-      const int g = std::min(plan->row_copies - 1, i / ((n_tiles + plan->row_copies - 1) / plan->row_copies));
+    for (int i = 0; i < nt; ++i) {
+      const int g = std::min(plan->row_copies - 1, i / ((nt + plan->row_copies - 1) / plan->row_copies));
       for (size_t j = 0; j < rows[i].size(); ++j)
         gpos[(size_t)i * kp + j] = plan->inv[(size_t)g * k + rows[i][j]];
     }
