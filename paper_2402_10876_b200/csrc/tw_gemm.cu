@@ -83,7 +83,7 @@ struct Cfg {
   static constexpr int kBarrierBytes = 256;
   static constexpr int kSubBytes = kRes ? 0 : kMaxSmemSub * static_cast<int>(sizeof(SubTile));
   // owner mode: the owned sub-tile's whole gather list, staged once
-  static constexpr int kIdxCap = kRes ? kResSteps * kBK : 60 * kBK;
+  static constexpr int kIdxCap = kRes ? kResSteps * kBK : 64 * kBK;
   static constexpr int kIdxBytes = kIdxCap * 4;
   static constexpr int kSmemBytes = kStages * kStageBytes + kPayloadRegion +
                                     kEpilogueWarps * kStgBytes + kBarrierBytes + kSubBytes +
@@ -172,8 +172,8 @@ __device__ __forceinline__ void reg_fence(uint32_t (&w)[16]) {
 // buffers used alternately (sbuf), so filling one overlaps the bulk read of
 // the other; otherwise 16-byte / scalar stores of each thread's row segment.
 __device__ __forceinline__ void epilogue_rows(const GemmArgs& args, const CUtensorMap* map_out,
-                                              uint8_t* stg, int& sbuf, uint32_t t0, int lane,
-                                              int orow, bool row_live, bool warp_full,
+                                              uint8_t* stg, int& sbuf, bool dbl, uint32_t t0,
+                                              int lane, int orow, bool row_live, bool warp_full,
                                               int row0_tma, int tok0, int ntok, int lim) {
   const bool do_store = !(args.flags & kFlagSkipStore);
   const int esz = args.out_dtype == kF32 ? 4 : 2;
@@ -214,8 +214,11 @@ __device__ __forceinline__ void epilogue_rows(const GemmArgs& args, const CUtens
     if (more) tmem_ld_32x32b_x16(t0 + c + 16, w);
     if (!live) continue;
     if (args.use_tma_store && warp_full && whole) {
-      // the store that last read this buffer (two stores ago) must be done
-      if (lane == 0) bulk_wait_read<1>();
+      // the store that last read this buffer (two stores ago; the previous
+      // one with a single buffer) must be done
+      if (lane == 0) {
+        if (dbl) bulk_wait_read<1>(); else bulk_wait_read<0>();
+      }
       __syncwarp();
       uint8_t* buf = stg + sbuf * 1024;
       // row `lane` = 32 bytes, 16-byte halves XOR-swizzled (SWIZZLE_32B)
@@ -229,7 +232,7 @@ __device__ __forceinline__ void epilogue_rows(const GemmArgs& args, const CUtens
         tma_store_2d(map_out, buf, tok, row0_tma);
         bulk_commit();
       }
-      sbuf ^= 1;
+      if (dbl) sbuf ^= 1;
       continue;
     }
     if (!row_live) continue;
@@ -278,6 +281,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int32_t flags = args.flags;
+  // Run path, streamed kernel: the gather warps have nothing to gather, so
+  // they join the epilogue (24 warps instead of 8, the extra 16 staging in
+  // the unused gather-list region) -- the epilogue is a fixed ~4K-cycle cost
+  // per unit that a CTA with one or two units cannot hide.
+  const bool wide_epi = !kRes && args.runs;
+  constexpr int kWideEpi = kEpilogueWarps + kGatherWarps;
 
   // Everything up to the role split reads only plan constants (tables, gather
   // lists, payload), so it overlaps the previous kernel's tail under
@@ -299,7 +308,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], kEpilogueWarps);
+      mbar_init(&tempty[a], wide_epi ? kWideEpi : kEpilogueWarps);
     }
     for (int k = 0; k < kResSteps; ++k) mbar_init(&pfull[k], 1);
     fence_barrier_init();
@@ -546,14 +555,23 @@ __global__ void __launch_bounds__(kThreads, 1)
         ++j;
       }
     }
-  } else if (warp >= kEpilogueWarp0) {
+  } else if (warp >= kEpilogueWarp0 || (wide_epi && warp >= kGatherWarp0)) {
     // ------------------------------------------------------------ epilogue
-    // Warp w owns TMEM lanes 32*(w%4).. (output columns c of the sub-tile)
-    // and token half h of the unit.
+    // Epilogue warp ew owns TMEM lanes 32*(ew%4).. (output columns c of the
+    // sub-tile) and token part ew/4 of the unit (2 parts, or 6 with the
+    // gather warps joining on the run path).  ew % 4 == warp % 4 because both
+    // warp ranges start on a warpgroup boundary.
+    const int ew = warp >= kEpilogueWarp0 ? warp - kEpilogueWarp0
+                                          : kEpilogueWarps + (warp - kGatherWarp0);
+    const int parts = (wide_epi ? kWideEpi : kEpilogueWarps) / 4;
     const int q = warp & 3;
-    const int h = (warp - kEpilogueWarp0) >> 2;
+    const int part = ew >> 2;
     const int c = q * 32 + lane;  // output column within the 128-wide sub-tile
-    uint8_t* stg = sStg + (warp - kEpilogueWarp0) * kStgBytes;
+    // 2 x 1 KB double-buffered staging for the 8 dedicated warps; 1 KB in the
+    // gather-list region for the gather warps
+    const bool dbl = ew < kEpilogueWarps;
+    uint8_t* stg = dbl ? sStg + ew * kStgBytes
+                       : reinterpret_cast<uint8_t*>(sIdx) + (ew - kEpilogueWarps) * 1024;
     int sbuf = 0;
     grid_dependency_wait();  // the previous kernel may still read our output buffer
     int j = 0;
@@ -562,17 +580,19 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&tfull[acc], (j >> 1) & 1);
       tc_fence_after();
       if (trace && warp == kEpilogueWarp0 && lane == 0 && j < 256) trace[2048 + 2 * j] = clock64();
+      const int n = (sg.ue - sg.ub + 15) & ~15;
+      const int per = ((n + parts - 1) / parts + 15) & ~15;  // tokens per part
+      const int tlo = part * per;
       const uint32_t t0 =
-          tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * kTileN + h * 128;
+          tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * kTileN + tlo;
       const bool row_live = c < sg.d.width;
       const bool warp_full = q * 32 + 32 <= sg.d.width && args.rowmap == nullptr;
       const int crow = sg.d.out_row + c;
       const int orow = row_live ? (args.rowmap ? __ldg(args.rowmap + crow) : crow) : 0;
-      const int tok0 = sg.ub + h * 128;
-      const int ntok = min(128, ((sg.ue - sg.ub + 15) & ~15) - h * 128);
+      const int ntok = min(per, n - tlo);
       if (ntok > 0)
-        epilogue_rows(args, &map_out, stg, sbuf, t0, lane, orow, row_live, warp_full,
-                      sg.d.out_row + q * 32, tok0, ntok, sg.ue);
+        epilogue_rows(args, &map_out, stg, sbuf, dbl, t0, lane, orow, row_live, warp_full,
+                      sg.d.out_row + q * 32, sg.ub + tlo, ntok, sg.ue);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
