@@ -251,6 +251,27 @@ __device__ __forceinline__ void epilogue_rows(const GemmArgs& args, const CUtens
   }
 }
 
+// One unit's epilogue for one warp: TMEM quadrant q (output columns
+// q*32..), token part `part` of `nparts` (multiples of 16 tokens).
+__device__ __forceinline__ void epilogue_unit(const GemmArgs& args, const CUtensorMap* map_out,
+                                              const Seg& sg, uint32_t tmem_base, int acc,
+                                              int tile_n, int q, int lane, int part, int nparts,
+                                              uint8_t* stg, int& sbuf, bool dbl) {
+  const int n = (sg.ue - sg.ub + 15) & ~15;
+  const int per = ((n + nparts - 1) / nparts + 15) & ~15;  // tokens per part
+  const int tlo = part * per;
+  const int ntok = min(per, n - tlo);
+  if (ntok <= 0) return;
+  const int c = q * 32 + lane;  // output column within the 128-wide sub-tile
+  const uint32_t t0 = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * tile_n + tlo;
+  const bool row_live = c < sg.d.width;
+  const bool warp_full = q * 32 + 32 <= sg.d.width && args.rowmap == nullptr;
+  const int crow = sg.d.out_row + c;
+  const int orow = row_live ? (args.rowmap ? __ldg(args.rowmap + crow) : crow) : 0;
+  epilogue_rows(args, map_out, stg, sbuf, dbl, t0, lane, orow, row_live, warp_full,
+                sg.d.out_row + q * 32, sg.ub + tlo, ntok, sg.ue);
+}
+
 template <bool kRes>
 __global__ void __launch_bounds__(kThreads, 1)
     tw_gemm_kernel(const __grid_constant__ CUtensorMap map_pay,
@@ -478,6 +499,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     grid_dependency_wait();  // A^T may be written by the previous kernel
     int gs = 0;
+    int units = 0;
+    Seg last = sg;
     while (have) {
       const int stage = gs % kStages;
       mbar_wait(&empty[stage], ((gs / kStages) & 1) ^ 1u);
@@ -500,6 +523,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       // advance and prefetch the next stage's indices (consumed after the
       // next empty-slot wait, which hides their latency)
       if (++ks >= sg.d.kp_steps) {
+        last = sg;
+        ++units;
         have = walk.next(args, sg);
         ks = 0;
         if (have) {
@@ -514,6 +539,20 @@ __global__ void __launch_bounds__(kThreads, 1)
         if ((c + 1) * kChunkSt < sg.d.kp_steps) stage_chunk(sg, c + 1);
       }
       if (have) load_idx(ks, idx);
+    }
+    // The CTA's last unit: nothing is left to gather, and once its
+    // accumulator is full every ring slot has been consumed, so the gather
+    // warps join its epilogue (6 token parts per quadrant instead of 2),
+    // staging in ring slot memory.  This shortens the exposed tail.
+    if (units > 0) {
+      const int j = units - 1;
+      const int ew = kEpilogueWarps + (warp - kGatherWarp0);
+      mbar_wait(&tfull[j & 1], (j >> 1) & 1);
+      tc_fence_after();
+      int sbuf = 0;
+      epilogue_unit(args, &map_out, last, tmem_base, j & 1, kTileN, warp & 3, lane, ew >> 2,
+                    kWideEpi / 4, sX + (ew - kEpilogueWarps) * kStgBytes, sbuf, true);
+      if (lane == 0) bulk_wait_all<0>();
     }
   } else if (warp == kMmaWarp) {
     // ---------------------------------------------------------- MMA issuer
@@ -566,7 +605,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int parts = (wide_epi ? kWideEpi : kEpilogueWarps) / 4;
     const int q = warp & 3;
     const int part = ew >> 2;
-    const int c = q * 32 + lane;  // output column within the 128-wide sub-tile
     // 2 x 1 KB double-buffered staging for the 8 dedicated warps; 1 KB in the
     // gather-list region for the gather warps
     const bool dbl = ew < kEpilogueWarps;
@@ -575,24 +613,20 @@ __global__ void __launch_bounds__(kThreads, 1)
     int sbuf = 0;
     grid_dependency_wait();  // the previous kernel may still read our output buffer
     int j = 0;
+    Walker ahead = walk;  // one unit ahead: is the current unit the last?
+    Seg nxt;
+    bool more = ahead.next(args, nxt);
     while (walk.next(args, sg)) {
+      more = ahead.next(args, nxt);
       const int acc = j & 1;
       mbar_wait(&tfull[acc], (j >> 1) & 1);
       tc_fence_after();
       if (trace && warp == kEpilogueWarp0 && lane == 0 && j < 256) trace[2048 + 2 * j] = clock64();
-      const int n = (sg.ue - sg.ub + 15) & ~15;
-      const int per = ((n + parts - 1) / parts + 15) & ~15;  // tokens per part
-      const int tlo = part * per;
-      const uint32_t t0 =
-          tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * kTileN + tlo;
-      const bool row_live = c < sg.d.width;
-      const bool warp_full = q * 32 + 32 <= sg.d.width && args.rowmap == nullptr;
-      const int crow = sg.d.out_row + c;
-      const int orow = row_live ? (args.rowmap ? __ldg(args.rowmap + crow) : crow) : 0;
-      const int ntok = min(per, n - tlo);
-      if (ntok > 0)
-        epilogue_rows(args, &map_out, stg, sbuf, dbl, t0, lane, orow, row_live, warp_full,
-                      sg.d.out_row + q * 32, sg.ub + tlo, ntok, sg.ue);
+      // the gather warps share the last unit of the cp.async path (and every
+      // unit of the run path)
+      const int nparts = (wide_epi || !more) ? kWideEpi / 4 : parts;
+      epilogue_unit(args, &map_out, sg, tmem_base, acc, kTileN, q, lane, part, nparts, stg, sbuf,
+                    dbl);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
