@@ -264,10 +264,9 @@ def run_ours(args, cfg, rank: int, world: int) -> None:
     for r in range(N_ROTATE):
         layer_set = []
         for li, L in enumerate(layers):
-            # TW layers take their activations in the plan's row-run layout
-            # (prepare() writes it); TEW plans keep the natural order
-            plan = tw.TwPlan(L["enc"], L["ov"], compute_dtype="fp16",
-                             row_layout="natural" if tew else "runs")
+            # activations in the plan's row-run layout (prepare() writes it;
+            # TEW plans read it in K1 and K2)
+            plan = tw.TwPlan(L["enc"], L["ov"], compute_dtype="fp16", row_layout="runs")
             a = activations(cfg, L["k"], li, rank)
             at = plan.prepare(torch.from_numpy(a).to(dev))
             rows = plan.info.n_union if tew else plan.info.n_condensed

@@ -157,6 +157,16 @@ TW_API int tw_gemm_tew_ws(const tw_plan* plan, const void* at, int64_t m, int64_
                           void* ct, int64_t ld_ct, int32_t out_dtype, void* workspace,
                           uint64_t ws_bytes, void* stream);
 
+/* tw_gemm_tew_ws with the activation layout of tw_gemm_ex: TW_LAYOUT_PLAN
+ * reads A^T in the plan's row-run order (tw_plan_prepare) in both K1 and K2
+ * (the overlay rows are remapped to layout positions at attach time), so a
+ * TEW layer gets the dense-TMA row runs too.  Results are bit-identical to
+ * tw_gemm_tew_ws on the natural-order A^T.
+ * Replaces: executor.gemm_tew (executor.py:180-203). */
+TW_API int tw_gemm_tew_ex(const tw_plan* plan, const void* at, int64_t m, int64_t ld_at,
+                          void* ct, int64_t ld_ct, int32_t out_dtype, void* workspace,
+                          uint64_t ws_bytes, int32_t x_layout, void* stream);
+
 /* A (m x k row-major, pitch lda, a_dtype) -> A^T (k x m, pitch ld_at, at_dtype).
  * Replaces the float32/float64 carrier copies of core.as_matrix
  * (core.py:32-43) and executor.py:158 on the device; the per-tile column

@@ -172,6 +172,8 @@ struct tw_plan {
   int32_t* d_ov_acc = nullptr;
   int4* d_ov_meta = nullptr;          // K2 per column: {first entry, entries, out row, accumulate}
   uint32_t* d_ov_rv = nullptr;         // K2 lists: row << 16 | 16-bit value
+  int32_t* d_ov_rows_pos = nullptr;     // row-run plans: d_ov_rows as layout positions (copy 0)
+  uint32_t* d_ov_rv_pos = nullptr;      // row-run plans: d_ov_rv as layout positions (copy 0)
   int32_t ov_block_tokens = 0, ov_ctas_per_sm = 0;
   std::vector<int32_t> ov_start;       // host copy of the K2 column pointers
 
@@ -179,7 +181,8 @@ struct tw_plan {
     for (void* p : {(void*)d_subtiles, (void*)d_gidx, d_payload, (void*)d_perm, (void*)d_inv,
                     (void*)d_box_first, (void*)d_boxes, (void*)d_gidx_pos,
                     (void*)d_union_rowmap, (void*)d_ov_start, (void*)d_ov_rows, (void*)d_ov_vals,
-                    (void*)d_ov_out, (void*)d_ov_acc, (void*)d_ov_rv, (void*)d_ov_meta})
+                    (void*)d_ov_out, (void*)d_ov_acc, (void*)d_ov_rv, (void*)d_ov_meta,
+                    (void*)d_ov_rows_pos, (void*)d_ov_rv_pos})
       if (p) cudaFree(p);
   }
 };
@@ -188,7 +191,7 @@ extern "C" {
 
 const char* tw_last_error(void) { return g_last_error.c_str(); }
 
-int32_t tw_abi_version(void) { return 400; }
+int32_t tw_abi_version(void) { return 410; }
 
 int tw_plan_create_cto(tw_plan** out, int32_t k, int32_t n, int32_t g, int32_t n_tiles,
                        const uint32_t* row_counts, const uint32_t* col_counts,
@@ -660,9 +663,10 @@ int tw_plan_attach_overlay(tw_plan* p, int32_t k, int32_t n, int64_t nnz, const 
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   for (void* q : {(void*)p->d_union_rowmap, (void*)p->d_ov_start, (void*)p->d_ov_rows,
                   (void*)p->d_ov_vals, (void*)p->d_ov_out, (void*)p->d_ov_acc, (void*)p->d_ov_rv,
-                  (void*)p->d_ov_meta})
+                  (void*)p->d_ov_meta, (void*)p->d_ov_rows_pos, (void*)p->d_ov_rv_pos})
     if (q) cudaFree(q);
-  p->d_ov_rv = nullptr;
+  p->d_ov_rv = p->d_ov_rv_pos = nullptr;
+  p->d_ov_rows_pos = nullptr;
   p->d_union_rowmap = nullptr;
   p->d_ov_start = p->d_ov_rows = p->d_ov_out = p->d_ov_acc = nullptr;
   p->d_ov_vals = nullptr;
@@ -673,6 +677,13 @@ int tw_plan_attach_overlay(tw_plan* p, int32_t k, int32_t n, int64_t nnz, const 
   if (int st = upload(&p->d_ov_vals, vals, s)) return st;
   if (int st = upload(&p->d_ov_out, out_rows, s)) return st;
   if (int st = upload(&p->d_ov_acc, acc, s)) return st;
+  // Row-run plans: K2 reads A^T in the plan layout too (tw_gemm_tew_ex with
+  // TW_LAYOUT_PLAN), through copy 0's positions (p->inv[r] < k).
+  if (p->runs) {
+    std::vector<int32_t> rows_pos(rows.size());
+    for (size_t e = 0; e < rows.size(); ++e) rows_pos[e] = p->inv[rows[e]];
+    if (int st = upload(&p->d_ov_rows_pos, rows_pos, s)) return st;
+  }
   // K2 geometry: A^T block of T tokens for all K rows in shared memory;
   // packed (row, value) lists need row < 2^16.  Each column's list starts on
   // a group boundary and is zero-padded to whole groups of L entries
@@ -703,6 +714,11 @@ int tw_plan_attach_overlay(tw_plan* p, int32_t k, int32_t n, int64_t nnz, const 
       rv.resize(rv.size() + 2 * G, (uint32_t)k << 16);  // the pipeline fetches two groups ahead
       if (int st = upload(&p->d_ov_rv, rv, s)) return st;
       if (int st = upload(&p->d_ov_meta, meta, s)) return st;
+      if (p->runs) {
+        for (uint32_t& x : rv)  // zero row k stays k (the staged block's appended row)
+          if ((int32_t)(x >> 16) < k) x = ((uint32_t)p->inv[x >> 16] << 16) | (x & 0xffffu);
+        if (int st = upload(&p->d_ov_rv_pos, rv, s)) return st;
+      }
     }
   }
   TW_CUDA(cudaStreamSynchronize(s));
@@ -934,14 +950,16 @@ int tw_plan_row_order(const tw_plan* p, int32_t* out_rows) {
 }
 
 static int run_tew(const tw_plan* p, const void* x, int64_t m, int64_t ld_x, void* ct,
-                   int64_t ld_ct, int32_t out_dtype, void* ws, int64_t ld_ws, cudaStream_t s) {
+                   int64_t ld_ct, int32_t out_dtype, void* ws, int64_t ld_ws, cudaStream_t s,
+                   bool plan_layout = false) {
   // TW_TEW_PARTS (diagnostics): 1 = K1 only, 2 = K2 only, otherwise both
   const int parts = env_int("TW_TEW_PARTS", 3);
   if (parts != 2) {
     if (ws) {
-      if (int st = run_tw(p, x, m, ld_x, ws, ld_ws, out_dtype, nullptr, p->n_cond, s)) return st;
+      if (int st = run_tw(p, x, m, ld_x, ws, ld_ws, out_dtype, nullptr, p->n_cond, s, plan_layout))
+        return st;
     } else if (int st = run_tw(p, x, m, ld_x, ct, ld_ct, out_dtype, p->d_union_rowmap,
-                               (int64_t)p->union_cols.size(), s)) {
+                               (int64_t)p->union_cols.size(), s, plan_layout)) {
       return st;
     }
   }
@@ -951,7 +969,7 @@ static int run_tew(const tw_plan* p, const void* x, int64_t m, int64_t ld_x, voi
   r.ld_at = ld_x;
   r.in_dtype = p->dtype;
   r.col_start = p->d_ov_start;
-  r.rows = p->d_ov_rows;
+  r.rows = plan_layout ? p->d_ov_rows_pos : p->d_ov_rows;
   r.vals = p->d_ov_vals;
   r.out_rows = p->d_ov_out;
   r.meta = p->d_ov_meta;
@@ -964,7 +982,7 @@ static int run_tew(const tw_plan* p, const void* x, int64_t m, int64_t ld_x, voi
   r.src = ws;
   r.ld_src = ld_ws;
   r.K = p->k;
-  r.rv = p->d_ov_rv;
+  r.rv = plan_layout ? p->d_ov_rv_pos : p->d_ov_rv;
   r.block_tokens = p->ov_block_tokens;
   if (r.block_tokens > 0) {
     // grid = token blocks x column splits; splits (nnz-balanced runs of the
@@ -1034,6 +1052,26 @@ int tw_gemm_tew_ws(const tw_plan* p, const void* x, int64_t m, int64_t ld_x, voi
                 (unsigned long long)need);
   return run_tew(p, x, m, ld_x, ct, ld_ct, out_dtype, ws, (m + 7) / 8 * 8,
                  static_cast<cudaStream_t>(stream));
+}
+
+int tw_gemm_tew_ex(const tw_plan* p, const void* x, int64_t m, int64_t ld_x, void* ct,
+                   int64_t ld_ct, int32_t out_dtype, void* workspace, uint64_t ws_bytes,
+                   int32_t x_layout, void* stream) {
+  g_last_error.clear();
+  if (int st = check_io(p, x, m, ld_x, ct, ld_ct, out_dtype)) return st;
+  if (!p->has_overlay) return fail(TW_ERR_INVALID_INPUT, "plan has no overlay attached");
+  if (x_layout != TW_LAYOUT_NATURAL && x_layout != TW_LAYOUT_PLAN)
+    return fail(TW_ERR_INVALID_INPUT, "unknown activation layout %d", x_layout);
+  const bool plan_layout = x_layout == TW_LAYOUT_PLAN;
+  if (plan_layout && !p->runs) return fail(TW_ERR_INVALID_INPUT, "this plan has no row-run layout");
+  uint64_t need = 0;
+  if (int st = tw_plan_tew_workspace_bytes(p, m, out_dtype, &need)) return st;
+  void* ws = need ? workspace : nullptr;
+  if (need && (!workspace || ws_bytes < need || reinterpret_cast<uintptr_t>(workspace) % 16))
+    return fail(TW_ERR_INVALID_INPUT, "workspace must hold %llu bytes, 16-byte aligned",
+                (unsigned long long)need);
+  return run_tew(p, x, m, ld_x, ct, ld_ct, out_dtype, ws, (m + 7) / 8 * 8,
+                 static_cast<cudaStream_t>(stream), plan_layout);
 }
 
 int tw_transpose_cast(const void* a, int32_t a_dtype, int64_t m, int64_t k, int64_t lda, void* at,

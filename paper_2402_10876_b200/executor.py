@@ -146,10 +146,9 @@ class TwPlan:
 
     @property
     def uses_row_runs(self) -> bool:
-        """True when run()'s input is in this plan's permuted row layout
-        (row_layout='runs', the library found few-run row orders, no overlay)."""
-        return (self.row_layout == "runs" and bool(self.info.row_runs)
-                and not bool(self.info.has_overlay))
+        """True when run()'s and run_tew()'s input is in this plan's permuted
+        row layout (row_layout='runs' and the library found few-run row orders)."""
+        return self.row_layout == "runs" and bool(self.info.row_runs)
 
     @property
     def has_overlay(self) -> bool:
@@ -300,14 +299,21 @@ class TwPlan:
                                      _native.stream_handle(stream)))
         return ct
 
-    def run_tew(self, x, out=None, out_dtype="fp32", stream=None):
+    def run_tew(self, x, out=None, out_dtype="fp32", stream=None, x_layout=None):
         """C^T over the union columns (|union| x M) = TW + overlay; K1 + K2.
         K1 writes the condensed TW result to a scratch buffer (torch caching
-        allocator, stream-ordered) that K2 scatters to the union rows."""
+        allocator, stream-ordered) that K2 scatters to the union rows.  x is
+        in the plan's row layout, as for :meth:`run`."""
         if not self.has_overlay:
             raise InvalidInputError("plan has no overlay attached")
+        if x_layout not in (None, "natural", "plan"):
+            raise InvalidInputError(f"unknown x_layout {x_layout!r}")
+        use_plan = self.uses_row_runs if x_layout is None else x_layout == "plan"
+        if use_plan and not self.info.row_runs:
+            raise InvalidInputError("this plan has no row-run layout")
         torch = _torch()
-        m, ld = self._check_x(x)
+        m, ld = self._check_x(x, self.original_dims[0] * int(self.info.row_copies)
+                              if use_plan else None)
         ct = self._out(self.info.n_union, m, out, out_dtype)
         lib = _native.load_library()
         code = _DTYPE_CODES[_dtype_name(ct.dtype)]
@@ -319,10 +325,11 @@ class TwPlan:
             ws = torch.empty(int(need.value), dtype=torch.uint8, device=ct.device)
             if stream is not None:
                 ws.record_stream(stream)  # freed by the caching allocator after K2 on `stream`
-        _native.check(lib.tw_gemm_tew_ws(self._handle, x.data_ptr(), m, ld, ct.data_ptr(),
+        layout = _native.TW_LAYOUT_PLAN if use_plan else _native.TW_LAYOUT_NATURAL
+        _native.check(lib.tw_gemm_tew_ex(self._handle, x.data_ptr(), m, ld, ct.data_ptr(),
                                          ct.stride(0), code,
                                          ws.data_ptr() if ws is not None else None,
-                                         int(need.value), _native.stream_handle(stream)))
+                                         int(need.value), layout, _native.stream_handle(stream)))
         return ct
 
 

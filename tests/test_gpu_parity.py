@@ -319,3 +319,31 @@ def test_tew_workspace_path_bit_identical(out_dtype):
                                   _native.TW_F32 if out_dtype == "fp32" else _native.TW_F16,
                                   _native.stream_handle()))
     assert torch.equal(o_ws, o_sc)
+
+
+@pytest.mark.parametrize("k,n,m,out_dtype,env", [
+    (768, 768, 700, "fp32", {}),
+    (3072, 768, 500, "fp16", {}),
+    (768, 3072, 300, "fp16", {"TW_RUN_COPIES": "3"}),   # G copies: K2 reads copy 0
+    (768, 768, 333, "fp32", {"TW_RESIDUAL_DIRECT": "1"}),  # K2 per-entry path, remapped rows
+])
+def test_tew_row_runs_layout_bit_identical(k, n, m, out_dtype, env, monkeypatch):
+    """TEW on a row-run plan: K1 and K2 both read A^T in the plan layout (the
+    overlay rows remapped to layout positions) and give exactly the result of
+    the natural-order input through the same plan; the oracle agrees."""
+    for name, value in env.items():
+        monkeypatch.setenv(name, value)
+    rng = np.random.default_rng(k + n + m)
+    w = tw.round_to(rng.normal(size=(k, n)).astype(np.float32), "fp16")
+    a = tw.round_to(rng.normal(size=(m, k)).astype(np.float32), "fp16")
+    _, tsm, ov = tw.prune_tew(w, 0.75, 0.015, 128)
+    plan = tw.TwPlan(tw.encode_cto(tsm), ov, row_layout="runs")
+    assert plan.uses_row_runs
+    o_plan = plan.run_tew(plan.prepare(a), out_dtype=out_dtype)
+    o_nat = plan.run_tew(tw.prepare_activations(a), out_dtype=out_dtype, x_layout="natural")
+    assert torch_equal(o_plan, o_nat)
+    out = tw.gemm_tew(a, tsm, ov)      # plan_for: row-run layout by default
+    ref, union = orc.tew_reference(a, tw.encode_cto(tsm), ov.col_ptr, ov.row_idx, ov.values, n)
+    assert np.array_equal(out.column_map.kept, union)
+    assert tw.relative_error(out.condensed, ref) <= TOL["fp32"]
+    assert tw.relative_error(o_plan.float().t(), ref) <= TOL[out_dtype]
