@@ -362,6 +362,7 @@ int tw_plan_create_cto(tw_plan** out, int32_t k, int32_t n, int32_t g, int32_t n
   // More than one copy (layers with > 6 tiles) measured no faster than the
   // gather on BERT 768x3072 (G = 3: 21.0 vs 20.9 us), so it is opt-in.
   const int max_copies = std::max(1, std::min(4, env_int("TW_RUN_COPIES", 1)));
+  const double run_stage_w = env_int("TW_RUN_STAGE_W", 8);
   if (row_runs && k < (1 << 20) && !env_int("TW_NO_RUNS", 0)) {
     const int stride = kp / kBK + 1;
     for (int G = (nt + 5) / 6; G <= max_copies && G <= nt; ++G) {
@@ -427,7 +428,7 @@ int tw_plan_create_cto(tw_plan** out, int32_t k, int32_t n, int32_t g, int32_t n
               }
               slot += len;
             }
-            cost[i] += 8.0 + (double)(bx.size() - nb0);  // per-stage cost: fixed + per box (best of 0/2/8/1000 measured)
+            cost[i] += run_stage_w + (double)(bx.size() - nb0);  // per-stage cost: fixed + per box
             ++stages;
           }
           for (int st = nst; st < stride; ++st) bf[(size_t)i * stride + st] = (int32_t)bx.size();
@@ -528,7 +529,8 @@ int tw_plan_create_cto(tw_plan** out, int32_t k, int32_t n, int32_t g, int32_t n
     double w = 0;
     for (int i = 0; i < plan->n_sub; ++i) {
       const SubTile& st = plan->subtiles[i];
-      wt[i] = plan->runs ? tile_cost[st.idx_row] + 3 * 16.0 : (double)st.kp_steps + 3.0;
+      wt[i] = plan->runs ? tile_cost[st.idx_row] + env_int("TW_RUN_FIX", 48)
+                         : (double)st.kp_steps + 3.0;
       w += wt[i];
     }
     std::vector<std::pair<double, int>> frac;
@@ -711,7 +713,12 @@ int tw_plan_attach_overlay(tw_plan* p, int32_t k, int32_t n, int64_t nnz, const 
                        (p->dtype == kBF16 ? float_to_bf16_bits(vals[e]) : float_to_half_bits(vals[e])));
         while (rv.size() % G) rv.push_back((uint32_t)k << 16);  // zero row, value 0
       }
-      rv.resize(rv.size() + 2 * G, (uint32_t)k << 16);  // the pipeline fetches two groups ahead
+      // A lane group keeps prefetching (two groups ahead) until the longest
+      // list of its warp is done, so the lists at the end need that much
+      // zero-row padding behind them.
+      int32_t max_len = 0;
+      for (size_t i = 0; i < ov_cols.size(); ++i) max_len = std::max(max_len, start[i + 1] - start[i]);
+      rv.resize(rv.size() + ((size_t)(max_len + G - 1) / G + 2) * G, (uint32_t)k << 16);
       if (int st = upload(&p->d_ov_rv, rv, s)) return st;
       if (int st = upload(&p->d_ov_meta, meta, s)) return st;
       if (p->runs) {

@@ -89,7 +89,7 @@ struct Cfg {
                                     kEpilogueWarps * kStgBytes + kBarrierBytes + kSubBytes +
                                     kIdxBytes + 1024;
   static_assert(kSmemBytes <= 227 * 1024, "shared memory budget");
-  static_assert(2 * kStages + kResSteps + 4 + 1 <= kBarrierBytes / 8, "barrier region");
+  static_assert(2 * kStages + kResSteps + 4 + 2 <= kBarrierBytes / 8, "barrier region");
 };
 
 // One unit of work: sub-tile d over tokens [ub, ue).
@@ -295,6 +295,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tempty = tfull + 2;
   uint64_t* pfull = tempty + 2;  // resident payload, one barrier per k-step
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pfull + kResSteps);
+  // completes once per kernel, when the last unit's accumulator is full: the
+  // gather warps then join that unit's epilogue (a parity wait on tfull could
+  // alias an earlier phase)
+  uint64_t* jbar = pfull + kResSteps + 1;
   SubTile* sub_smem = reinterpret_cast<SubTile*>(bar_region + C::kBarrierBytes);
   int32_t* sIdx = reinterpret_cast<int32_t*>(bar_region + C::kBarrierBytes + C::kSubBytes);
   long long* trace = args.trace ? args.trace + static_cast<int64_t>(blockIdx.x) * 4096 : nullptr;
@@ -332,6 +336,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&tempty[a], wide_epi ? kWideEpi : kEpilogueWarps);
     }
     for (int k = 0; k < kResSteps; ++k) mbar_init(&pfull[k], 1);
+    mbar_init(jbar, 1);
     fence_barrier_init();
     fence_proxy_async_smem();
   }
@@ -392,6 +397,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int nb1 = ks + 1 < sg.d.kp_steps ? __ldg(bf + ks + 2) : 0;
           const uint32_t e = b0 + lane < b1 ? __ldg(args.boxes + b0 + lane) : 0u;
           mbar_wait(&empty[stage], ((gs / kStages) & 1) ^ 1u);
+          if (trace && lane == 0 && gs < 1024) {
+            trace[gs] = clock64();
+            trace[3076] += b1 - b0;
+          }
           if (lane == 0) {
             mbar_arrive_expect_tx(&full[stage], (kRes ? 0u : static_cast<uint32_t>(kPBytes)) +
                                                     static_cast<uint32_t>(chunks * kBK * 128));
@@ -547,7 +556,31 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (units > 0) {
       const int j = units - 1;
       const int ew = kEpilogueWarps + (warp - kGatherWarp0);
-      mbar_wait(&tfull[j & 1], (j >> 1) & 1);
+      // released by the dedicated epilogue warps once the last accumulator
+      // is full (a parity wait on tfull could alias an earlier phase)
+      mbar_wait(jbar, 0);
+      tc_fence_after();
+      int sbuf = 0;
+      epilogue_unit(args, &map_out, last, tmem_base, j & 1, kTileN, warp & 3, lane, ew >> 2,
+                    kWideEpi / 4, sX + (ew - kEpilogueWarps) * kStgBytes, sbuf, true);
+      if (lane == 0) bulk_wait_all<0>();
+    }
+  } else if (warp >= kGatherWarp0 && warp < kEpilogueWarp0 && kRes && args.runs) {
+    // Run path with a resident payload: nothing to gather, but the dedicated
+    // epilogue warps still count on these warps for the last unit's token
+    // parts (see below), staged in the drained ring slots as on the cp.async
+    // path.
+    int units = 0;
+    Seg last;
+    while (walk.next(args, sg)) {
+      last = sg;
+      ++units;
+    }
+    grid_dependency_wait();  // the previous kernel may still read our output buffer
+    if (units > 0) {
+      const int j = units - 1;
+      const int ew = kEpilogueWarps + (warp - kGatherWarp0);
+      mbar_wait(jbar, 0);
       tc_fence_after();
       int sbuf = 0;
       epilogue_unit(args, &map_out, last, tmem_base, j & 1, kTileN, warp & 3, lane, ew >> 2,
@@ -620,6 +653,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       more = ahead.next(args, nxt);
       const int acc = j & 1;
       mbar_wait(&tfull[acc], (j >> 1) & 1);
+      // last unit of a non-wide epilogue: release the gather warps into it
+      if (!more && !wide_epi && ew == 0 && lane == 0) mbar_arrive(jbar);
       tc_fence_after();
       if (trace && warp == kEpilogueWarp0 && lane == 0 && j < 256) trace[2048 + 2 * j] = clock64();
       // the gather warps share the last unit of the cp.async path (and every

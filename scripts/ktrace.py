@@ -76,6 +76,21 @@ def main():
               f"first start -> last epilogue end {int(g1.max() - g0.min())} ns, "
               f"median CTA body {int(np.median(g1 - g0[:len(g1)]))} ns")
     print(" cta end (last epilogue) p10/50/90/max", q(ends))
+    # per-CTA summary: stages, boxes (run path), last full, end
+    rows = []
+    for c in range(148):
+        t0 = t[c, 3072]
+        if t0 == 0:
+            continue
+        ful = t[c, 1024:2048]
+        ns = int(np.count_nonzero(ful))
+        e = t[c, 2048:2048 + 512].reshape(-1, 2)
+        e = e[e[:, 0] > 0]
+        rows.append((c, ns, int(t[c, 3076]), int(ful[ns - 1] - t0) if ns else 0,
+                     int(e[-1, 1] - t0) if len(e) else 0, int(ful[0] - t0) if ns else 0))
+    print(" per-CTA cta:stages/boxes/first/lastfull/end")
+    for i in range(0, len(rows), 6):
+        print("  " + "  ".join(f"{c}:{ns}/{nb}/{f0}/{lf}/{en}" for c, ns, nb, lf, en, f0 in rows[i:i + 6]))
     print(" epilogue per segment p10/50/90/max", q(epi))
 
 

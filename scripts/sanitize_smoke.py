@@ -3,7 +3,10 @@
     compute-sanitizer --tool memcheck|racecheck|synccheck python scripts/sanitize_smoke.py
 
 Covers the resident (K' <= 448) and streamed K1 kernels in owner and strided
-modes, ragged M / widths, 16-bit and fp32 outputs, K2 and both K4 paths.
+modes, ragged M / widths, 16-bit and fp32 outputs, K2 and both K4 paths, and
+the row-run layout: streamed and resident payload with 3-4 units per CTA (the
+last unit's epilogue joined by the idle gather warps), grouped copies, and the
+cp.async gather by layout position.
 """
 import os
 import sys
@@ -17,9 +20,10 @@ import paper_2402_10876_b200 as tw  # noqa: E402
 
 
 def main():
+    only = sys.argv[1] if len(sys.argv) > 1 else "all"   # all | small | runs | gather
     rng = np.random.default_rng(0)
-    for (k, n, m, s, g) in [(256, 384, 300, 0.75, 128), (1024, 512, 200, 0.5, 128),
-                            (96, 80, 37, 0.3, 16)]:
+    for (k, n, m, s, g) in ([] if only in ("runs", "gather") else [(256, 384, 300, 0.75, 128), (1024, 512, 200, 0.5, 128),
+                            (96, 80, 37, 0.3, 16)]):
         w = tw.round_to(rng.standard_normal((k, n)).astype(np.float32), "fp16")
         a = tw.round_to(rng.standard_normal((m, k)).astype(np.float32), "fp16")
         _, tsm = tw.prune_tw(w, s, g)
@@ -31,6 +35,24 @@ def main():
         _, ttsm, ov = tw.prune_tew(w, s, 0.02, g)
         tw.gemm_tew(a, ttsm, ov, out_dtype="fp16")
         tw.prepare_activations(torch.from_numpy(a).cuda().half())
+    # row-run layout, several units per CTA
+    cases = [(768, 768, 16384, {}), (768, 3072, 8192, {"TW_RUN_COPIES": "3"}),
+             (768, 768, 16384, {"TW_RUN_MAX_UNITS": "0"})]
+    if only == "runs":
+        cases = cases[:2]
+    elif only == "gather":
+        cases = cases[2:]
+    elif only == "small":
+        cases = []
+    for (k, n, m, env) in cases:
+        os.environ.update(env)
+        w = tw.round_to(rng.standard_normal((k, n)).astype(np.float32), "fp16")
+        a = tw.round_to(rng.standard_normal((m, k)).astype(np.float32), "fp16")
+        _, tsm = tw.prune_tw(w, 0.75, 128)
+        plan = tw.TwPlan(tw.encode_cto(tsm), row_layout="runs")
+        plan.run(plan.prepare(a), out_dtype="fp16")
+        for key in env:
+            del os.environ[key]
     torch.cuda.synchronize()
     print("sanitize smoke done")
 

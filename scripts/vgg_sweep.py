@@ -84,10 +84,16 @@ def run(layers, sparsities, gs, reps_for=lambda m: 20 if m < 1_000_000 else 5):
                 x = plan.prepare(at=at) if plan.uses_row_runs else at   # plan row order
                 out = torch.empty((tsm.n_condensed, m), device="cuda", dtype=torch.float16)
                 us = time_graph(lambda: plan.run(x, out=out), reps)
+                # the row-run path must equal the natural-order gather bit for bit
+                same = None
+                if plan.uses_row_runs:
+                    nat = plan.run(at, out_dtype="fp16", x_layout="natural")
+                    same = bool(torch.equal(out, nat))
+                    del nat
                 flops = tw.sparse_flops(tsm, m)
                 rows.append({"layer": name, "M": m, "K": k, "N": n, "s": s, "g": g,
                              "n_tiles": len(tsm.tiles), "n_condensed": int(tsm.n_condensed),
-                             "row_runs": bool(plan.uses_row_runs),
+                             "row_runs": bool(plan.uses_row_runs), "runs_bit_identical": same,
                              "kept_rows_min": min(t.kept_rows.n_kept for t in tsm.tiles),
                              "us": us, "us_cublas": us_dense, "speedup": us_dense / us,
                              "tflops_effective": flops / (us * 1e-6) / 1e12,
@@ -112,6 +118,9 @@ def main():
     text = json.dumps(doc, indent=1)
     if args.out:
         Path(args.out).write_text(text)
+    bad = [r for r in rows if r["runs_bit_identical"] is False]
+    if bad:
+        print(f"ERROR: {len(bad)} points differ between the run path and the gather")
     for r in rows:
         print(f"{r['layer']:8s} s={r['s']:.1f} g={r['g']:3d} tiles={r['n_tiles']:2d} "
               f"K'min={r['kept_rows_min']:4d} {r['us']:9.1f} us  cuBLAS {r['us_cublas']:9.1f} us  "

@@ -269,6 +269,8 @@ def test_transpose_cast_exact(m, k, src, dst):
     (4608, 512, 900, 0.9, 256, {}),                       # one wide tile (VGG conv4 shape)
     (1024, 512, 300, 0.5, 256, {}),                       # g = 256: 2 sub-tiles per tile
     (768, 3072, 1000, 0.75, 128, {"TW_RUN_COPIES": "3"}), # 12 tiles: one order per tile group
+    (768, 3072, 8192, 0.75, 128, {"TW_RUN_COPIES": "3"}), # resident payload + runs, 3 units per CTA
+    (768, 768, 16384, 0.75, 128, {}),                     # resident payload + runs, 4 units per CTA
 ])
 def test_row_runs_layout_bit_identical(k, n, m, s, g, env, monkeypatch):
     """Plans with the row-run layout: activations prepared into the permuted
