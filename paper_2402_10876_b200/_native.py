@@ -8,6 +8,7 @@ raises :class:`DeviceError`.
 from __future__ import annotations
 
 import ctypes
+import os
 import threading
 from pathlib import Path
 
@@ -66,8 +67,10 @@ _lib = None
 
 
 def load_library(path: Path = LIB_PATH) -> ctypes.CDLL:
-    """Load (once) and type the C ABI.  Does not touch the GPU."""
+    """Load (once) and type the C ABI.  Does not touch the GPU.
+    ``TW_LIB_PATH`` (diagnostics: A/B builds of the same ABI) overrides the path."""
     global _lib
+    path = Path(os.environ.get("TW_LIB_PATH", str(path)))
     with _lock:
         if _lib is not None:
             return _lib
