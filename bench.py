@@ -63,6 +63,11 @@ CONFIGS = {
     "bert_tew": {"layers": BERT_LAYERS, "m": 8192, "s": 0.75, "g": 128, "delta": 0.015,
                  "workload": "BERT-base TEW: TW 75% + 1.5% element overlay, G=128, "
                              "M=8192 (configs[2])"},
+    "bert_tvw": {"layers": BERT_LAYERS, "m": 8192, "s": 0.75, "g": 128, "delta": 0.0,
+                 "pattern": "tvw",
+                 "workload": "BERT-base TVW: TW at 50% then 2:4 down every payload column "
+                             "(75% total), G=128, M=8192 (SURVEY 8f1; dense UMMA over the "
+                             "2:4 payload)"},
     "cfg1": {"layers": [(1024, 1024)], "m": 128, "s": 0.75, "g": 128, "delta": 0.0,
              "workload": "single 1024x1024 weight, TW 75% G=128, M=128 (configs[0])"},
     "big": {"layers": [(16384, 16384)], "m": 8192, "s": 0.75, "g": 128, "delta": 0.0,
@@ -154,6 +159,9 @@ def build_layers(cfg: dict):
         w = tw.round_to(tw.synthetic_matrix(0, k, n, tw.STREAM_WEIGHTS), "fp16")
         if cfg["delta"] > 0:
             plan, tsm, ov = tw.prune_tew(w, cfg["s"], cfg["delta"], cfg["g"])
+        elif cfg.get("pattern") == "tvw":
+            plan, tsm, _ = tw.prune_tvw(w, cfg["s"], cfg["g"])
+            ov = None
         else:
             plan, tsm = tw.prune_tw(w, cfg["s"], cfg["g"])
             ov = None
