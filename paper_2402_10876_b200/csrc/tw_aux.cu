@@ -202,7 +202,8 @@ __global__ void __launch_bounds__(kResThreads, 1)
     // loop has no branches.
     const uint32_t* lp = args.rv + m.x + tl;
     uint32_t c = __ldg(lp), n1 = __ldg(lp + L);
-    for (int eo = 0; eo < maxlen; eo += G) {
+    int eo = 0;
+    for (; eo + G <= maxlen; eo += G) {
       const uint32_t f = __ldg(lp + 2 * L);
       lp += L;
       if (eo >= m.y) c = zrow;
@@ -214,6 +215,18 @@ __global__ void __launch_bounds__(kResThreads, 1)
       }
       c = n1;
       n1 = f;
+    }
+    // the warp's last, partial group stops at its longest list (warp-uniform
+    // count): the padding entries past it are not computed
+    if (eo < maxlen) {
+      if (eo >= m.y) c = zrow;
+      const int cnt = maxlen - eo;
+#pragma unroll 1
+      for (int j = 0; j < cnt; ++j) {
+        const uint32_t q = L == 1 ? c : __shfl_sync(0xffffffffu, c, gbase + j);
+        fma8<kBf>(ac, *reinterpret_cast<const uint4*>(sAb + (q >> 16) * (T * 2)),
+                  static_cast<uint16_t>(q & 0xFFFFu));
+      }
     }
     if (live) {
       if (vec) {
