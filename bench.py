@@ -240,6 +240,17 @@ def run_reference_arm(args, cfg, rank: int, world: int) -> None:
 # our arm
 # ----------------------------------------------------------------------------
 
+def ncu_traffic(config: str):
+    """DRAM bytes per step of the product kernels, from the committed ncu
+    launch lists (profiles/ncu_traffic.json, scripts/ncu_traffic.sh); None
+    when not captured for this config."""
+    tfile = ROOT / "profiles" / "ncu_traffic.json"
+    try:
+        return json.loads(tfile.read_text()).get(config)
+    except (ValueError, OSError):
+        return None
+
+
 def capture_graph(fn):
     """CUDA graph of fn() (eager warm-up first, captured on a side stream)."""
     import torch
@@ -496,13 +507,7 @@ def run_ours(args, cfg, rank: int, world: int) -> None:
     achieved_gbs = tot_bytes / (tot_us * 1e-6) / 1e9
     ai = flops_step / tot_bytes
     ridge = pk["tc"] * 1e12 / (pk["hbm"] * 1e9)
-    traffic = None
-    tfile = ROOT / "profiles" / "ncu_traffic.json"
-    if tfile.exists():
-        try:
-            traffic = json.loads(tfile.read_text()).get(args.config)
-        except (ValueError, OSError):
-            traffic = None
+    traffic = ncu_traffic(args.config)
     if ai < ridge:
         roofline = {"bound": "hbm", "achieved": achieved_gbs, "peak": pk["hbm"], "unit": "GB/s",
                     "frac": achieved_gbs / pk["hbm"], "traffic": traffic}
@@ -657,7 +662,9 @@ def run_big(args, cfg, rank: int, world: int) -> None:
     pk = peaks()
     tf_k1 = flops_local / (ms_k1 * 1e-3) / 1e12
     roofline = {"bound": "tensor", "achieved": tf_k1, "peak": pk["tc"], "unit": "TFLOP/s",
-                "frac": tf_k1 / pk["tc"], "traffic": None, "kernel": "tw_gemm_kernel",
+                "frac": tf_k1 / pk["tc"],
+                "traffic": ncu_traffic(args.config) if world == 1 else None,
+                "kernel": "tw_gemm_kernel",
                 "peak_source": pk["source"],
                 "arithmetic_intensity": flops_total / tw.algorithmic_bytes(tsm, m),
                 "k1_ms": ms_k1, "allgather_ms": ms_ag}
