@@ -48,8 +48,9 @@ __device__ __forceinline__ void store_from_float(void* p, int32_t dtype, int64_t
 // their columns independently: a lane group of L = T / 8 lanes per column
 // (8 tokens per lane, one 16-byte shared load per entry), 32 / L columns per
 // warp step, columns in descending-nnz order (host) so the groups of a warp
-// finish together.  Each lane group fetches 2 L packed entries (row << 16 |
-// 16-bit value, rounded like the TW payload) per 8-byte load, two groups
+// finish together.  Each lane group fetches L packed entries (16-bit value,
+// rounded like the TW payload, << 16 | the row's offset in the staged block in
+// 16-byte units) per 4-byte load per lane, two groups
 // ahead, and broadcasts them with shuffles; one fma.rn.f32.f16 (FHFMA: 16-bit
 // operands, fp32 accumulator, no conversions) per token, fp32 accumulation in ascending row order (CSC order of
 // patterns.py:145-214), then one read-modify-write of the TW result
@@ -170,7 +171,8 @@ __global__ void __launch_bounds__(kResThreads, 1)
   // prefetched one step ahead.
   constexpr int kStep = kCols * kResWarps;
   constexpr int G = L;  // entries per group (1 per lane, one 4-byte load)
-  const uint32_t zrow = static_cast<uint32_t>(K) << 16;
+  // entries: 16-bit value << 16 | row offset in 16-byte units (row * L)
+  const uint32_t zrow = static_cast<uint32_t>(K) * L;
   const uint8_t* sAb = reinterpret_cast<const uint8_t*>(sAt);
   const bool fast = args.out_dtype != kF32 && args.ld_out % 8 == 0;
   int cs = c0 + warp * kCols;
@@ -210,8 +212,9 @@ __global__ void __launch_bounds__(kResThreads, 1)
 #pragma unroll
       for (int j = 0; j < G; ++j) {
         const uint32_t q = L == 1 ? c : __shfl_sync(0xffffffffu, c, gbase + j);
-        fma8<kBf>(ac, *reinterpret_cast<const uint4*>(sAb + (q >> 16) * (T * 2)),
-                  static_cast<uint16_t>(q & 0xFFFFu));
+        // PRMT (zero-extended low half) + LEA: two instructions per address
+        fma8<kBf>(ac, *reinterpret_cast<const uint4*>(sAb + __byte_perm(q, 0u, 0x4410) * 16u),
+                  static_cast<uint16_t>(q >> 16));
       }
       c = n1;
       n1 = f;
@@ -224,8 +227,9 @@ __global__ void __launch_bounds__(kResThreads, 1)
 #pragma unroll 1
       for (int j = 0; j < cnt; ++j) {
         const uint32_t q = L == 1 ? c : __shfl_sync(0xffffffffu, c, gbase + j);
-        fma8<kBf>(ac, *reinterpret_cast<const uint4*>(sAb + (q >> 16) * (T * 2)),
-                  static_cast<uint16_t>(q & 0xFFFFu));
+        // PRMT (zero-extended low half) + LEA: two instructions per address
+        fma8<kBf>(ac, *reinterpret_cast<const uint4*>(sAb + __byte_perm(q, 0u, 0x4410) * 16u),
+                  static_cast<uint16_t>(q >> 16));
       }
     }
     if (live) {

@@ -719,12 +719,19 @@ int tw_plan_attach_overlay(tw_plan* p, int32_t k, int32_t n, int64_t nnz, const 
       int32_t max_len = 0;
       for (size_t i = 0; i < ov_cols.size(); ++i) max_len = std::max(max_len, start[i + 1] - start[i]);
       rv.resize(rv.size() + ((size_t)(max_len + G - 1) / G + 2) * G, (uint32_t)k << 16);
-      if (int st = upload(&p->d_ov_rv, rv, s)) return st;
+      // device form: value << 16 | row offset in 16-byte units of the staged
+      // block (row * T * 2 / 16 = row * G < 2^16 since the block is <= 200 KB),
+      // so K2 forms the shared-memory address with one mask and one shift-add
+      auto device_form = [G](std::vector<uint32_t> v) {
+        for (uint32_t& x : v) x = ((x & 0xffffu) << 16) | ((x >> 16) * (uint32_t)G);
+        return v;
+      };
+      if (int st = upload(&p->d_ov_rv, device_form(rv), s)) return st;
       if (int st = upload(&p->d_ov_meta, meta, s)) return st;
       if (p->runs) {
         for (uint32_t& x : rv)  // zero row k stays k (the staged block's appended row)
           if ((int32_t)(x >> 16) < k) x = ((uint32_t)p->inv[x >> 16] << 16) | (x & 0xffffu);
-        if (int st = upload(&p->d_ov_rv_pos, rv, s)) return st;
+        if (int st = upload(&p->d_ov_rv_pos, device_form(rv), s)) return st;
       }
     }
   }

@@ -105,7 +105,7 @@ struct ResidualArgs {
   const int32_t* col_start; // [n_cols + 1] CSC pointers (columns in descending-nnz order)
   const int32_t* rows;      // [nnz] K rows            (direct kernel)
   const float* vals;        // [nnz]                   (direct kernel)
-  const uint32_t* rv;       // [nnz] row << 16 | 16-bit value; nullptr = direct kernel
+  const uint32_t* rv;       // [nnz] 16-bit value << 16 | row * T / 8 (16-byte units); nullptr = direct kernel
   const int32_t* out_rows;  // [n_cols] output row (union position)
   const int32_t* accumulate;// [n_cols] 1 = add onto TW result, 0 = overwrite
   const int4* meta;         // [n_cols] {first entry, entries, out row, source row + 1 (0: none)}
