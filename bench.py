@@ -187,6 +187,17 @@ def activations(cfg: dict, k: int, li: int, rank: int):
 # reference arm / CPU baseline: the reference algorithm on host cores
 # ----------------------------------------------------------------------------
 
+def cpu_model() -> str:
+    """Host CPU model name (for the cpu_baseline record)."""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_reference_rate(cfg: dict, layers, m_sample: int, reps: int = 1):
     """Time the oracle port of execute_batched (+ gemm_tew overlay) on an
     M-slice; returns (TFLOP/s, seconds, flops, workers)."""
@@ -228,7 +239,7 @@ def run_reference_arm(args, cfg, rank: int, world: int) -> None:
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (Philox seed 0, fp16-rounded)",
         "config": {"workload": cfg["workload"], "parallelism": "cpu", "m_sample": m_sample},
-        "cpu_baseline": {"value": rate, "unit": "TFLOP/s", "cores": workers, "kind": "port",
+        "cpu_baseline": {"cpu_model": cpu_model(), "value": rate, "unit": "TFLOP/s", "cores": workers, "kind": "port",
                          "sample": sample},
         "e2e": {"value": rate, "unit": "TFLOP/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
@@ -548,7 +559,7 @@ def run_ours(args, cfg, rank: int, world: int) -> None:
                         "(K1) -> D2H of the fp16 C'^T; layers pipelined over H2D / compute / "
                         "D2H streams"},
         "roofline": roofline,
-        "cpu_baseline": {"value": cpu_rate, "unit": "TFLOP/s", "cores": workers, "kind": "port",
+        "cpu_baseline": {"cpu_model": cpu_model(), "value": cpu_rate, "unit": "TFLOP/s", "cores": workers, "kind": "port",
                          "sample": f"{m_sample} of {m} tokens through every layer "
                                    f"({cpu_s:.1f} s, oracle port of execute_batched lpt)"},
         "gpu_launches": args.steps * len(layers) * (2 if tew else 1),
@@ -693,7 +704,7 @@ def run_big(args, cfg, rank: int, world: int) -> None:
                 "d2h_bytes_per_step": c_pin.numel() * 2,
                 "path": "pinned host fp16 A -> H2D -> K4 -> K1 -> all-gather -> D2H"},
         "roofline": roofline,
-        "cpu_baseline": {"value": cpu_rate, "unit": "TFLOP/s", "cores": os.cpu_count() or 1,
+        "cpu_baseline": {"cpu_model": cpu_model(), "value": cpu_rate, "unit": "TFLOP/s", "cores": os.cpu_count() or 1,
                          "kind": "port", "sample": f"tile 0 (K'={t.kept_rows.n_kept}) x 64 tokens "
                                                    f"({cpu_s:.1f} s, one lane: one tile)"},
         "gpu_launches": args.steps,
