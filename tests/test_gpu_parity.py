@@ -122,6 +122,22 @@ def test_tew_matches_oracle():
     assert tw.relative_error(out.expand(), dense) <= TOL["fp32"]
 
 
+@pytest.mark.parametrize("k,compute", [(4608, "fp16"), (4608, "bf16"), (3072, "bf16")])
+def test_tew_block_sizes_match_oracle(k, compute):
+    """K2 with the 16- and 32-token staged blocks (K > 1536 rows) and the
+    bf16 kernel: every packed entry's block offset (row * T / 8) stays in 16
+    bits up to the largest block, and the result matches the oracle."""
+    rng = np.random.default_rng(k)
+    n, m = 256, 203
+    w = tw.round_to(rng.normal(size=(k, n)).astype(np.float32), compute)
+    a = tw.round_to(rng.normal(size=(m, k)).astype(np.float32), compute)
+    _, tsm, ov = tw.prune_tew(w, 0.75, 0.02, 128)
+    out = tw.gemm_tew(a, tsm, ov, compute_dtype=compute)
+    ref, union = orc.tew_reference(a, tw.encode_cto(tsm), ov.col_ptr, ov.row_idx, ov.values, n)
+    assert np.array_equal(out.column_map.kept, union)
+    assert tw.relative_error(out.condensed, ref) <= TOL["fp32"]
+
+
 def test_tew_bert_golden_rows():
     z, meta = load_npz("bert.npz")
     for li, info in enumerate(meta):
