@@ -365,3 +365,32 @@ def test_tew_row_runs_layout_bit_identical(k, n, m, out_dtype, env, monkeypatch)
     assert np.array_equal(out.column_map.kept, union)
     assert tw.relative_error(out.condensed, ref) <= TOL["fp32"]
     assert tw.relative_error(o_plan.float().t(), ref) <= TOL[out_dtype]
+
+
+def test_big_layer_full_size():
+    """configs[4] at its full size (16384 x 16384 weight, TW 75 %, G = 128,
+    M = 8192; 64 tiles, streamed payload, strided units): the launch is
+    deterministic, 64 sampled tokens of the fp32 output match the oracle
+    (fp64, reference accumulation order) and the fp16 output is the fp32 one
+    rounded."""
+    import torch
+
+    k = n = 16384
+    m = 8192
+    w = tw.round_to(tw.synthetic_matrix(0, k, n, tw.STREAM_WEIGHTS), "fp16")
+    _, tsm = tw.prune_tw(w, 0.75, 128)
+    del w
+    assert len(tsm.tiles) == 64 and tsm.n_condensed == 8192
+    enc = tw.encode_cto(tsm)
+    a = tw.round_to(tw.synthetic_matrix(0, m, k, tw.STREAM_INPUT), "fp16")
+    plan = tw.TwPlan(enc)
+    at = plan.prepare(torch.from_numpy(a).cuda())
+    c1 = plan.run(at)
+    c2 = plan.run(at)
+    assert torch.equal(c1, c2)
+    h = plan.run(at, out_dtype="fp16")
+    assert torch.equal(h, c1.half())
+    idx = np.sort(np.random.default_rng(4).choice(m, 64, replace=False))
+    ref = orc.c_gemm_cto_enc(np.ascontiguousarray(a[idx]), enc)
+    got = c1[:, torch.from_numpy(idx).cuda()].t().cpu().numpy()
+    assert tw.relative_error(got, ref) <= TOL["fp32"]
