@@ -198,12 +198,13 @@ def cpu_model() -> str:
     return "unknown"
 
 
-def cpu_reference_rate(cfg: dict, layers, m_sample: int, reps: int = 1):
+def cpu_reference_rate(cfg: dict, layers, m_sample: int, reps: int = 1, workers: int = 0):
     """Time the oracle port of execute_batched (+ gemm_tew overlay) on an
-    M-slice; returns (TFLOP/s, seconds, flops, workers)."""
+    M-slice with `workers` lanes (0: every host core); returns (TFLOP/s,
+    seconds, flops, workers)."""
     from oracle import tilesparse_oracle as orc
 
-    workers = os.cpu_count() or 1
+    workers = workers or os.cpu_count() or 1
     total_s, total_f = 0.0, 0
     for _ in range(reps):
         for li, L in enumerate(layers):
@@ -533,6 +534,8 @@ def run_ours(args, cfg, rank: int, world: int) -> None:
     # CPU baseline: the reference algorithm on this host, bounded sample
     m_sample = min(m, 1024)
     cpu_rate, cpu_s, _, workers = cpu_reference_rate(cfg, layers, m_sample)
+    # the single-lane figure (W = 1, as cmd_bench's default) on a quarter sample
+    cpu1_rate, cpu1_s, _, _ = cpu_reference_rate(cfg, layers, max(64, m_sample // 4), workers=1)
     clocks = clk.summary()
     line = {
         "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
@@ -561,7 +564,9 @@ def run_ours(args, cfg, rank: int, world: int) -> None:
         "roofline": roofline,
         "cpu_baseline": {"cpu_model": cpu_model(), "value": cpu_rate, "unit": "TFLOP/s", "cores": workers, "kind": "port",
                          "sample": f"{m_sample} of {m} tokens through every layer "
-                                   f"({cpu_s:.1f} s, oracle port of execute_batched lpt)"},
+                                   f"({cpu_s:.1f} s, oracle port of execute_batched lpt)",
+                         "value_1_worker": cpu1_rate,
+                         "sample_1_worker": f"{max(64, m_sample // 4)} tokens, 1 lane ({cpu1_s:.1f} s)"},
         "gpu_launches": args.steps * len(layers) * (2 if tew else 1),
         "launch": "CUDA graph per step (one graph per rotating buffer set)",
         "clocks": clocks,
