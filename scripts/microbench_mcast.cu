@@ -51,6 +51,23 @@ __device__ __forceinline__ void tma_load_2d_mc(void* dst, const CUtensorMap* map
 
 // mode 0: unicast (each CTA loads its full stage: 4 boxes of {64 tok, 64 rows})
 // mode 1: multicast (CTA r loads boxes r, r + csz, ... and multicasts them)
+// spin on test_wait (no suspend hint): a remote (cluster) arrival may not
+// wake a thread suspended in try_wait promptly
+__device__ __forceinline__ void mbar_spin(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tSPIN_%=:\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra SPIN_%=;\n\t}" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_remote_relaxed(uint64_t* bar, uint32_t rank) {
+  asm volatile(
+      "{\n .reg .b32 ra;\n mapa.shared::cluster.u32 ra, %0, %1;\n"
+      " mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [ra];\n}" ::"r"(smem_u32(bar)),
+      "r"(rank)
+      : "memory");
+}
+
 __global__ void ring(const __grid_constant__ CUtensorMap map, int M, int K, int iters, int csz,
                      int mode, long long* cycles, int share) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -62,7 +79,7 @@ __global__ void ring(const __grid_constant__ CUtensorMap map, int M, int K, int 
   if (tid == 0) {
     for (int s = 0; s < kSt; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], mode == 1 ? csz : 1);
+      mbar_init(&empty[s], (mode == 1 || mode == 3) ? csz : 1);  // mode 2: multicast, local release only (raw delivery rate; racy by design)
     }
     fence_barrier_init();
   }
@@ -71,7 +88,10 @@ __global__ void ring(const __grid_constant__ CUtensorMap map, int M, int K, int 
   if (tid == 0) {
     for (int it = 0; it < iters; ++it) {
       const int stage = it % kSt;
-      if (it >= kSt) mbar_wait(&empty[stage], ((it / kSt) - 1) & 1);
+      if (it >= kSt) {
+        if (mode == 3) mbar_spin(&empty[stage], ((it / kSt) - 1) & 1);
+        else mbar_wait(&empty[stage], ((it / kSt) - 1) & 1);
+      }
       mbar_arrive_expect_tx(&full[stage], kStage);
       // same tile for the whole cluster (that is what multicast shares)
       int kb = ((it + cluster_id * 7) * 64) % (K - 64);
@@ -92,8 +112,12 @@ __global__ void ring(const __grid_constant__ CUtensorMap map, int M, int K, int 
     for (int it = 0; it < iters; ++it) {
       const int stage = it % kSt;
       mbar_wait(&full[stage], (it / kSt) & 1);
-      if (mode == 1) {
+      if (mode == 3) {
+        for (int r = 0; r < csz; ++r) mbar_arrive_remote_relaxed(&empty[stage], r);
+      } else if (mode == 1) {
         for (int r = 0; r < csz; ++r) mbar_arrive_remote(&empty[stage], r);
+      } else if (mode == 2) {
+        mbar_arrive(&empty[stage]);
       } else {
         mbar_arrive(&empty[stage]);
       }
@@ -132,8 +156,8 @@ int main() {
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   for (int share : {1, -1, -2}) for (int csz : {1, 2, 4}) {
-    for (int mode : {0, 1}) {
-      if (mode == 1 && csz == 1) continue;
+    for (int mode : {0, 1, 2, 3}) {
+      if (mode >= 1 && csz == 1) continue;
       if (share > 1 && mode == 1) continue;
       const int grid = 148 / csz * csz;
       cudaLaunchConfig_t cfg{};
@@ -160,7 +184,7 @@ int main() {
       std::sort(c.begin(), c.end());
       const double bytes = (double)grid * iters * kStage;  // bytes landed in smem
       printf("share %2d cluster %d %-10s grid %3d  %8.1f GB/s landed  %6.1f B/cyc/SM landed (median)\n",
-             share, csz, mode ? "multicast" : "unicast", grid, bytes / ms / 1e6,
+             share, csz, mode == 3 ? "mc-relax+spin" : mode == 2 ? "mc-local" : mode ? "multicast" : "unicast", grid, bytes / ms / 1e6,
              (double)iters * kStage / c[grid / 2]);
       (void)share;
     }
