@@ -704,11 +704,41 @@ int tw_plan_attach_overlay(tw_plan* p, int32_t k, int32_t n, int64_t nnz, const 
       const int G = T / 8;
       std::vector<uint32_t> rv;
       std::vector<int4> meta(ov_cols.size());
+      // Shared-memory bank classes: a staged row is T * 2 bytes, so
+      // C = 64 / T rows share one 128-byte line and row r sits in class
+      // r % C of it.  The kCols columns of a warp step read entry j of their
+      // lists in one 16-byte load each; entries of random rows pile onto
+      // some classes (30 % extra wavefronts measured at T = 32).  So each
+      // column's list is interleaved by class (the row order within a class
+      // kept), starting at class (column % kCols) % C: entry j of a warp step
+      // then covers the classes evenly.  Classes follow the row the kernel
+      // reads (layout position on row-run plans); the natural-order list uses
+      // the same entry order, so both paths stay bit-identical.
+      const int C = std::max(1, 64 / T), kCols = 256 / T;
+      std::vector<int32_t> order;
+      std::vector<std::vector<int32_t>> cls(C);
       for (size_t i = 0; i < ov_cols.size(); ++i) {
         const int32_t n = start[i + 1] - start[i];
         // w: condensed source row + 1 of a TW-kept column (0: residual only)
         meta[i] = make_int4((int32_t)rv.size(), n, out_rows[i], src_cond[i] + 1);
-        for (int32_t e = start[i]; e < start[i + 1]; ++e)
+        order.clear();
+        if (C > 1) {
+          for (auto& q : cls) q.clear();
+          for (int32_t e = start[i]; e < start[i + 1]; ++e) {
+            const int32_t r = p->runs ? p->inv[rows[e]] : rows[e];
+            cls[r % C].push_back(e);
+          }
+          std::vector<size_t> head(C, 0);
+          int c = (int)(i % (size_t)kCols) % C;
+          for (int32_t t = 0; t < n; ++t) {
+            while (head[c] >= cls[c].size()) c = (c + 1) % C;
+            order.push_back(cls[c][head[c]++]);
+            c = (c + 1) % C;
+          }
+        } else {
+          for (int32_t e = start[i]; e < start[i + 1]; ++e) order.push_back(e);
+        }
+        for (int32_t e : order)
           rv.push_back(((uint32_t)rows[e] << 16) |
                        (p->dtype == kBF16 ? float_to_bf16_bits(vals[e]) : float_to_half_bits(vals[e])));
         while (rv.size() % G) rv.push_back((uint32_t)k << 16);  // zero row, value 0
