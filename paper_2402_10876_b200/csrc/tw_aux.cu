@@ -52,8 +52,9 @@ __device__ __forceinline__ void store_from_float(void* p, int32_t dtype, int64_t
 // rounded like the TW payload, << 16 | the row's offset in the staged block in
 // 16-byte units) per 4-byte load per lane, two groups
 // ahead, and broadcasts them with shuffles; one fma.rn.f32.f16 (FHFMA: 16-bit
-// operands, fp32 accumulator, no conversions) per token, fp32 accumulation in ascending row order (CSC order of
-// patterns.py:145-214), then one read-modify-write of the TW result
+// operands, fp32 accumulator, no conversions) per token, fp32 accumulation in
+// the list order (the CSC rows of patterns.py:145-214, interleaved by bank
+// class on the host, tw_capi.cu), then one read-modify-write of the TW result
 // (accumulate = 1) or a plain store (residual-only column).
 constexpr int kResThreads = 1024;  // 32 warps: one CTA per SM, 64 registers per thread
 constexpr int kResWarps = kResThreads / 32;
