@@ -154,6 +154,9 @@ __global__ void __launch_bounds__(kResThreads, 1)
   const int ntok = rem < T ? static_cast<int>(rem) : T;
   // this CTA's columns: split y of the descending-nnz order (by nnz)
   const int c0 = args.group_first[blockIdx.y], c1 = args.group_first[blockIdx.y + 1];
+  // launched with programmatic dependent launch after K1: the TW result (and,
+  // in a chain, A^T) is complete and visible only after this wait
+  grid_dependency_wait();
   {
     constexpr int per_row = T / 8;
     // row K stays zero: padding entries (row K, value 0) add exactly 0
@@ -167,6 +170,8 @@ __global__ void __launch_bounds__(kResThreads, 1)
     cp_async_wait<0>();
     __syncthreads();
   }
+  // the next kernel may launch; it waits for this grid before touching data
+  grid_launch_dependents();
   const uint16_t* sAt = sA + tok;
   // One column per lane group per step; the next step's metadata is
   // prefetched one step ahead.
@@ -385,9 +390,19 @@ static cudaError_t launch_res_t(const ResidualArgs& args, cudaStream_t stream) {
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
-  dim3 grid(static_cast<unsigned>(args.n_blocks), static_cast<unsigned>(args.n_groups));
-  tw_residual_kernel<T, kBf><<<grid, kResThreads, smem, stream>>>(args);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(args.n_blocks), static_cast<unsigned>(args.n_groups));
+  cfg.blockDim = dim3(kResThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  // programmatic dependent launch: K2's CTAs start as K1's leave (the
+  // kernel waits with griddepcontrol.wait before reading anything)
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, tw_residual_kernel<T, kBf>, args);
 }
 
 template <int T>
