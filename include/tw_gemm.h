@@ -167,6 +167,23 @@ TW_API int tw_gemm_tew_ex(const tw_plan* plan, const void* at, int64_t m, int64_
                           void* ct, int64_t ld_ct, int32_t out_dtype, void* workspace,
                           uint64_t ws_bytes, int32_t x_layout, void* stream);
 
+/* TEW product on a tile product the caller already holds (K2 only; the TW
+ * GEMM is not run again).  Replaces the tile_output path of executor.gemm_tew
+ * (executor.py:180-203, `tile_out = tile_output if ... else ...` at line 194):
+ * the tile product is expanded to the original columns, the overlay added and
+ * the result re-condensed to the union columns.
+ *   tile_ct (ld_tile): the tile product as C^T rows (one row per column of the
+ *     caller's GemmOutput.column_map, tokens contiguous), in out_dtype.
+ *   tile_row_of_union: host array [n_union]: row of tile_ct holding union
+ *     column u, or -1 (that column starts from zero).  NULL means tile_ct rows
+ *     are this plan's condensed columns (tw_plan_condensed_columns order).
+ * With NULL the call is stream-ordered and graph-capturable; with a map it
+ * uploads the map and synchronises `stream` once. */
+TW_API int tw_gemm_tew_reuse(const tw_plan* plan, const void* at, int64_t m, int64_t ld_at,
+                             const void* tile_ct, int64_t ld_tile,
+                             const int32_t* tile_row_of_union, void* ct, int64_t ld_ct,
+                             int32_t out_dtype, int32_t at_layout, void* stream);
+
 /* A (m x k row-major, pitch lda, a_dtype) -> A^T (k x m, pitch ld_at, at_dtype).
  * Replaces the float32/float64 carrier copies of core.as_matrix
  * (core.py:32-43) and executor.py:158 on the device; the per-tile column

@@ -54,6 +54,8 @@ SIGNATURES = {
     "tw_gemm_tew_ws": (_c_int, [_vp, _vp, _i64, _i64, _vp, _i64, _i32, _vp, ctypes.c_uint64, _vp]),
     "tw_gemm_tew_ex": (_c_int, [_vp, _vp, _i64, _i64, _vp, _i64, _i32, _vp, ctypes.c_uint64, _i32,
                                 _vp]),
+    "tw_gemm_tew_reuse": (_c_int, [_vp, _vp, _i64, _i64, _vp, _i64, _i32p, _vp, _i64, _i32, _i32,
+                                   _vp]),
     "tw_plan_tew_workspace_bytes": (_c_int, [_vp, _i64, _i32, ctypes.POINTER(ctypes.c_uint64)]),
     "tw_transpose_cast": (_c_int, [_vp, _i32, _i64, _i64, _i64, _vp, _i32, _i64, _vp]),
     "tw_plan_destroy": (None, [_vp]),

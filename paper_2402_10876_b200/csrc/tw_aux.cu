@@ -97,7 +97,7 @@ __device__ __forceinline__ void residual_store4(const ResidualArgs& args, int64_
                                                 float o2, float o3) {
   const bool obf = args.out_dtype == kBF16;
   const bool accum = ps >= 0;
-  if (n >= 4 && bs % 4 == 0 && (!accum || ps % 4 == 0)) {
+  if (args.vec_ok && n >= 4 && bs % 4 == 0 && (!accum || ps % 4 == 0)) {
     if (args.out_dtype != kF32) {
       uint2* p = reinterpret_cast<uint2*>(static_cast<uint16_t*>(args.out) + bs);
       const uint2 prev =
@@ -180,7 +180,7 @@ __global__ void __launch_bounds__(kResThreads, 1)
   // entries: 16-bit value << 16 | row offset in 16-byte units (row * L)
   const uint32_t zrow = static_cast<uint32_t>(K) * L;
   const uint8_t* sAb = reinterpret_cast<const uint8_t*>(sAt);
-  const bool fast = args.out_dtype != kF32 && args.ld_out % 8 == 0;
+  const bool fast = args.vec_ok && args.out_dtype != kF32 && args.ld_out % 8 == 0;
   int cs = c0 + warp * kCols;
   // columns past c1 read the (zero-row) padding at the start of the lists
   int4 m = cs + sub < c1 ? __ldg(args.meta + cs + sub) : make_int4(0, 0, 0, 0);
@@ -192,7 +192,8 @@ __global__ void __launch_bounds__(kResThreads, 1)
     // the TW result of a kept column (workspace row m.w - 1, else the out row
     // itself), read now and consumed after the sum
     const void* src = args.src ? args.src : args.out;
-    const int64_t ps = m.w == 0 ? -1
+    const int64_t ps = args.acc_all ? bs
+                       : m.w == 0 ? -1
                        : args.src ? static_cast<int64_t>(m.w - 1) * args.ld_src + t0 + tok
                                   : bs;
     uint4 prev = make_uint4(0u, 0u, 0u, 0u);
@@ -280,8 +281,22 @@ __global__ void __launch_bounds__(256)
     acc = fmaf(load_as_float(args.at, args.in_dtype, args.rows[e] * args.ld_at + m), args.vals[e],
                acc);
   const int64_t base = static_cast<int64_t>(args.out_rows[col]) * args.ld_out + m;
-  if (args.accumulate[col]) acc += load_as_float(args.out, args.out_dtype, base);
+  if (args.accumulate[col] || args.acc_all) acc += load_as_float(args.out, args.out_dtype, base);
   store_from_float(args.out, args.out_dtype, base, acc);
+}
+
+// ct[u] = src[src_row[u]] or 0: the caller's tile product placed at the union
+// rows (GemmOutput.expand + re-condense of executor.py:194-203, on the device).
+__global__ void scatter_rows_kernel(const uint8_t* src, int64_t ld_src, const int32_t* src_row,
+                                    uint8_t* dst, int64_t ld_dst, int64_t M, int esz) {
+  const int u = blockIdx.y;
+  const int sr = __ldg(src_row + u);
+  const int64_t bytes = M * esz;
+  uint8_t* d = dst + static_cast<int64_t>(u) * ld_dst * esz;
+  const uint8_t* s = sr >= 0 ? src + static_cast<int64_t>(sr) * ld_src * esz : nullptr;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < bytes;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    d[i] = s ? s[i] : 0;
 }
 
 // 32 x 32 shared-memory transpose with dtype conversion (general fallback).
@@ -386,10 +401,18 @@ int residual_block_tokens(int32_t K, int* ctas_per_sm) {
 template <int T, bool kBf>
 static cudaError_t launch_res_t(const ResidualArgs& args, cudaStream_t stream) {
   const size_t smem = static_cast<size_t>(args.K + 1) * T * 2;
-  cudaError_t e = cudaFuncSetAttribute(tw_residual_kernel<T, kBf>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem));
+  // the dynamic shared-memory limit is raised once per device (to the
+  // largest block any K allows), not on every launch
+  static uint64_t configured = 0;  // bit per device ordinal
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
+  if (dev >= 64 || !(configured >> dev & 1u)) {
+    e = cudaFuncSetAttribute(tw_residual_kernel<T, kBf>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(200 * 1024 + 2 * T));
+    if (e != cudaSuccess) return e;
+    if (dev < 64) configured |= uint64_t{1} << dev;
+  }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(static_cast<unsigned>(args.n_blocks), static_cast<unsigned>(args.n_groups));
   cfg.blockDim = dim3(kResThreads);
@@ -441,6 +464,18 @@ cudaError_t launch_transpose_cast(const void* a, int32_t a_dtype, int64_t M, int
   dim3 block(32, 8);
   transpose_cast_kernel<<<grid, block, 0, stream>>>(a, a_dtype, M, K, lda, at, at_dtype, ld_at,
                                                      out_row);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_scatter_rows(const void* src, int64_t ld_src, const int32_t* src_row,
+                                int32_t n_rows, void* dst, int64_t ld_dst, int64_t M, int esz,
+                                cudaStream_t stream) {
+  if (n_rows <= 0 || M <= 0) return cudaSuccess;
+  const int64_t bytes = M * esz;
+  unsigned gx = static_cast<unsigned>(std::min<int64_t>((bytes + 255) / 256, 64));
+  dim3 grid(gx, static_cast<unsigned>(n_rows));
+  scatter_rows_kernel<<<grid, 256, 0, stream>>>(static_cast<const uint8_t*>(src), ld_src, src_row,
+                                                static_cast<uint8_t*>(dst), ld_dst, M, esz);
   return cudaGetLastError();
 }
 

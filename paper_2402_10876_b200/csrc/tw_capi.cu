@@ -162,28 +162,36 @@ struct tw_plan {
   bool has_overlay = false;
   int64_t nnz = 0;
   std::vector<int32_t> union_cols;
-  int32_t* d_union_rowmap = nullptr;  // condensed col -> union position
   int32_t n_ov_cols = 0;                // overlay columns with entries (listed first)
   int32_t n_ov_cols_all = 0;            // + kept columns without entries (workspace mode)
-  int32_t* d_ov_start = nullptr;
-  int32_t* d_ov_rows = nullptr;
-  float* d_ov_vals = nullptr;
-  int32_t* d_ov_out = nullptr;
-  int32_t* d_ov_acc = nullptr;
-  int4* d_ov_meta = nullptr;          // K2 per column: {first entry, entries, out row, accumulate}
-  uint32_t* d_ov_rv = nullptr;         // K2 lists: row << 16 | 16-bit value
-  int32_t* d_ov_rows_pos = nullptr;     // row-run plans: d_ov_rows as layout positions (copy 0)
-  uint32_t* d_ov_rv_pos = nullptr;      // row-run plans: d_ov_rv as layout positions (copy 0)
+  // device overlay arrays; replaced as a whole by tw_plan_attach_overlay
+  // (built into a fresh set first, so a failed attach leaves the old one)
+  struct OvDev {
+    int32_t* union_rowmap = nullptr;    // condensed col -> union position
+    int32_t* start = nullptr;
+    int32_t* rows = nullptr;
+    float* vals = nullptr;
+    int32_t* out = nullptr;
+    int32_t* acc = nullptr;
+    int4* meta = nullptr;               // K2 per column: {first entry, entries, out row, src row + 1}
+    uint32_t* rv = nullptr;             // K2 lists: 16-bit value << 16 | staged-row offset
+    int32_t* rows_pos = nullptr;        // row-run plans: rows as layout positions (copy 0)
+    uint32_t* rv_pos = nullptr;         // row-run plans: rv as layout positions (copy 0)
+    void release() {
+      for (void* q : {(void*)union_rowmap, (void*)start, (void*)rows, (void*)vals, (void*)out,
+                      (void*)acc, (void*)meta, (void*)rv, (void*)rows_pos, (void*)rv_pos})
+        if (q) cudaFree(q);
+      *this = OvDev{};
+    }
+  } ov;
   int32_t ov_block_tokens = 0, ov_ctas_per_sm = 0;
   std::vector<int32_t> ov_start;       // host copy of the K2 column pointers
 
   ~tw_plan() {
     for (void* p : {(void*)d_subtiles, (void*)d_gidx, d_payload, (void*)d_perm, (void*)d_inv,
-                    (void*)d_box_first, (void*)d_boxes, (void*)d_gidx_pos,
-                    (void*)d_union_rowmap, (void*)d_ov_start, (void*)d_ov_rows, (void*)d_ov_vals,
-                    (void*)d_ov_out, (void*)d_ov_acc, (void*)d_ov_rv, (void*)d_ov_meta,
-                    (void*)d_ov_rows_pos, (void*)d_ov_rv_pos})
+                    (void*)d_box_first, (void*)d_boxes, (void*)d_gidx_pos})
       if (p) cudaFree(p);
+    ov.release();
   }
 };
 
@@ -663,28 +671,26 @@ int tw_plan_attach_overlay(tw_plan* p, int32_t k, int32_t n, int64_t nnz, const 
     src_cond.push_back(cond_of[c]);
   }
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  for (void* q : {(void*)p->d_union_rowmap, (void*)p->d_ov_start, (void*)p->d_ov_rows,
-                  (void*)p->d_ov_vals, (void*)p->d_ov_out, (void*)p->d_ov_acc, (void*)p->d_ov_rv,
-                  (void*)p->d_ov_meta, (void*)p->d_ov_rows_pos, (void*)p->d_ov_rv_pos})
-    if (q) cudaFree(q);
-  p->d_ov_rv = p->d_ov_rv_pos = nullptr;
-  p->d_ov_rows_pos = nullptr;
-  p->d_union_rowmap = nullptr;
-  p->d_ov_start = p->d_ov_rows = p->d_ov_out = p->d_ov_acc = nullptr;
-  p->d_ov_vals = nullptr;
-  p->d_ov_meta = nullptr;
-  if (int st = upload(&p->d_union_rowmap, rowmap, s)) return st;
-  if (int st = upload(&p->d_ov_start, start, s)) return st;
-  if (int st = upload(&p->d_ov_rows, rows, s)) return st;
-  if (int st = upload(&p->d_ov_vals, vals, s)) return st;
-  if (int st = upload(&p->d_ov_out, out_rows, s)) return st;
-  if (int st = upload(&p->d_ov_acc, acc, s)) return st;
+  // new device arrays go into a fresh set, swapped in only when every upload
+  // succeeded (a failure frees them and leaves the plan's previous overlay)
+  struct Guard {
+    tw_plan::OvDev d;
+    bool keep = false;
+    ~Guard() { if (!keep) d.release(); }
+  } ng;
+  tw_plan::OvDev& nd = ng.d;
+  if (int st = upload(&nd.union_rowmap, rowmap, s)) return st;
+  if (int st = upload(&nd.start, start, s)) return st;
+  if (int st = upload(&nd.rows, rows, s)) return st;
+  if (int st = upload(&nd.vals, vals, s)) return st;
+  if (int st = upload(&nd.out, out_rows, s)) return st;
+  if (int st = upload(&nd.acc, acc, s)) return st;
   // Row-run plans: K2 reads A^T in the plan layout too (tw_gemm_tew_ex with
   // TW_LAYOUT_PLAN), through copy 0's positions (p->inv[r] < k).
   if (p->runs) {
     std::vector<int32_t> rows_pos(rows.size());
     for (size_t e = 0; e < rows.size(); ++e) rows_pos[e] = p->inv[rows[e]];
-    if (int st = upload(&p->d_ov_rows_pos, rows_pos, s)) return st;
+    if (int st = upload(&nd.rows_pos, rows_pos, s)) return st;
   }
   // K2 geometry: A^T block of T tokens for all K rows in shared memory;
   // packed (row, value) lists need row < 2^16.  Each column's list starts on
@@ -692,15 +698,13 @@ int tw_plan_attach_overlay(tw_plan* p, int32_t k, int32_t n, int64_t nnz, const 
   // (L = T / 8 lanes per column), so every lane fetches its next entry with
   // one 4-byte load (1 instead of 2 per lane: less padding, 11.5 entries per
   // column on BERT).
-  p->ov_block_tokens = 0;
-  p->ov_ctas_per_sm = 0;
-  p->ov_start = start;
+  int32_t new_block_tokens = 0, new_ctas_per_sm = 0;
   if (k < 65535 && !ov_cols.empty() && !env_int("TW_RESIDUAL_DIRECT", 0)) {
     int cps = 0;
     const int T = residual_block_tokens(k, &cps);
     if (T > 0) {
-      p->ov_block_tokens = T;
-      p->ov_ctas_per_sm = cps;
+      new_block_tokens = T;
+      new_ctas_per_sm = cps;
       const int G = T / 8;
       std::vector<uint32_t> rv;
       std::vector<int4> meta(ov_cols.size());
@@ -756,16 +760,22 @@ int tw_plan_attach_overlay(tw_plan* p, int32_t k, int32_t n, int64_t nnz, const 
         for (uint32_t& x : v) x = ((x & 0xffffu) << 16) | ((x >> 16) * (uint32_t)G);
         return v;
       };
-      if (int st = upload(&p->d_ov_rv, device_form(rv), s)) return st;
-      if (int st = upload(&p->d_ov_meta, meta, s)) return st;
+      if (int st = upload(&nd.rv, device_form(rv), s)) return st;
+      if (int st = upload(&nd.meta, meta, s)) return st;
       if (p->runs) {
         for (uint32_t& x : rv)  // zero row k stays k (the staged block's appended row)
           if ((int32_t)(x >> 16) < k) x = ((uint32_t)p->inv[x >> 16] << 16) | (x & 0xffffu);
-        if (int st = upload(&p->d_ov_rv_pos, device_form(rv), s)) return st;
+        if (int st = upload(&nd.rv_pos, device_form(rv), s)) return st;
       }
     }
   }
   TW_CUDA(cudaStreamSynchronize(s));
+  p->ov.release();
+  p->ov = nd;
+  ng.keep = true;
+  p->ov_block_tokens = new_block_tokens;
+  p->ov_ctas_per_sm = new_ctas_per_sm;
+  p->ov_start = start;
   p->union_cols = uni;
   p->n_ov_cols = n_with_entries;
   p->n_ov_cols_all = (int32_t)ov_cols.size();
@@ -993,40 +1003,39 @@ int tw_plan_row_order(const tw_plan* p, int32_t* out_rows) {
   return TW_OK;
 }
 
-static int run_tew(const tw_plan* p, const void* x, int64_t m, int64_t ld_x, void* ct,
-                   int64_t ld_ct, int32_t out_dtype, void* ws, int64_t ld_ws, cudaStream_t s,
-                   bool plan_layout = false) {
-  // TW_TEW_PARTS (diagnostics): 1 = K1 only, 2 = K2 only, otherwise both
-  const int parts = env_int("TW_TEW_PARTS", 3);
-  if (parts != 2) {
-    if (ws) {
-      if (int st = run_tw(p, x, m, ld_x, ws, ld_ws, out_dtype, nullptr, p->n_cond, s, plan_layout))
-        return st;
-    } else if (int st = run_tw(p, x, m, ld_x, ct, ld_ct, out_dtype, p->d_union_rowmap,
-                               (int64_t)p->union_cols.size(), s, plan_layout)) {
-      return st;
-    }
-  }
-  if (parts == 1) return TW_OK;
+// K2 over n_cols columns of the plan's overlay lists.  src (ld_src): the
+// condensed TW result the kept columns read (workspace mode), nullptr = the
+// out rows themselves; meta overrides the plan's per-column table; acc_all:
+// every column adds onto its out row.
+static int launch_k2(const tw_plan* p, const void* x, int64_t m, int64_t ld_x, void* ct,
+                     int64_t ld_ct, int32_t out_dtype, const void* src, int64_t ld_src,
+                     int32_t n_cols, const int4* meta, bool acc_all, cudaStream_t s,
+                     bool plan_layout) {
   ResidualArgs r{};
   r.at = x;
   r.ld_at = ld_x;
   r.in_dtype = p->dtype;
-  r.col_start = p->d_ov_start;
-  r.rows = plan_layout ? p->d_ov_rows_pos : p->d_ov_rows;
-  r.vals = p->d_ov_vals;
-  r.out_rows = p->d_ov_out;
-  r.meta = p->d_ov_meta;
-  r.accumulate = p->d_ov_acc;
+  r.col_start = p->ov.start;
+  r.rows = plan_layout ? p->ov.rows_pos : p->ov.rows;
+  r.vals = p->ov.vals;
+  r.out_rows = p->ov.out;
+  r.meta = meta ? meta : p->ov.meta;
+  r.accumulate = p->ov.acc;
   r.out = ct;
   r.ld_out = ld_ct;
   r.out_dtype = out_dtype;
   r.M = (int32_t)m;
-  r.n_cols = ws ? p->n_ov_cols_all : p->n_ov_cols;
-  r.src = ws;
-  r.ld_src = ld_ws;
+  r.n_cols = n_cols;
+  r.src = src;
+  r.ld_src = ld_src;
   r.K = p->k;
-  r.rv = plan_layout ? p->d_ov_rv_pos : p->d_ov_rv;
+  r.acc_all = acc_all ? 1 : 0;
+  const int esz = out_dtype == kF32 ? 4 : 2;
+  auto al16 = [](const void* q, int64_t ld, int e) {
+    return reinterpret_cast<uintptr_t>(q) % 16 == 0 && (ld * e) % 16 == 0;
+  };
+  r.vec_ok = al16(ct, ld_ct, esz) && (!src || al16(src, ld_src, esz)) ? 1 : 0;
+  r.rv = plan_layout ? p->ov.rv_pos : p->ov.rv;
   r.block_tokens = p->ov_block_tokens;
   if (r.block_tokens > 0) {
     // grid = token blocks x column splits; splits (nnz-balanced runs of the
@@ -1062,6 +1071,25 @@ static int run_tew(const tw_plan* p, const void* x, int64_t m, int64_t ld_x, voi
   }
   TW_CUDA(launch_tw_residual(r, s));
   return TW_OK;
+}
+
+static int run_tew(const tw_plan* p, const void* x, int64_t m, int64_t ld_x, void* ct,
+                   int64_t ld_ct, int32_t out_dtype, void* ws, int64_t ld_ws, cudaStream_t s,
+                   bool plan_layout = false) {
+  // TW_TEW_PARTS (diagnostics): 1 = K1 only, 2 = K2 only, otherwise both
+  const int parts = env_int("TW_TEW_PARTS", 3);
+  if (parts != 2) {
+    if (ws) {
+      if (int st = run_tw(p, x, m, ld_x, ws, ld_ws, out_dtype, nullptr, p->n_cond, s, plan_layout))
+        return st;
+    } else if (int st = run_tw(p, x, m, ld_x, ct, ld_ct, out_dtype, p->ov.union_rowmap,
+                               (int64_t)p->union_cols.size(), s, plan_layout)) {
+      return st;
+    }
+  }
+  if (parts == 1) return TW_OK;
+  return launch_k2(p, x, m, ld_x, ct, ld_ct, out_dtype, ws, ld_ws,
+                   ws ? p->n_ov_cols_all : p->n_ov_cols, nullptr, false, s, plan_layout);
 }
 
 int tw_gemm_tew(const tw_plan* p, const void* x, int64_t m, int64_t ld_x, void* ct,
@@ -1116,6 +1144,49 @@ int tw_gemm_tew_ex(const tw_plan* p, const void* x, int64_t m, int64_t ld_x, voi
                 (unsigned long long)need);
   return run_tew(p, x, m, ld_x, ct, ld_ct, out_dtype, ws, (m + 7) / 8 * 8,
                  static_cast<cudaStream_t>(stream), plan_layout);
+}
+
+int tw_gemm_tew_reuse(const tw_plan* p, const void* x, int64_t m, int64_t ld_x,
+                      const void* tile_ct, int64_t ld_tile, const int32_t* tile_row_of_union,
+                      void* ct, int64_t ld_ct, int32_t out_dtype, int32_t x_layout, void* stream) {
+  g_last_error.clear();
+  if (int st = check_io(p, x, m, ld_x, ct, ld_ct, out_dtype)) return st;
+  if (!p->has_overlay) return fail(TW_ERR_INVALID_INPUT, "plan has no overlay attached");
+  if (!tile_ct || ld_tile < m) return fail(TW_ERR_INVALID_INPUT, "tile product must be given, ld >= m");
+  if (x_layout != TW_LAYOUT_NATURAL && x_layout != TW_LAYOUT_PLAN)
+    return fail(TW_ERR_INVALID_INPUT, "unknown activation layout %d", x_layout);
+  const bool plan_layout = x_layout == TW_LAYOUT_PLAN;
+  if (plan_layout && !p->runs) return fail(TW_ERR_INVALID_INPUT, "this plan has no row-run layout");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int esz = out_dtype == kF32 ? 4 : 2;
+  const int32_t nu = (int32_t)p->union_cols.size();
+  if (!tile_row_of_union && p->ov_block_tokens > 0) {
+    // the tile product is in this plan's condensed column order: K2 alone in
+    // workspace mode, reading it as the kept columns' source rows
+    return launch_k2(p, x, m, ld_x, ct, ld_ct, out_dtype, tile_ct, ld_tile, p->n_ov_cols_all,
+                     nullptr, false, s, plan_layout);
+  }
+  // general: scatter the caller's rows to the union rows (zeros where the
+  // tile product has no such column), then K2 adds every overlay column
+  std::vector<int32_t> map(nu, -1);
+  if (tile_row_of_union) {
+    for (int32_t u = 0; u < nu; ++u) map[u] = tile_row_of_union[u];
+  } else {
+    std::vector<int32_t> cond_of(p->n, -1);
+    for (int32_t i = 0; i < p->n_cond; ++i) cond_of[p->cond_cols[i]] = i;
+    for (int32_t u = 0; u < nu; ++u) map[u] = cond_of[p->union_cols[u]];
+  }
+  int32_t* d_map = nullptr;
+  TW_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_map), (size_t)nu * sizeof(int32_t), s));
+  cudaError_t e = cudaMemcpyAsync(d_map, map.data(), (size_t)nu * sizeof(int32_t),
+                                  cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = launch_scatter_rows(tile_ct, ld_tile, d_map, nu, ct, ld_ct, m, esz, s);
+  // the host vector must outlive the (pageable, staged) copy
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  cudaFreeAsync(d_map, s);
+  if (e != cudaSuccess) return fail(TW_ERR_CUDA, "tile product scatter failed: %s", cudaGetErrorString(e));
+  return launch_k2(p, x, m, ld_x, ct, ld_ct, out_dtype, nullptr, 0, p->n_ov_cols, nullptr, true, s,
+                   plan_layout);
 }
 
 int tw_transpose_cast(const void* a, int32_t a_dtype, int64_t m, int64_t k, int64_t lda, void* at,

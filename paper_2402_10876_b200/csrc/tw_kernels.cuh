@@ -120,9 +120,18 @@ struct ResidualArgs {
   int32_t block_tokens;     // T: tokens of the staged A^T block (0 = direct kernel)
   int32_t n_blocks;         // ceil(M / T): grid.x
   int32_t n_groups;         // nnz-balanced column splits: grid.y
+  int32_t vec_ok;           // out (and src) bases and pitches 16-byte aligned: vector I/O allowed
+  int32_t acc_all;          // every column adds onto its out row (caller's tile output already
+                            // scattered there: gemm_tew(tile_output=...), executor.py:194)
   int32_t group_first[kMaxColGroups + 1];  // first column of every split
 };
 cudaError_t launch_tw_residual(const ResidualArgs& args, cudaStream_t stream);
+
+// ct[u] = src[src_row[u]] (or 0 where src_row[u] < 0) for u < n_rows, M tokens,
+// element size esz (the caller's tile product scattered to the union rows).
+cudaError_t launch_scatter_rows(const void* src, int64_t ld_src, const int32_t* src_row,
+                                int32_t n_rows, void* dst, int64_t ld_dst, int64_t M, int esz,
+                                cudaStream_t stream);
 // Token-block size of the staged SpMM for K rows (0 = direct kernel) and the
 // number of resident CTAs per SM it allows.
 int residual_block_tokens(int32_t K, int* ctas_per_sm);

@@ -214,9 +214,10 @@ class TwPlan:
             at = at.index_select(0, self._row_order_dev)
         if _at_ready(at, self.compute_dtype):
             return at
-        m = int(at.shape[1])
+        # (after the row permutation at has layout_rows rows: row_copies x K)
+        rows, m = int(at.shape[0]), int(at.shape[1])
         ld = (m + 7) // 8 * 8
-        buf = torch.zeros((k, ld), dtype=_torch_dtype(self.compute_dtype), device=at.device)
+        buf = torch.zeros((rows, ld), dtype=_torch_dtype(self.compute_dtype), device=at.device)
         buf[:, :m].copy_(at)
         return buf[:, :m]
 
@@ -271,11 +272,24 @@ class TwPlan:
         return int(x.shape[1]), int(x.stride(0)) if x.shape[0] > 1 else ((int(x.shape[1]) + 7) // 8 * 8)
 
     def _out(self, rows: int, m: int, out, out_dtype):
+        """The C'^T output: a fresh (rows x M) tensor, or the caller's ``out``
+        checked like the C ABI needs it (CUDA tensor on the plan's device,
+        fp32/fp16/bf16, unit token stride, room for rows x M).  Misaligned
+        views are allowed: the kernels fall back to narrower stores."""
         torch = _torch()
         if out is None:
             return torch.empty((rows, m), dtype=_torch_dtype(_dtype_name(out_dtype)),
                                device=f"cuda:{self.device}")
-        if out.shape[0] < rows or out.shape[1] < m or out.stride(1) != 1:
+        if not isinstance(out, torch.Tensor) or not out.is_cuda:
+            raise InvalidInputError("out must be a CUDA tensor")
+        if out.device.index != self.device:
+            raise InvalidInputError(f"out is on cuda:{out.device.index}, the plan on "
+                                    f"cuda:{self.device}")
+        if out.dtype not in (torch.float32, torch.float16, torch.bfloat16):
+            raise InvalidInputError(f"out dtype {out.dtype} is not fp32/fp16/bf16")
+        if out.dim() != 2 or out.shape[0] < rows or out.shape[1] < m or \
+                (out.shape[1] > 1 and out.stride(1) != 1) or \
+                (out.shape[0] > 1 and out.stride(0) < m):
             raise InvalidInputError("out must be a (rows x M) CUDA tensor with unit token stride")
         return out
 
@@ -330,6 +344,53 @@ class TwPlan:
                                          ct.stride(0), code,
                                          ws.data_ptr() if ws is not None else None,
                                          int(need.value), layout, _native.stream_handle(stream)))
+        return ct
+
+
+    def run_tew_reuse(self, x, tile_ct, tile_columns=None, out=None, stream=None,
+                      x_layout=None):
+        """TEW result over the union columns from a tile product the caller
+        already holds (K2 only: reference gemm_tew's ``tile_output``,
+        executor.py:194).  ``tile_ct`` is the tile product as C^T rows (one row
+        per output column, tokens contiguous) in the output dtype;
+        ``tile_columns`` lists the original column of each of its rows (None:
+        this plan's condensed columns).  Columns of the union missing from it
+        start from zero, columns not in the union are dropped, exactly as
+        ``expand()`` + re-condensing does in the reference."""
+        if not self.has_overlay:
+            raise InvalidInputError("plan has no overlay attached")
+        if x_layout not in (None, "natural", "plan"):
+            raise InvalidInputError(f"unknown x_layout {x_layout!r}")
+        use_plan = self.uses_row_runs if x_layout is None else x_layout == "plan"
+        torch = _torch()
+        m, ld = self._check_x(x, self.original_dims[0] * int(self.info.row_copies)
+                              if use_plan else None)
+        if not isinstance(tile_ct, torch.Tensor) or not tile_ct.is_cuda or tile_ct.dim() != 2 \
+                or tile_ct.shape[1] != m or (m > 1 and tile_ct.stride(1) != 1):
+            raise InvalidInputError("tile_ct must be a CUDA (columns x M) tensor with unit "
+                                    "token stride")
+        ct = self._out(self.info.n_union, m, out, _dtype_name(tile_ct.dtype))
+        if ct.dtype != tile_ct.dtype:
+            raise InvalidInputError("out and the tile product must share a dtype")
+        rows_arg = None
+        if tile_columns is not None:
+            cols = np.asarray(tile_columns, dtype=np.int64)
+            if cols.shape != (tile_ct.shape[0],):
+                raise InvalidInputError("tile_columns must give one column per tile_ct row")
+            pos = {int(c): i for i, c in enumerate(cols)}
+            rows_arg = np.array([pos.get(int(u), -1) for u in self.union_columns],
+                                dtype=np.int32)
+        elif tile_ct.shape[0] != self.info.n_condensed:
+            raise InvalidInputError(f"tile_ct has {tile_ct.shape[0]} rows, the plan "
+                                    f"{self.info.n_condensed} condensed columns")
+        ld_tile = int(tile_ct.stride(0)) if tile_ct.shape[0] > 1 else m
+        lib = _native.load_library()
+        layout = _native.TW_LAYOUT_PLAN if use_plan else _native.TW_LAYOUT_NATURAL
+        _native.check(lib.tw_gemm_tew_reuse(
+            self._handle, x.data_ptr(), m, ld, tile_ct.data_ptr(), ld_tile,
+            None if rows_arg is None else _native.ptr(rows_arg, _native.ctypes.c_int32),
+            ct.data_ptr(), ct.stride(0) if ct.shape[0] > 1 else m,
+            _DTYPE_CODES[_dtype_name(ct.dtype)], layout, _native.stream_handle(stream)))
         return ct
 
 
@@ -557,16 +618,57 @@ def gemm_tew(a, b: TileSparseMatrix, ov: SparseOverlay,
              tile_output: Optional[GemmOutput] = None, *, compute_dtype: str = "fp16",
              out_dtype: str = "fp32") -> GemmOutput:
     """TW product + CSC overlay SpMM, condensed to the union of surviving
-    columns (reference executor.py:180-203).  The TW part is recomputed in
-    the same stream (K1 writes straight into union rows, K2 adds the
-    residual), so ``tile_output`` is accepted but not needed."""
+    columns (reference executor.py:180-203).  Without ``tile_output`` K1 and
+    K2 run back to back; with it (the reference CLI's composition, cli.py:
+    304-307) only K2 runs, on the caller's tile product, which is expanded
+    to the original columns and re-condensed exactly as executor.py:194-203
+    does (so a tile product that is not gemm_tile_sparse(a, b) is honoured)."""
     if tuple(ov.dims) != tuple(b.original_dims):
         raise InvalidInputError(f"overlay dims {tuple(ov.dims)} do not match weights "
                                 f"{tuple(b.original_dims)}")
     plan = plan_for(b, overlay=ov, compute_dtype=compute_dtype)
-    ct = plan.run_tew(_activations(a, plan), out_dtype=out_dtype)
+    x = _activations(a, plan)
+    if tile_output is None:
+        ct = plan.run_tew(x, out_dtype=out_dtype)
+    else:
+        # reuse the caller's tile product (executor.py:194): K2 alone adds the
+        # overlay onto it at the union columns
+        cols = np.asarray(tile_output.column_map.kept, dtype=np.int64)
+        same = cols.shape == plan.condensed_columns.shape and \
+            np.array_equal(cols, plan.condensed_columns)
+        ct = plan.run_tew_reuse(x, _tile_rows(tile_output, out_dtype),
+                                tile_columns=None if same else cols)
     return GemmOutput(condensed=ct.t(), column_map=IndexMask(b.original_dims[1],
                                                              plan.union_columns))
+
+
+def _tile_rows(out: "GemmOutput", out_dtype: str):
+    """A GemmOutput's condensed M x N_t product as C^T rows (N_t x M, tokens
+    contiguous) in ``out_dtype`` on the device: our own outputs already are
+    (a transposed view), anything else goes through the K4 transpose-cast."""
+    torch = _torch()
+    cd = _dtype_name(out_dtype)
+    c = out.condensed
+    if isinstance(c, torch.Tensor) and c.is_cuda and c.dim() == 2 and \
+            c.dtype == _torch_dtype(cd) and (c.shape[0] <= 1 or c.stride(0) == 1):
+        return c.t()
+    src = c if isinstance(c, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(c))
+    if src.dim() != 2:
+        raise InvalidInputError("tile_output.condensed must be 2-D (M x N_t)")
+    src = src.cuda()
+    if src.dtype not in (torch.float32, torch.float16, torch.bfloat16):
+        src = src.float()
+    if src.stride(1) != 1:
+        src = src.contiguous()
+    m, n_t = src.shape
+    ld = max(1, m)
+    rows = torch.empty((max(1, n_t), ld), dtype=_torch_dtype(cd), device=src.device)
+    if m and n_t:
+        lib = _native.load_library()
+        _native.check(lib.tw_transpose_cast(src.data_ptr(), _DTYPE_CODES[_dtype_name(src.dtype)],
+                                            m, n_t, src.stride(0), rows.data_ptr(),
+                                            _DTYPE_CODES[cd], ld, _native.stream_handle()))
+    return rows[:n_t, :m]
 
 
 def gemm_dense(a, b):

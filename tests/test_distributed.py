@@ -96,3 +96,55 @@ def test_token_slice_covers_m():
             spans = [D.token_slice(m, world, r) for r in range(world)]
             assert spans[0][0] == 0 and spans[-1][1] == m
             assert all(spans[i][1] == spans[i + 1][0] for i in range(world - 1))
+
+
+def _sharded_worker(rank, world, port, chunks, results):
+    import torch
+    import torch.distributed as dist
+
+    from oracle import tilesparse_oracle as orc
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        a, enc = _problem()
+        # the per-rank product stands in for K1 (no GPU here): the oracle on
+        # this rank's tile group, written into the shard view like K1 does
+        lo, hi = D.column_shards(enc, world)[rank]
+        sub = D.shard_encoding(enc, lo, hi)
+
+        def local(x, out):
+            out.copy_(torch.from_numpy(orc.c_gemm_cto_enc(x.t().numpy().copy(), sub).T))
+
+        sp = D.TwShardedPlan(enc, chunks=chunks, local_product=local)
+        at = torch.from_numpy(np.ascontiguousarray(a.T))
+        res = sp.run(at, out_dtype="fp32")
+        full = res.full() if isinstance(res, D.ChunkedRows) else res
+        if isinstance(res, D.ChunkedRows):
+            assert len(res.parts) == len(D.token_chunks(a.shape[0], chunks))
+        results[rank] = (full.numpy().T.copy(), sp.condensed_columns.copy())
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,chunks", [(2, 1), (2, 3), (3, 2)])
+def test_sharded_plan_all_gathers_full_product(world, chunks):
+    """TwShardedPlan: every rank ends with the whole condensed product (the
+    column shards all-gathered, M-chunked when chunks > 1) equal to the
+    single-device product, with the reference's condensed column map."""
+    from oracle import tilesparse_oracle as orc
+
+    a, enc = _problem()
+    want = orc.c_gemm_cto_enc(a, enc)
+    mgr = mp.Manager()
+    results = mgr.dict()
+    mp.spawn(_sharded_worker, args=(world, _free_port(), chunks, results), nprocs=world,
+             join=True)
+    kept = np.concatenate([np.arange(int(enc.col_counts[i])) +
+                           enc.col_offsets[i, :int(enc.col_counts[i])]
+                           for i in range(enc.tile_count)])
+    for r in range(world):
+        got, cols = results[r]
+        assert np.allclose(got, want, rtol=0, atol=1e-5 * np.abs(want).max())
+        assert np.array_equal(cols, kept)
