@@ -198,13 +198,91 @@ def cpu_model() -> str:
     return "unknown"
 
 
+REF_DIR = ROOT / "baseline" / "_ref"
+
+
+def load_reference():
+    """The unmodified reference package, pip-installed into baseline/_ref
+    (DESIGN.md section 5), or None when it is absent."""
+    if not (REF_DIR / "tilesparse" / "__init__.py").exists():
+        return None
+    if str(REF_DIR) not in sys.path:
+        sys.path.append(str(REF_DIR))
+    import tilesparse
+
+    return tilesparse
+
+
+def _ref_cli(ts):
+    import importlib
+
+    return importlib.import_module(ts.__name__ + ".cli")
+
+
+def reference_layers(ts, cfg: dict):
+    """The step's layers pruned by the reference's own API (prune_tw /
+    prune_tew, patterns.py:542-642) on the same fp16-rounded synthetic
+    weights as our arm (the reference's synthetic_matrix, cli.py:52-56)."""
+    out = []
+    for k, n in cfg["layers"]:
+        w = _ref_cli(ts).synthetic_matrix(0, k, n, 0).astype(np.float16).astype(np.float32)
+        if cfg["delta"] > 0:
+            _, tsm, ov = ts.prune_tew(w, cfg["s"], cfg["delta"], cfg["g"])
+        elif cfg.get("pattern") == "tvw":
+            res = ts.prune_matrix("tvw", w, cfg["s"], g=cfg["g"])
+            tsm, ov = res.tile_matrix, None
+        else:
+            _, tsm = ts.prune_tw(w, cfg["s"], cfg["g"])
+            ov = None
+        out.append({"k": k, "n": n, "tsm": tsm, "ov": ov})
+    return out
+
+
+def reference_inputs(ts, cfg: dict, m: int):
+    return [_ref_cli(ts).synthetic_matrix(0, m, k, 1)[:m].astype(np.float16).astype(np.float32)
+            for k, _ in cfg["layers"]]
+
+
+def reference_step(ts, rlayers, inputs, workers: int):
+    """One step of the reference's own bench composition (cli.py:302-308):
+    execute_batched(lpt) per layer, plus gemm_tew(tile_output=...) for TEW."""
+    outs = []
+    for L, a in zip(rlayers, inputs):
+        out, _ = ts.execute_batched(a, L["tsm"], workers=workers, strategy="lpt")
+        if L["ov"] is not None and L["ov"].nnz:
+            out = ts.gemm_tew(a, L["tsm"], L["ov"], tile_output=out)
+        outs.append(out)
+    return outs
+
+
+def step_flops(rlayers, m: int) -> int:
+    """metrics.report.sparse_flops of the step (metrics.py:114-118)."""
+    tot = 0
+    for L in rlayers:
+        macs = sum(t.width * t.kept_rows.n_kept for t in L["tsm"].tiles)
+        nnz = L["ov"].nnz if L["ov"] is not None else 0
+        tot += 2 * m * (macs + nnz)
+    return tot
+
+
 def cpu_reference_rate(cfg: dict, layers, m_sample: int, reps: int = 1, workers: int = 0):
-    """Time the oracle port of execute_batched (+ gemm_tew overlay) on an
-    M-slice with `workers` lanes (0: every host core); returns (TFLOP/s,
-    seconds, flops, workers)."""
+    """Time the reference's CPU path on an M-slice with `workers` lanes (0:
+    every host core).  The unmodified reference from baseline/_ref when
+    present ("reference"), else the oracle port ("port").  Returns
+    (TFLOP/s, seconds, flops, workers, kind)."""
+    workers = workers or os.cpu_count() or 1
+    ts = load_reference()
+    if ts is not None:
+        rl = reference_layers(ts, cfg)
+        inputs = reference_inputs(ts, cfg, m_sample)
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            reference_step(ts, rl, inputs, workers)
+        secs = time.perf_counter() - t0
+        flops = reps * step_flops(rl, m_sample)
+        return flops / secs / 1e12, secs, flops, workers, "reference"
     from oracle import tilesparse_oracle as orc
 
-    workers = workers or os.cpu_count() or 1
     total_s, total_f = 0.0, 0
     for _ in range(reps):
         for li, L in enumerate(layers):
@@ -220,32 +298,75 @@ def cpu_reference_rate(cfg: dict, layers, m_sample: int, reps: int = 1, workers:
             nnz = L["ov"].nnz if L["ov"] is not None else 0
             total_f += 2 * m_sample * (sum(t.width * t.kept_rows.n_kept for t in L["tsm"].tiles)
                                        + nnz)
-    return total_f / total_s / 1e12, total_s, total_f, workers
+    return total_f / total_s / 1e12, total_s, total_f, workers, "port"
+
+
+def port_matches_reference(cfg: dict, m: int = 16):
+    """Cross-check on a few tokens: the oracle port of execute_batched gives
+    the reference's fp64 result bit for bit (same ascending-k rank-1 order)."""
+    ts = load_reference()
+    if ts is None:
+        return None
+    from oracle import tilesparse_oracle as orc
+
+    rl = reference_layers(ts, cfg)
+    inputs = reference_inputs(ts, cfg, m)
+    ref = reference_step(ts, [dict(L, ov=None) for L in rl], inputs, 1)
+    for L, a, r in zip(rl, inputs, ref):
+        tiles = [(t.kept_rows.kept, t.payload) for t in L["tsm"].tiles]
+        if not np.array_equal(orc.execute_batched(a, tiles, 1, "lpt"), r.condensed):
+            return False
+    return True
 
 
 def run_reference_arm(args, cfg, rank: int, world: int) -> None:
+    """--impl reference: the reference's own CPU implementation of the path
+    (the unmodified tilesparse from baseline/_ref) on this host's cores, on
+    our arm's config.  Every step is the full workload (all M tokens of
+    every layer); rank 0 alone runs it under torchrun."""
     if rank != 0:
         return
-    layers = build_layers(cfg)
-    m_sample = min(cfg["m"], 512)
-    for _ in range(args.warmup):
-        cpu_reference_rate(cfg, layers, m_sample)
-    rate, secs, flops, workers = cpu_reference_rate(cfg, layers, m_sample, reps=args.steps)
-    sample = (f"{m_sample} of {cfg['m']} tokens per step through every layer "
-              f"(oracle port of execute_batched, lpt, {workers} workers)")
+    ts = load_reference()
+    m = cfg["m"]
+    workers = os.cpu_count() or 1
+    if ts is not None:
+        rl = reference_layers(ts, cfg)
+        inputs = reference_inputs(ts, cfg, m)
+        flops = step_flops(rl, m)
+        for _ in range(args.warmup):
+            reference_step(ts, rl, inputs, workers)
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            reference_step(ts, rl, inputs, workers)
+        secs = time.perf_counter() - t0
+        rate = flops * args.steps / secs / 1e12
+        kind = "reference"
+        sample = (f"full step: all {m} tokens of every layer per step, unmodified tilesparse "
+                  f"0.1.0 (baseline/_ref) execute_batched lpt with {workers} workers"
+                  + (" + gemm_tew(tile_output)" if cfg["delta"] > 0 else ""))
+        m_run = m
+    else:
+        layers = build_layers(cfg)
+        m_run = min(m, 512)
+        for _ in range(args.warmup):
+            cpu_reference_rate(cfg, layers, m_run)
+        rate, secs, flops, workers, kind = cpu_reference_rate(cfg, layers, m_run, reps=args.steps)
+        sample = (f"{m_run} of {m} tokens per step through every layer "
+                  f"(oracle port of execute_batched, lpt, {workers} workers)")
     line = {
         "metric": METRIC, "value": rate, "unit": "TFLOP/s", "impl": "reference",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": secs / args.steps * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (Philox seed 0, fp16-rounded)",
-        "config": {"workload": cfg["workload"], "parallelism": "cpu", "m_sample": m_sample},
-        "cpu_baseline": {"cpu_model": cpu_model(), "value": rate, "unit": "TFLOP/s", "cores": workers, "kind": "port",
-                         "sample": sample},
+        "config": {"workload": cfg["workload"], "parallelism": "cpu", "m_tokens": m_run,
+                   "same_config": m_run == m},
+        "cpu_baseline": {"cpu_model": cpu_model(), "value": rate, "unit": "TFLOP/s",
+                         "cores": workers, "kind": kind, "sample": sample},
         "e2e": {"value": rate, "unit": "TFLOP/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line))
+    print(json.dumps(line), flush=True)
 
 
 # ----------------------------------------------------------------------------
@@ -354,11 +475,7 @@ def run_ours(args, cfg, rank: int, world: int) -> None:
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    ms = ev0.elapsed_time(ev1)
-    t = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
+    ms_max = reduce_max(ev0.elapsed_time(ev1), world)
     ms_step = ms_max / args.steps
     value = world * flops_step / (ms_step * 1e-3) / 1e12
 
@@ -422,11 +539,7 @@ def run_ours(args, cfg, rank: int, world: int) -> None:
         dense_step(i)
     d1.record(stream)
     torch.cuda.synchronize()
-    dense_ms = d0.elapsed_time(d1) / args.steps
-    td = torch.tensor([dense_ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(td, op=dist.ReduceOp.MAX)
-    dense_ms = float(td.item())
+    dense_ms = reduce_max(d0.elapsed_time(d1) / args.steps, world)
     dense_flops = sum(2 * m * L["k"] * L["n"] for L in layers)
     del dense, dense_graphs
 
@@ -504,10 +617,7 @@ def run_ours(args, cfg, rank: int, world: int) -> None:
     stream.wait_stream(s_out)
     e1.record(stream)
     torch.cuda.synchronize()
-    te = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_ms = float(te.item()) / args.steps
+    e2e_ms = reduce_max(e0.elapsed_time(e1), world) / args.steps
     e2e_value = world * flops_step / (e2e_ms * 1e-3) / 1e12
 
     if rank != 0:
@@ -531,11 +641,13 @@ def run_ours(args, cfg, rank: int, world: int) -> None:
                      "peak_source": pk["source"], "arithmetic_intensity": ai,
                      "layers": per_layer})
 
-    # CPU baseline: the reference algorithm on this host, bounded sample
+    # CPU baseline: the reference's own CPU path on this host, bounded sample
     m_sample = min(m, 1024)
-    cpu_rate, cpu_s, _, workers = cpu_reference_rate(cfg, layers, m_sample)
+    cpu_rate, cpu_s, _, workers, cpu_kind = cpu_reference_rate(cfg, layers, m_sample)
     # the single-lane figure (W = 1, as cmd_bench's default) on a quarter sample
-    cpu1_rate, cpu1_s, _, _ = cpu_reference_rate(cfg, layers, max(64, m_sample // 4), workers=1)
+    cpu1_rate, cpu1_s, _, _, _ = cpu_reference_rate(cfg, layers, max(64, m_sample // 4),
+                                                    workers=1)
+    port_ok = port_matches_reference(cfg)
     clocks = clk.summary()
     line = {
         "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
@@ -562,11 +674,16 @@ def run_ours(args, cfg, rank: int, world: int) -> None:
                         "(K1) -> D2H of the fp16 C'^T; layers pipelined over H2D / compute / "
                         "D2H streams"},
         "roofline": roofline,
-        "cpu_baseline": {"cpu_model": cpu_model(), "value": cpu_rate, "unit": "TFLOP/s", "cores": workers, "kind": "port",
+        "cpu_baseline": {"cpu_model": cpu_model(), "value": cpu_rate, "unit": "TFLOP/s",
+                         "cores": workers, "kind": cpu_kind,
                          "sample": f"{m_sample} of {m} tokens through every layer "
-                                   f"({cpu_s:.1f} s, oracle port of execute_batched lpt)",
+                                   f"({cpu_s:.1f} s, "
+                                   + ("unmodified tilesparse execute_batched lpt"
+                                      if cpu_kind == "reference" else
+                                      "oracle port of execute_batched lpt") + ")",
                          "value_1_worker": cpu1_rate,
-                         "sample_1_worker": f"{max(64, m_sample // 4)} tokens, 1 lane ({cpu1_s:.1f} s)"},
+                         "sample_1_worker": f"{max(64, m_sample // 4)} tokens, 1 lane ({cpu1_s:.1f} s)",
+                         "port_matches_reference": port_ok},
         "gpu_launches": args.steps * len(layers) * (2 if tew else 1),
         "launch": "CUDA graph per step (one graph per rotating buffer set)",
         "clocks": clocks,
@@ -579,10 +696,12 @@ def run_ours(args, cfg, rank: int, world: int) -> None:
 # ----------------------------------------------------------------------------
 
 def run_big(args, cfg, rank: int, world: int) -> None:
-    """16384^2 TW layer, M=8192.  Rank r owns a contiguous, MAC-balanced group
-    of column tiles (distributed.column_shards), runs K1 on it and one
-    all_gather_into_tensor assembles the full C'^T (N' x M).  A step = K1 on
-    the shard + the all-gather; value = the WHOLE layer's surviving FLOPs /
+    """16384^2 TW layer, M=8192, through the product's sharded entry point
+    (distributed.TwShardedPlan): rank r owns a contiguous, MAC-balanced group
+    of column tiles, runs K1 on it and the ranks all-gather C'^T; for N > 1
+    the tokens go in 4 M-chunks so the all-gather of chunk j (NCCL stream)
+    overlaps K1 of chunk j + 1.  A step = the whole sharded layer ending with
+    the full C'^T on every rank; value = the layer's surviving FLOPs /
     max-over-ranks step time (strong scaling).  Inputs (268 MB A^T, 134 MB
     payload, 134 MB output per rank) exceed L2, so there is no rotation."""
     import torch
@@ -596,25 +715,28 @@ def run_big(args, cfg, rank: int, world: int) -> None:
     w = tw.round_to(tw.synthetic_matrix(0, k, n, tw.STREAM_WEIGHTS), "fp16")
     _, tsm = tw.prune_tw(w, cfg["s"], cfg["g"])
     enc = tw.encode_cto(tsm)
-    shards = D.column_shards(enc, world)
-    rows = D.shard_rows(enc, shards)
-    lo, hi = shards[rank]
-    plan = tw.TwPlan(D.shard_encoding(enc, lo, hi), compute_dtype="fp16")
+    # one rank: the plain plan (no process group); N ranks: the sharded plan
+    chunks = 4 if world > 1 else 1
+    if world > 1:
+        sp = D.TwShardedPlan(enc, chunks=chunks)
+        plan = sp.plan
+    else:
+        sp = None
+        plan = tw.TwPlan(enc, compute_dtype="fp16")
     flops_total = tw.sparse_flops(tsm, m)
-    flops_local = plan.flops(m)
+    flops_local = plan.flops(m) if plan is not None else 0
     a_host = tw.round_to(tw.synthetic_matrix(0, m, k, tw.STREAM_INPUT), "fp16")
     a_dev = torch.from_numpy(a_host).to(dev, torch.float16)
-    at = plan.prepare(a_dev)
-    r0, r1 = rows[rank]
-    tallest = max(b - a for a, b in rows)
-    local = torch.empty((tallest, m), dtype=torch.float16, device=dev)
-    full = torch.empty((tallest * world, m), dtype=torch.float16, device=dev)
+    at = plan.prepare(a_dev) if plan is not None else tw.prepare_activations(a_dev)
     stream = torch.cuda.current_stream()
+    out1 = torch.empty((tsm.n_condensed, m), dtype=torch.float16, device=dev) \
+        if world == 1 else None
 
     def step(i: int = 0):
-        plan.run(at, out=local[: r1 - r0])
-        if world > 1:
-            dist.all_gather_into_tensor(full, local)
+        if sp is not None:
+            sp.run(at, out_dtype="fp16")
+        else:
+            plan.run(at, out=out1)
 
     def timed(fn, steps):
         for i in range(args.warmup):
@@ -630,22 +752,27 @@ def run_big(args, cfg, rank: int, world: int) -> None:
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
-        t = torch.tensor([e0.elapsed_time(e1) / steps], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+        return reduce_max(e0.elapsed_time(e1) / steps, world)
 
     with ClockSampler(torch.cuda.current_device()) as clk:
-        t_soak = time.time()
-        while time.time() - t_soak < 1.0:
+        # soak (~1 s) so the clock sampler sees the GPU under this load; a
+        # fixed count on every rank, since a step contains a collective
+        for i in range(400):
             step()
-            torch.cuda.synchronize()
+            if i % 50 == 49:
+                torch.cuda.synchronize()
+        torch.cuda.synchronize()
         ms_step = timed(step, args.steps)
     value = flops_total / (ms_step * 1e-3) / 1e12
 
     # K1 alone on this rank's shard (roofline) and the all-gather alone
-    ms_k1 = timed(lambda i: plan.run(at, out=local[: r1 - r0]), args.steps)
-    ms_ag = timed(lambda i: dist.all_gather_into_tensor(full, local), args.steps) if world > 1 else 0.0
+    h = sp.heights[rank] if sp is not None else tsm.n_condensed
+    local = torch.empty((max(1, h), m), dtype=torch.float16, device=dev)
+    ms_k1 = timed(lambda i: plan.run(at, out=local[:h]), args.steps) if plan is not None else 0.0
+    ms_ag = 0.0
+    if sp is not None:
+        shard = torch.empty((sp.tallest, m), dtype=torch.float16, device=dev)
+        ms_ag = timed(lambda i: sp._gather(shard), args.steps)
 
     # dense cuBLAS on the same column share (N/world columns of W, same A^T)
     c0 = n * rank // world
@@ -654,29 +781,31 @@ def run_big(args, cfg, rank: int, world: int) -> None:
     at_plain = tw.prepare_activations(a_dev)
     dense_out = torch.empty((c1 - c0, m), dtype=torch.float16, device=dev)
     ms_dense = timed(lambda i: torch.matmul(wt, at_plain, out=dense_out), args.steps)
-    del wt, dense_out
+    del wt, dense_out, at_plain
 
-    # e2e through the public API: pinned host A (M x K) -> H2D -> K4 -> K1 ->
-    # all-gather -> D2H of the full fp16 C'^T
+    # e2e through the public API: pinned host A (M x K) -> H2D -> prepare (K4)
+    # -> K1 (+ all-gather) -> D2H of the full fp16 C'^T
     a_pin = torch.from_numpy(a_host).to(torch.float16).pin_memory()
-    c_pin = torch.empty((tallest * world if world > 1 else r1 - r0, m),
-                        dtype=torch.float16).pin_memory()
+    c_pin = torch.empty((tsm.n_condensed, m), dtype=torch.float16).pin_memory()
 
     def e2e(i: int = 0):
         a_dev.copy_(a_pin, non_blocking=True)
-        x = plan.prepare(a_dev)
-        plan.run(x, out=local[: r1 - r0])
-        if world > 1:
-            dist.all_gather_into_tensor(full, local)
-            c_pin.copy_(full, non_blocking=True)
+        if sp is not None:
+            res = sp.run(sp.prepare(a_dev), out_dtype="fp16")
+            if isinstance(res, D.ChunkedRows):
+                for (t0, t1), part in zip(res.spans, res.parts):
+                    c_pin[:, t0:t1].copy_(part, non_blocking=True)
+            else:
+                c_pin.copy_(res, non_blocking=True)
         else:
-            c_pin.copy_(local[: r1 - r0], non_blocking=True)
+            plan.run(plan.prepare(a_dev), out=out1)
+            c_pin.copy_(out1, non_blocking=True)
 
     ms_e2e = timed(e2e, max(2, args.steps // 4))
     if rank != 0:
         return
     pk = peaks()
-    tf_k1 = flops_local / (ms_k1 * 1e-3) / 1e12
+    tf_k1 = flops_local / (ms_k1 * 1e-3) / 1e12 if ms_k1 else 0.0
     roofline = {"bound": "tensor", "achieved": tf_k1, "peak": pk["tc"], "unit": "TFLOP/s",
                 "frac": tf_k1 / pk["tc"],
                 "traffic": ncu_traffic(args.config) if world == 1 else None,
@@ -684,38 +813,81 @@ def run_big(args, cfg, rank: int, world: int) -> None:
                 "peak_source": pk["source"],
                 "arithmetic_intensity": flops_total / tw.algorithmic_bytes(tsm, m),
                 "k1_ms": ms_k1, "allgather_ms": ms_ag}
-    # CPU baseline: the reference algorithm on one tile over 64 tokens, scaled
-    from oracle import tilesparse_oracle as orc
+    # CPU baseline: the reference's execute_batched on one tile over 64 tokens, scaled
+    ts = load_reference()
     t = tsm.tiles[0]
-    a_s = a_host[:64]
+    n_tok = 512
+    a_s = a_host[:n_tok]
     t0 = time.perf_counter()
-    orc.execute_batched(a_s, [(t.kept_rows.kept, t.payload)], os.cpu_count() or 1, "lpt")
+    if ts is not None:
+        # the reference's per-tile kernel (executor.py:121-124), one lane
+        ts.executor._tile_product(a_s.astype(np.float64), t.kept_rows.kept, t.payload)
+        kind = "reference"
+    else:
+        from oracle import tilesparse_oracle as orc
+
+        orc.execute_batched(a_s, [(t.kept_rows.kept, t.payload)], os.cpu_count() or 1, "lpt")
+        kind = "port"
     cpu_s = time.perf_counter() - t0
-    cpu_rate = 2 * 64 * t.width * t.kept_rows.n_kept / cpu_s / 1e12
+    cpu_rate = 2 * n_tok * t.width * t.kept_rows.n_kept / cpu_s / 1e12
     line = {
         "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "fp16",
         "data": "synthetic (Philox seed 0, fp16-rounded)",
         "config": {"workload": cfg["workload"], "m_tokens": m, "sparsity": cfg["s"],
-                   "g": cfg["g"], "parallelism": f"column tiles / {world} ranks + all-gather",
+                   "g": cfg["g"],
+                   "parallelism": (f"column tiles / {world} ranks + all-gather in {chunks} "
+                                   f"M-chunks overlapped with K1") if world > 1
+                                  else "one GPU, all 64 column tiles",
                    "l2": "inputs > L2 (268 MB A^T, 134 MB payload, 134 MB C'^T)"},
-        "speedup_vs_cublas": ms_dense / ms_k1,
+        "speedup_vs_cublas": ms_dense / ms_k1 if ms_k1 else None,
         "cublas": {"ms_per_step": ms_dense, "columns_per_rank": c1 - c0,
                    "tflops_dense": 2 * m * k * (c1 - c0) / (ms_dense * 1e-3) / 1e12},
         "frac_of_dense_peak": tf_k1 / pk["tc"],
         "e2e": {"value": flops_total / (ms_e2e * 1e-3) / 1e12, "unit": "TFLOP/s",
                 "ms_per_step": ms_e2e, "h2d_bytes_per_step": a_pin.numel() * 2,
                 "d2h_bytes_per_step": c_pin.numel() * 2,
-                "path": "pinned host fp16 A -> H2D -> K4 -> K1 -> all-gather -> D2H"},
+                "path": "pinned host fp16 A -> H2D -> prepare (K4) -> K1 -> all-gather -> D2H"},
         "roofline": roofline,
-        "cpu_baseline": {"cpu_model": cpu_model(), "value": cpu_rate, "unit": "TFLOP/s", "cores": os.cpu_count() or 1,
-                         "kind": "port", "sample": f"tile 0 (K'={t.kept_rows.n_kept}) x 64 tokens "
-                                                   f"({cpu_s:.1f} s, one lane: one tile)"},
-        "gpu_launches": args.steps,
+        "cpu_baseline": {"cpu_model": cpu_model(), "value": cpu_rate, "unit": "TFLOP/s",
+                         "cores": 1, "kind": kind,
+                         "sample": f"tile 0 (K'={t.kept_rows.n_kept}) x {n_tok} tokens "
+                                   f"({cpu_s:.1f} s, one lane: the reference runs one tile "
+                                   f"per lane)"},
+        "gpu_launches": args.steps * chunks,
         "clocks": clk.summary(),
     }
     print(json.dumps(line))
+
+
+def reduce_max(value: float, world: int) -> float:
+    """max over ranks of a host float (device tensor under NCCL, host tensor
+    under gloo: ranks sharing one GPU)."""
+    if world <= 1:
+        return float(value)
+    import torch
+    import torch.distributed as dist
+
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([float(value)], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def relaunch(n: int) -> int:
+    """`bench.py --gpus N` run without torchrun: re-exec under
+    torch.distributed.run with N ranks on this node (rendezvous on 127.0.0.1),
+    exactly as the driver launches it.  Rank 0 prints the JSON line."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={n}", "--master-addr", "127.0.0.1", f"--master-port={port}",
+           str(Path(__file__).resolve()), *sys.argv[1:]]
+    return subprocess.run(cmd).returncode
 
 
 def main() -> None:
@@ -728,11 +900,18 @@ def main() -> None:
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.gpus < 1:
+        ap.error("--gpus must be >= 1")
     cfg = CONFIGS[args.config]
 
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(relaunch(args.gpus))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus and rank == 0:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; using {world} ranks",
+              file=sys.stderr)
 
     if args.impl == "reference":
         run_reference_arm(args, cfg, rank, world)
@@ -741,9 +920,19 @@ def main() -> None:
     import torch
     import torch.distributed as dist
 
-    torch.cuda.set_device(local)
+    n_dev = torch.cuda.device_count()
+    if n_dev < 1:
+        raise SystemExit("bench.py: no CUDA device (the TW path runs only on the GPU)")
+    # one rank per GPU; more ranks than GPUs (a smoke run of the multi-rank
+    # harness on a smaller box) share devices and use gloo for the control
+    # collectives, since NCCL refuses two ranks on one GPU
+    shared = world > n_dev
+    torch.cuda.set_device(local % n_dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     try:
         if args.config == "big":
             run_big(args, cfg, rank, world)

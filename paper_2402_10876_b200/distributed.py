@@ -226,6 +226,12 @@ class TwShardedPlan:
         if self.world == 1:
             buf.copy_(local)
             return buf, None
+        if local.is_cuda and dist.get_backend(self.group) != "nccl":
+            # a host-only backend (gloo, e.g. ranks sharing one GPU): stage on the host
+            host = torch.empty((self.tallest * self.world, m), dtype=local.dtype)
+            dist.all_gather_into_tensor(host, local.cpu(), group=self.group)
+            buf.copy_(host)
+            return buf, None
         work = dist.all_gather_into_tensor(buf, local, group=self.group, async_op=async_op)
         return buf, work
 
