@@ -79,6 +79,9 @@ typedef struct tw_plan_info {
                                  which every tile's kept rows form runs     */
   int32_t row_copies;         /* rows of the plan layout = row_copies * k
                                  (one row order per group of tiles)         */
+  int32_t sm_budget;          /* SMs K1 uses (tw_plan_set_sm_budget)     */
+  int64_t stage_work;         /* sum over sub-tiles of 64-row k-steps: the
+                                 per-token cost model of the work split     */
 } tw_plan_info;
 
 /* Build a device plan from a CTO encoding held in host memory.
@@ -110,6 +113,13 @@ TW_API int tw_plan_attach_overlay(tw_plan* plan, int32_t k, int32_t n, int64_t n
                            void* stream);
 
 TW_API int tw_plan_get_info(const tw_plan* plan, tw_plan_info* info);
+
+/* Number of SMs the plan's product kernel (K1) may occupy (0 = all of the
+ * device).  With a budget below the SM count, several plans launched on
+ * concurrent streams run side by side (a grouped step over independent
+ * layers, paper_2402_10876_b200.TwPlanGroup); the work split over the
+ * budget mirrors the LPT balancing of executor.py:206-227. */
+TW_API int tw_plan_set_sm_budget(tw_plan* plan, int32_t sms);
 
 /* Output column maps (host buffers sized n_condensed / n_union):
  * original column id of every row of C'^T. */

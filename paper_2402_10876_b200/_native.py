@@ -35,7 +35,7 @@ class PlanInfo(ctypes.Structure):
                 ("bn", _i32), ("kp", _i32), ("n_condensed", _i32), ("n_union", _i32),
                 ("compute_dtype", _i32), ("nnz", _i64), ("kept_macs_per_token", _i64),
                 ("sm_count", _i32), ("has_overlay", _i32), ("row_runs", _i32),
-                ("row_copies", _i32)]
+                ("row_copies", _i32), ("sm_budget", _i32), ("stage_work", _i64)]
 
 
 # name -> (restype, argtypes); must match include/tw_gemm.h exactly
@@ -44,6 +44,7 @@ SIGNATURES = {
                                     _u32p, _i32, _u32p, _i32, _f32p, _i32, _i32, _i32, _vp]),
     "tw_plan_attach_overlay": (_c_int, [_vp, _i32, _i32, _i64, _i64p, _i64p, _f32p, _vp]),
     "tw_plan_get_info": (_c_int, [_vp, ctypes.POINTER(PlanInfo)]),
+    "tw_plan_set_sm_budget": (_c_int, [_vp, _i32]),
     "tw_plan_condensed_columns": (_c_int, [_vp, _i32p]),
     "tw_plan_union_columns": (_c_int, [_vp, _i32p]),
     "tw_gemm": (_c_int, [_vp, _vp, _i64, _i64, _vp, _i64, _i32, _vp]),

@@ -142,6 +142,8 @@ struct tw_plan {
   bool owner = false;                    // n_sub <= SMs: one sub-tile per CTA
   bool resident = false;                 // owner and every payload fits in smem
   std::vector<int32_t> cta_first;        // owner mode: [n_sub + 1]
+  int32_t sm_budget = 0;                 // SMs K1 may use (<= sm_count; tw_plan_set_sm_budget)
+  std::vector<double> tile_cost;         // owner split weight per tile (run path)
   // row-run layout: A^T rows permuted so each tile's kept rows form a few
   // runs; position p holds original row perm[p] (empty = not used)
   bool runs = false;
@@ -194,6 +196,54 @@ struct tw_plan {
     ov.release();
   }
 };
+
+// Owner-mode split over the plan's SM budget G: sub-tile s gets c_s CTAs,
+// c_s proportional to its per-token cost, largest remainder, at least one
+// each.  Mirrors the LPT balancing of executor.py:206-227.  Plans with more
+// sub-tiles than G run the strided decomposition instead.
+static void owner_split(tw_plan* plan) {
+  const int G = plan->sm_budget;
+  plan->cta_first.clear();
+  plan->owner = plan->n_sub <= G && G <= kMaxCtas;
+  plan->resident = false;
+  if (!plan->owner) return;
+  // weight (per token): k-steps, or (row-run plans) the stages' TMA issue
+  // cost, plus a fixed per-unit share for the epilogue and pipeline fill,
+  // which dominates short-K' sub-tiles (TEW 768x3072 keeps K' = 1 on one
+  // tile: proportional-to-k-steps gave it 2 CTAs for all 8192 tokens)
+  std::vector<int32_t> c(plan->n_sub, 1);
+  std::vector<double> wt(plan->n_sub);
+  double w = 0;
+  for (int i = 0; i < plan->n_sub; ++i) {
+    const SubTile& st = plan->subtiles[i];
+    wt[i] = plan->runs ? plan->tile_cost[st.idx_row] + env_int("TW_RUN_FIX", 48)
+                       : (double)st.kp_steps + 3.0;
+    w += wt[i];
+  }
+  std::vector<std::pair<double, int>> frac;
+  int used = 0;
+  for (int i = 0; i < plan->n_sub; ++i) {
+    const double q = (double)G * wt[i] / w;
+    c[i] = std::max(1, (int)q);
+    used += c[i];
+    frac.push_back({q - (int)q, i});
+  }
+  std::stable_sort(frac.begin(), frac.end(),
+                   [](const std::pair<double, int>& a, const std::pair<double, int>& b) {
+                     return a.first > b.first;
+                   });
+  for (size_t t = 0; used < G && t < frac.size(); ++t, ++used) c[frac[t].second] += 1;
+  while (used > G) {  // only when the max(1, .) floor overshot
+    int big = (int)(std::max_element(c.begin(), c.end()) - c.begin());
+    c[big] -= 1;
+    --used;
+  }
+  plan->cta_first.assign(plan->n_sub + 1, 0);
+  for (int i = 0; i < plan->n_sub; ++i) plan->cta_first[i + 1] = plan->cta_first[i] + c[i];
+  int max_steps = 0;
+  for (const SubTile& st : plan->subtiles) max_steps = std::max(max_steps, (int)st.kp_steps);
+  plan->resident = max_steps <= kResSteps && !env_int("TW_NO_RESIDENT", 0);
+}
 
 extern "C" {
 
@@ -522,49 +572,9 @@ int tw_plan_create_cto(tw_plan** out, int32_t k, int32_t n, int32_t g, int32_t n
   }
   (void)off;
 
-  // Owner-mode split: sub-tile s gets c_s CTAs, c_s proportional to its
-  // k-steps (the per-token cost of its gather and MMA), largest remainder,
-  // at least one each.  Mirrors the LPT balancing of executor.py:206-227.
-  const int G = plan->sm_count;
-  plan->owner = plan->n_sub <= G && G <= kMaxCtas;
-  if (plan->owner) {
-    // weight (per token): k-steps, or (row-run plans) the stages' TMA issue
-    // cost, plus a fixed per-unit share for the epilogue and pipeline
-    // fill, which dominates short-K' sub-tiles (TEW 768x3072 keeps K' = 1 on
-    // one tile: proportional-to-k-steps gave it 2 CTAs for all 8192 tokens)
-    std::vector<int32_t> c(plan->n_sub, 1);
-    std::vector<double> wt(plan->n_sub);
-    double w = 0;
-    for (int i = 0; i < plan->n_sub; ++i) {
-      const SubTile& st = plan->subtiles[i];
-      wt[i] = plan->runs ? tile_cost[st.idx_row] + env_int("TW_RUN_FIX", 48)
-                         : (double)st.kp_steps + 3.0;
-      w += wt[i];
-    }
-    std::vector<std::pair<double, int>> frac;
-    int used = 0;
-    for (int i = 0; i < plan->n_sub; ++i) {
-      const double q = (double)G * wt[i] / w;
-      c[i] = std::max(1, (int)q);
-      used += c[i];
-      frac.push_back({q - (int)q, i});
-    }
-    std::stable_sort(frac.begin(), frac.end(),
-                     [](const std::pair<double, int>& a, const std::pair<double, int>& b) {
-                       return a.first > b.first;
-                     });
-    for (size_t t = 0; used < G && t < frac.size(); ++t, ++used) c[frac[t].second] += 1;
-    while (used > G) {  // only when the max(1, .) floor overshot
-      int big = (int)(std::max_element(c.begin(), c.end()) - c.begin());
-      c[big] -= 1;
-      --used;
-    }
-    plan->cta_first.assign(plan->n_sub + 1, 0);
-    for (int i = 0; i < plan->n_sub; ++i) plan->cta_first[i + 1] = plan->cta_first[i] + c[i];
-    int max_steps = 0;
-    for (const SubTile& st : plan->subtiles) max_steps = std::max(max_steps, (int)st.kp_steps);
-    plan->resident = max_steps <= kResSteps && !env_int("TW_NO_RESIDENT", 0);
-  }
+  plan->tile_cost = tile_cost;
+  plan->sm_budget = plan->sm_count;
+  owner_split(plan);
 
   if (int st = upload(&plan->d_subtiles, plan->subtiles, s)) return st;
   if (int st = upload(&plan->d_gidx, gidx, s)) return st;
@@ -784,6 +794,18 @@ int tw_plan_attach_overlay(tw_plan* p, int32_t k, int32_t n, int64_t nnz, const 
   return TW_OK;
 }
 
+int tw_plan_set_sm_budget(tw_plan* p, int32_t sms) {
+  g_last_error.clear();
+  if (!p) return fail(TW_ERR_INVALID_INPUT, "plan is null");
+  if (sms < 0) return fail(TW_ERR_INVALID_INPUT, "sm budget must be >= 0");
+  const int32_t b = sms == 0 ? p->sm_count : std::min(sms, p->sm_count);
+  if (b != p->sm_budget) {
+    p->sm_budget = b;
+    owner_split(p);
+  }
+  return TW_OK;
+}
+
 int tw_plan_get_info(const tw_plan* p, tw_plan_info* info) {
   if (!p || !info) return fail(TW_ERR_INVALID_INPUT, "null argument");
   info->k = p->k;
@@ -802,6 +824,10 @@ int tw_plan_get_info(const tw_plan* p, tw_plan_info* info) {
   info->has_overlay = p->has_overlay ? 1 : 0;
   info->row_runs = p->runs ? 1 : 0;
   info->row_copies = p->runs ? p->row_copies : 1;
+  info->sm_budget = p->sm_budget;
+  int64_t steps = 0;
+  for (const SubTile& st : p->subtiles) steps += st.kp_steps;
+  info->stage_work = steps;
   return TW_OK;
 }
 
@@ -856,6 +882,7 @@ static int run_tw(const tw_plan* p, const void* x, int64_t m, int64_t ld_x, void
   a.trace = g_trace;
   const int esz = out_dtype == kF32 ? 4 : 2;
   a.vec_ok = ((ld_ct * esz) % 16 == 0 && reinterpret_cast<uintptr_t>(ct) % 16 == 0) ? 1 : 0;
+  a.vec32_ok = ((ld_ct * esz) % 32 == 0 && reinterpret_cast<uintptr_t>(ct) % 32 == 0) ? 1 : 0;
   // condensed 16-bit output: 32 x 16 blocks leave through TMA 2-D stores
   CUtensorMap map_out;
   std::memset(&map_out, 0, sizeof(map_out));
@@ -882,7 +909,7 @@ static int run_tw(const tw_plan* p, const void* x, int64_t m, int64_t ld_x, void
       max_steps = std::max<int64_t>(max_steps, p->subtiles[sidx].kp_steps);
     }
     const int64_t units = (int64_t)p->n_sub * ((m + kTN - 1) / kTN);
-    const int64_t strided = (units + p->sm_count - 1) / p->sm_count * kTN * max_steps;
+    const int64_t strided = (units + p->sm_budget - 1) / p->sm_budget * kTN * max_steps;
     if (strided < own) owner = false;
   }
   if (owner) {
@@ -921,7 +948,7 @@ static int run_tw(const tw_plan* p, const void* x, int64_t m, int64_t ld_x, void
   } else {
     a.owner = 0;
     a.n_units = (int32_t)(p->n_sub * ((m + kTN - 1) / kTN));
-    grid = std::min(a.n_units, p->sm_count);
+    grid = std::min(a.n_units, p->sm_budget);
   }
   bool resident = a.owner && p->resident;
   // Plan-layout input: TMA row runs unless a CTA has many units.  Runs win

@@ -179,8 +179,8 @@ __device__ __forceinline__ void epilogue_rows(const GemmArgs& args, const CUtens
   const int esz = args.out_dtype == kF32 ? 4 : 2;
   uint8_t* row_base =
       static_cast<uint8_t*>(args.out) + static_cast<int64_t>(orow) * args.ld_out * esz;
-  uint32_t w[16];
   if (ntok <= 0) return;
+  uint32_t w[16];
   tmem_ld_32x32b_x16(t0, w);
 #pragma unroll 1
   for (int c = 0; c < ntok; c += 16) {
@@ -373,8 +373,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       Walker w0 = walk;
       Seg s0;
       if (w0.next(args, s0)) {
+        const bool skip_p = flags & kFlagSkipP;
         for (int ks = 0; ks < s0.d.kp_steps; ++ks) {
           if (!args.runs) mbar_wait(&empty[ks % kStages], ((ks / kStages) & 1) ^ 1u);
+          if (skip_p) {
+            mbar_arrive(&pfull[ks]);
+            continue;
+          }
           mbar_arrive_expect_tx(&pfull[ks], kPBytes);
           tma_load_2d(sP + ks * kPBytes, &map_pay, &pfull[ks], ks * kBK, s0.d.pay_row);
         }
@@ -401,14 +406,16 @@ __global__ void __launch_bounds__(kThreads, 1)
             trace[gs] = clock64();
             trace[3076] += b1 - b0;
           }
+          const bool skip_p = kRes || (flags & kFlagSkipP);
+          const bool skip_a = flags & kFlagSkipA;
           if (lane == 0) {
-            mbar_arrive_expect_tx(&full[stage], (kRes ? 0u : static_cast<uint32_t>(kPBytes)) +
-                                                    static_cast<uint32_t>(chunks * kBK * 128));
-            if (!kRes)
+            mbar_arrive_expect_tx(&full[stage], (skip_p ? 0u : static_cast<uint32_t>(kPBytes)) +
+                                                    (skip_a ? 0u : static_cast<uint32_t>(chunks * kBK * 128)));
+            if (!skip_p)
               tma_load_2d(sP + stage * kPBytes, &map_pay, &full[stage], ks * kBK, sg.d.pay_row);
           }
           __syncwarp();
-          for (int j = b0 + lane, jj = 0; j < b1; j += 32, jj += 32) {
+          for (int j = b0 + lane, jj = 0; j < b1 && !skip_a; j += 32, jj += 32) {
             const uint32_t ej = jj == 0 ? e : __ldg(args.boxes + j);
             const int slot = static_cast<int>(ej & 63u), code = static_cast<int>((ej >> 6) & 7u);
             const int32_t pos = static_cast<int32_t>(ej >> 9);
@@ -427,6 +434,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int stage = gs % kStages;
           mbar_wait(&empty[stage], ((gs / kStages) & 1) ^ 1u);
           if (trace && gs < 1024) trace[gs] = clock64();
+          if (flags & kFlagSkipP) {
+            mbar_arrive(&full[stage]);
+            continue;
+          }
           mbar_arrive_expect_tx(&full[stage], kPBytes);
           tma_load_2d(sP + stage * kPBytes, &map_pay, &full[stage], ks * kBK, sg.d.pay_row);
         }

@@ -61,6 +61,7 @@ struct GemmArgs {
   int32_t owner;            // 1 = one sub-tile + token range per CTA (WorkTable), 0 = strided units
   int32_t flags;            // diagnostics (kFlag*); 0 in production
   int32_t vec_ok;           // output rows 16-byte aligned: vector stores allowed
+  int32_t vec32_ok;         // output rows 32-byte aligned: 32-byte (full-sector) stores
   int32_t use_tma_store;    // map_out valid (16-bit output): 32 x 16 blocks via TMA stores
   long long* trace;         // optional per-CTA clock64 trace (4096 entries per CTA)
   // row-run path (x in the plan's permuted row layout): activation stages are
@@ -83,6 +84,7 @@ constexpr int32_t kFlagSkipA = 1;       // do not load the activations
 constexpr int32_t kFlagSkipStore = 2;   // do not write the output
 constexpr int32_t kFlagSkipMma = 4;     // do not issue tcgen05.mma
 constexpr int32_t kFlagNoPdl = 8;       // launch without programmatic dependent launch (timing only)
+constexpr int32_t kFlagSkipP = 16;      // do not load the payload
 
 // K1: persistent warp-specialised TW GEMM (tcgen05 + TMA + cp.async gather).
 //   map_pay : payload [n_sub * kBN][Kp], box {64 k, kBN rows}, 128-B swizzle

@@ -172,6 +172,13 @@ class TwPlan:
             _native.stream_handle()))
         self._refresh_info()
 
+    def set_sm_budget(self, sms: int) -> None:
+        """Let K1 occupy at most ``sms`` SMs (0: all), so several plans
+        launched on concurrent streams share the GPU (see TwPlanGroup)."""
+        lib = _native.load_library()
+        _native.check(lib.tw_plan_set_sm_budget(self._handle, int(sms)))
+        self._refresh_info()
+
     def flops(self, m: int, tew: bool = False) -> int:
         """Surviving FLOPs of one product (metrics.py:114-117)."""
         macs = self.info.kept_macs_per_token if tew else self.info.kept_macs_per_token - self.info.nnz
