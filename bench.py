@@ -400,6 +400,170 @@ def capture_graph(fn):
     return g
 
 
+def graph_us(fn, n_calls: int, reps: int = 5) -> float:
+    """Median microseconds per call of fn(0..n_calls-1) captured in one CUDA
+    graph (back-to-back launches, programmatic dependent launch between
+    them), CUDA events on the replaying stream."""
+    import torch
+
+    g = capture_graph(lambda: [fn(i) for i in range(n_calls)])
+    g.replay()
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    ts = []
+    for _ in range(reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        g.replay()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1) * 1e3 / n_calls)
+    del g
+    return statistics.median(ts)
+
+
+def fork_join(fns):
+    """Run fns on side streams forked from / joined back to the current one
+    (graph-capturable): the cuBLAS counterpart of TwPlanGroup."""
+    import torch
+
+    cur = torch.cuda.current_stream()
+    ev = torch.cuda.Event()
+    ev.record(cur)
+    if not hasattr(fork_join, "streams"):
+        fork_join.streams = [torch.cuda.Stream() for _ in range(8)]
+    joins = []
+    for s, fn in zip(fork_join.streams, fns):
+        s.wait_event(ev)
+        with torch.cuda.stream(s):
+            fn()
+        e = torch.cuda.Event()
+        e.record(s)
+        joins.append(e)
+    for e in joins:
+        cur.wait_event(e)
+
+
+def extra_measurements(cfg, layers, sets, rank, dense_ms, ms_step, tew):
+    """Numbers reported beside the headline:
+    natural-layout step (plain A^T, what cuBLAS reads), cold per-layer K1
+    launches (12 buffer sets > L2), the grouped step (TwPlanGroup over SM
+    shares, vs cuBLAS on three forked streams) and, for configs[1], the BERT
+    FFN pair chained in the row-run layout (chain_plans)."""
+    import torch
+
+    import paper_2402_10876_b200 as tw
+
+    dev = torch.device("cuda", torch.cuda.current_device())
+    m = cfg["m"]
+    R = len(sets)
+    out = {}
+    run = (lambda p, x, o, **kw: p.run_tew(x, out=o, **kw)) if tew else \
+        (lambda p, x, o, **kw: p.run(x, out=o, **kw))
+
+    # natural layout: plain A^T (the original row order), cp.async gather
+    nat = [[tw.prepare_activations(torch.from_numpy(activations(cfg, L["k"], li, rank)).to(dev))
+            for li, L in enumerate(layers)] for _ in range(R)]
+
+    def nat_step(i):
+        for (plan, _, ct), x in zip(sets[i % R], nat[i % R]):
+            run(plan, x, ct, x_layout="natural")
+
+    us_nat = graph_us(nat_step, 4 * R)
+    out["natural_layout"] = {"ms_per_step": us_nat / 1e3,
+                             "speedup_vs_cublas": dense_ms / (us_nat / 1e3),
+                             "what": "same step on plain A^T (original row order; the layout "
+                                     "cuBLAS reads): kept rows gathered with cp.async"}
+    del nat
+
+    # cold per-layer launches: 12 (A^T, C'^T) sets per layer (> L2 for every layer)
+    cold = []
+    for li, L in enumerate(layers):
+        bufs = []
+        for j in range(12):
+            plan, at, ct = sets[j % R][li]
+            bufs.append((plan, at.clone(), torch.empty_like(ct)))
+        us = graph_us(lambda i, b=bufs: run(b[i % 12][0], b[i % 12][1], b[i % 12][2]), 36)
+        cold.append({"shape": f"{L['k']}x{L['n']}", "us": us,
+                     "gbs": L["bytes"] / (us * 1e-6) / 1e9,
+                     "tflops": L["flops"] / (us * 1e-6) / 1e12})
+        del bufs
+    out["per_layer_cold"] = cold
+
+    # grouped step: the three independent layers on SM shares, concurrent streams
+    groups = [tw.TwPlanGroup([p for p, _, _ in sets[r]], m) for r in range(R)]
+
+    def grp_step(i):
+        plans_xs = sets[i % R]
+        g = groups[i % R]
+        if tew:
+            g.run_tew([x for _, x, _ in plans_xs], [o for _, _, o in plans_xs])
+        else:
+            g.run([x for _, x, _ in plans_xs], [o for _, _, o in plans_xs])
+
+    us_grp = graph_us(grp_step, 4 * R)
+    budgets = groups[0].budgets
+    for g in groups:
+        g.release()
+    dense = []
+    for r in range(R):
+        row = []
+        for li, L in enumerate(layers):
+            wt = torch.from_numpy(np.ascontiguousarray(L["w"].T)).to(dev, torch.float16)
+            at = torch.randn((L["k"], m), device=dev, dtype=torch.float16)
+            row.append((wt, at, torch.empty((L["n"], m), dtype=torch.float16, device=dev)))
+        dense.append(row)
+    us_d3 = graph_us(lambda i: fork_join([lambda d=d: torch.matmul(d[0], d[1], out=d[2])
+                                          for d in dense[i % R]]), 4 * R)
+    out["grouped"] = {"ms_per_step": us_grp / 1e3, "sm_budgets": budgets,
+                      "cublas_3_streams_ms": us_d3 / 1e3,
+                      "speedup_vs_cublas_3_streams": us_d3 / us_grp,
+                      "speedup_vs_cublas": dense_ms / (us_grp / 1e3),
+                      "what": "TwPlanGroup: each layer on an SM share (LPT split over it), "
+                              "concurrent streams; cuBLAS forked onto 3 streams the same way"}
+    del dense
+
+    # BERT FFN chained in the row-run layout (configs[1] layers 768x3072 -> 3072x768)
+    if not tew and len(layers) == 3:
+        L1, L2 = layers[1], layers[2]
+        prev, nxt = tw.chain_plans(L1["enc"], L2["enc"])
+        xs = [tw.prepare_activations(torch.from_numpy(activations(cfg, L1["k"], 1, rank))
+                                     .to(dev)) for _ in range(R)]
+        hs = [torch.empty((prev.info.n_condensed, m), dtype=torch.float16, device=dev)
+              for _ in range(R)]
+        ys = [torch.empty((nxt.info.n_condensed, m), dtype=torch.float16, device=dev)
+              for _ in range(R)]
+
+        def chain_step(i):
+            prev.run(xs[i % R], out=hs[i % R])
+            nxt.run(hs[i % R], out=ys[i % R])
+
+        us_chain = graph_us(chain_step, 4 * R)
+        w1 = torch.from_numpy(np.ascontiguousarray(L1["w"].T)).to(dev, torch.float16)
+        w2 = torch.from_numpy(np.ascontiguousarray(L2["w"].T)).to(dev, torch.float16)
+        dh = [torch.empty((L1["n"], m), dtype=torch.float16, device=dev) for _ in range(R)]
+        dy = [torch.empty((L2["n"], m), dtype=torch.float16, device=dev) for _ in range(R)]
+
+        def dense_chain(i):
+            torch.matmul(w1, xs[i % R], out=dh[i % R])
+            torch.matmul(w2, dh[i % R], out=dy[i % R])
+
+        us_dchain = graph_us(dense_chain, 4 * R)
+        fl = prev.flops(m) + nxt.flops(m)
+        out["ffn_chain"] = {
+            "ms": us_chain / 1e3, "cublas_ms": us_dchain / 1e3,
+            "speedup_vs_cublas": us_dchain / us_chain,
+            "tflops_effective": fl / (us_chain * 1e-6) / 1e12,
+            "next_uses_row_runs": bool(nxt.uses_row_runs),
+            "next_kept_rows": int(nxt.info.kept_macs_per_token // max(1, nxt.info.n_condensed)),
+            "what": "768x3072 -> 3072x768 chained: layer 1's epilogue writes C'^T in layer 2's "
+                    "row-run order (chain_plans), layer 2 reads it with TMA boxes; layer 2 "
+                    "skips its rows on layer 1's pruned columns (exact zeros)"}
+        del xs, hs, ys, dh, dy, prev, nxt
+    torch.cuda.empty_cache()
+    return out
+
+
 def run_ours(args, cfg, rank: int, world: int) -> None:
     import torch
     import torch.distributed as dist
@@ -641,6 +805,8 @@ def run_ours(args, cfg, rank: int, world: int) -> None:
                      "peak_source": pk["source"], "arithmetic_intensity": ai,
                      "layers": per_layer})
 
+    extra = extra_measurements(cfg, layers, sets, rank, dense_ms, ms_step, tew)
+
     # CPU baseline: the reference's own CPU path on this host, bounded sample
     m_sample = min(m, 1024)
     cpu_rate, cpu_s, _, workers, cpu_kind = cpu_reference_rate(cfg, layers, m_sample)
@@ -684,6 +850,7 @@ def run_ours(args, cfg, rank: int, world: int) -> None:
                          "value_1_worker": cpu1_rate,
                          "sample_1_worker": f"{max(64, m_sample // 4)} tokens, 1 lane ({cpu1_s:.1f} s)",
                          "port_matches_reference": port_ok},
+        **extra,
         "gpu_launches": args.steps * len(layers) * (2 if tew else 1),
         "launch": "CUDA graph per step (one graph per rotating buffer set)",
         "clocks": clocks,

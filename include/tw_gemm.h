@@ -103,6 +103,29 @@ TW_API int tw_plan_create_cto(tw_plan** out, int32_t k, int32_t n, int32_t g, in
                        const uint32_t* col_offsets, int32_t max_cols, const float* payload,
                        int32_t compute_dtype, int32_t schedule, int32_t row_runs, void* stream);
 
+/* tw_plan_create_cto with the chained-layer options:
+ *   row_groups [n_groups + 1]: bounds 0 = b_0 < ... < b_n = k of row groups;
+ *     the row-run permutation (row_runs = 1) then only reorders rows inside
+ *     each group (NULL: unconstrained).  Pass the previous layer's
+ *     tw_plan_output_groups so that its epilogue can write this plan's layout.
+ *   out_row_of_cond [N']: the C'^T row each condensed column is written to;
+ *     it may only permute rows inside each 128-column sub-tile block (free:
+ *     the payload rows are reordered), so a layer writes its output directly
+ *     in the next layer's row-run order (NULL: condensed order).
+ * tw_plan_condensed_columns then reports the original column of every output
+ * row in that order. */
+TW_API int tw_plan_create_cto_ex(tw_plan** out, int32_t k, int32_t n, int32_t g, int32_t n_tiles,
+                                 const uint32_t* row_counts, const uint32_t* col_counts,
+                                 const uint32_t* row_offsets, int32_t max_rows,
+                                 const uint32_t* col_offsets, int32_t max_cols,
+                                 const float* payload, int32_t compute_dtype, int32_t schedule,
+                                 int32_t row_runs, const int32_t* row_groups, int32_t n_groups,
+                                 const int32_t* out_row_of_cond, void* stream);
+
+/* Row blocks of C'^T written by one sub-tile each (host buffer of n_sub + 1
+ * ascending bounds): the groups tw_plan_create_cto_ex may permute within. */
+TW_API int tw_plan_output_groups(const tw_plan* plan, int32_t* bounds);
+
 /* Attach a TEW overlay (CSC, int64 like patterns.SparseOverlay,
  * patterns.py:145-214).  Replaces the overlap/dims checks of
  * executor.gemm_tew (executor.py:186-193): dims mismatch -> TW_ERR_INVALID_INPUT,
@@ -146,6 +169,13 @@ TW_API int tw_gemm_ex(const tw_plan* plan, const void* at, int64_t m, int64_t ld
  * executor.py:158) for inputs of this plan. */
 TW_API int tw_plan_prepare(const tw_plan* plan, const void* a, int32_t a_dtype, int64_t m,
                            int64_t lda, void* at, int64_t ld_at, void* stream);
+
+/* A natural-order A^T (k x m, pitch ld_at, compute dtype) -> the plan's row
+ * layout (row_copies * k x m, pitch ld_x): row perm[p] copied to position p
+ * (a plain copy for plans without row runs).  The device form of
+ * tw_plan_row_order for callers that already hold A^T. */
+TW_API int tw_plan_permute_rows(const tw_plan* plan, const void* at, int64_t m, int64_t ld_at,
+                                void* x, int64_t ld_x, void* stream);
 
 /* Original K row held at each position of the plan's row layout (host buffer
  * of row_copies * k entries; the identity when row_runs == 0). */

@@ -42,6 +42,10 @@ class PlanInfo(ctypes.Structure):
 SIGNATURES = {
     "tw_plan_create_cto": (_c_int, [ctypes.POINTER(_vp), _i32, _i32, _i32, _i32, _u32p, _u32p,
                                     _u32p, _i32, _u32p, _i32, _f32p, _i32, _i32, _i32, _vp]),
+    "tw_plan_create_cto_ex": (_c_int, [ctypes.POINTER(_vp), _i32, _i32, _i32, _i32, _u32p, _u32p,
+                                       _u32p, _i32, _u32p, _i32, _f32p, _i32, _i32, _i32, _i32p,
+                                       _i32, _i32p, _vp]),
+    "tw_plan_output_groups": (_c_int, [_vp, _i32p]),
     "tw_plan_attach_overlay": (_c_int, [_vp, _i32, _i32, _i64, _i64p, _i64p, _f32p, _vp]),
     "tw_plan_get_info": (_c_int, [_vp, ctypes.POINTER(PlanInfo)]),
     "tw_plan_set_sm_budget": (_c_int, [_vp, _i32]),
@@ -51,6 +55,7 @@ SIGNATURES = {
     "tw_gemm_ex": (_c_int, [_vp, _vp, _i64, _i64, _vp, _i64, _i32, _i32, _vp]),
     "tw_plan_prepare": (_c_int, [_vp, _vp, _i32, _i64, _i64, _vp, _i64, _vp]),
     "tw_plan_row_order": (_c_int, [_vp, _i32p]),
+    "tw_plan_permute_rows": (_c_int, [_vp, _vp, _i64, _i64, _vp, _i64, _vp]),
     "tw_gemm_tew": (_c_int, [_vp, _vp, _i64, _i64, _vp, _i64, _i32, _vp]),
     "tw_gemm_tew_ws": (_c_int, [_vp, _vp, _i64, _i64, _vp, _i64, _i32, _vp, ctypes.c_uint64, _vp]),
     "tw_gemm_tew_ex": (_c_int, [_vp, _vp, _i64, _i64, _vp, _i64, _i32, _vp, ctypes.c_uint64, _i32,

@@ -69,4 +69,34 @@ def chain_encoding(enc_next: CtoEncoding, prev_columns) -> CtoEncoding:
                        payload=np.concatenate([p.ravel() for p in payload_out]))
 
 
-__all__ = ["chain_encoding"]
+def chain_plans(enc_prev: CtoEncoding, enc_next: CtoEncoding, compute_dtype: str = "fp16"):
+    """Two device plans for layer l -> layer l+1 in the row-run layout.
+
+    Layer l+1 is re-encoded over layer l's condensed output rows
+    (:func:`chain_encoding`) and gets a row-run layout whose permutation stays
+    inside each 128-row block that one of layer l's sub-tiles writes; layer l
+    is then built with that permutation as its output row order (payload rows
+    reordered inside each sub-tile, so its TMA-store epilogue is unchanged).
+    Layer l's C'^T is therefore already layer l+1's plan-layout A^T: the
+    second product reads it with dense TMA boxes, with no prepare / permute
+    pass between them.  Returns ``(prev, next)``; ``prev.condensed_columns``
+    lists the original column of each of its output rows in that order.
+    """
+    from .executor import TwPlan
+
+    probe = TwPlan(enc_prev, compute_dtype=compute_dtype)
+    groups = probe.output_groups()
+    cols = probe.condensed_columns
+    del probe
+    chained = chain_encoding(enc_next, cols)
+    nxt = TwPlan(chained, compute_dtype=compute_dtype, row_layout="runs", row_groups=groups)
+    if nxt.uses_row_runs:
+        order = np.empty(nxt.row_order.size, dtype=np.int64)
+        order[nxt.row_order] = np.arange(nxt.row_order.size)   # condensed col -> position
+        prev = TwPlan(enc_prev, compute_dtype=compute_dtype, out_order=order)
+    else:
+        prev = TwPlan(enc_prev, compute_dtype=compute_dtype)
+    return prev, nxt
+
+
+__all__ = ["chain_encoding", "chain_plans"]

@@ -287,16 +287,23 @@ __global__ void __launch_bounds__(256)
 
 // ct[u] = src[src_row[u]] or 0: the caller's tile product placed at the union
 // rows (GemmOutput.expand + re-condense of executor.py:194-203, on the device).
+// Also the row permutation of a natural-order A^T into a plan's row-run
+// layout (TwPlan.prepare(at=...)): 16-byte copies when rows are aligned.
 __global__ void scatter_rows_kernel(const uint8_t* src, int64_t ld_src, const int32_t* src_row,
-                                    uint8_t* dst, int64_t ld_dst, int64_t M, int esz) {
+                                    uint8_t* dst, int64_t ld_dst, int64_t M, int esz, int vec) {
   const int u = blockIdx.y;
   const int sr = __ldg(src_row + u);
   const int64_t bytes = M * esz;
   uint8_t* d = dst + static_cast<int64_t>(u) * ld_dst * esz;
   const uint8_t* s = sr >= 0 ? src + static_cast<int64_t>(sr) * ld_src * esz : nullptr;
-  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < bytes;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
-    d[i] = s ? s[i] : 0;
+  const int64_t t0 = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t step = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  if (vec) {
+    for (int64_t i = t0; i < bytes / 16; i += step)
+      reinterpret_cast<uint4*>(d)[i] = s ? reinterpret_cast<const uint4*>(s)[i] : make_uint4(0, 0, 0, 0);
+    return;
+  }
+  for (int64_t i = t0; i < bytes; i += step) d[i] = s ? s[i] : 0;
 }
 
 // 32 x 32 shared-memory transpose with dtype conversion (general fallback).
@@ -472,10 +479,14 @@ cudaError_t launch_scatter_rows(const void* src, int64_t ld_src, const int32_t* 
                                 cudaStream_t stream) {
   if (n_rows <= 0 || M <= 0) return cudaSuccess;
   const int64_t bytes = M * esz;
-  unsigned gx = static_cast<unsigned>(std::min<int64_t>((bytes + 255) / 256, 64));
+  const int vec = bytes % 16 == 0 && (ld_src * esz) % 16 == 0 && (ld_dst * esz) % 16 == 0 &&
+                  reinterpret_cast<uintptr_t>(src) % 16 == 0 &&
+                  reinterpret_cast<uintptr_t>(dst) % 16 == 0;
+  const int64_t items = vec ? bytes / 16 : bytes;
+  unsigned gx = static_cast<unsigned>(std::min<int64_t>((items + 255) / 256, 64));
   dim3 grid(gx, static_cast<unsigned>(n_rows));
   scatter_rows_kernel<<<grid, 256, 0, stream>>>(static_cast<const uint8_t*>(src), ld_src, src_row,
-                                                static_cast<uint8_t*>(dst), ld_dst, M, esz);
+                                                static_cast<uint8_t*>(dst), ld_dst, M, esz, vec);
   return cudaGetLastError();
 }
 

@@ -256,10 +256,35 @@ int tw_plan_create_cto(tw_plan** out, int32_t k, int32_t n, int32_t g, int32_t n
                        const uint32_t* row_offsets, int32_t max_rows,
                        const uint32_t* col_offsets, int32_t max_cols, const float* payload,
                        int32_t compute_dtype, int32_t schedule, int32_t row_runs, void* stream) {
+  return tw_plan_create_cto_ex(out, k, n, g, n_tiles, row_counts, col_counts, row_offsets,
+                               max_rows, col_offsets, max_cols, payload, compute_dtype, schedule,
+                               row_runs, nullptr, 0, nullptr, stream);
+}
+
+int tw_plan_create_cto_ex(tw_plan** out, int32_t k, int32_t n, int32_t g, int32_t n_tiles,
+                          const uint32_t* row_counts, const uint32_t* col_counts,
+                          const uint32_t* row_offsets, int32_t max_rows,
+                          const uint32_t* col_offsets, int32_t max_cols, const float* payload,
+                          int32_t compute_dtype, int32_t schedule, int32_t row_runs,
+                          const int32_t* row_groups, int32_t n_groups,
+                          const int32_t* out_row_of_cond, void* stream) {
   g_last_error.clear();
   if (!out) return fail(TW_ERR_INVALID_INPUT, "out is null");
   *out = nullptr;
   if (k < 1 || n < 1 || g < 1) return fail(TW_ERR_INVALID_INPUT, "dims must be >= 1");
+  // row groups (chained layout): bounds 0 = b0 < b1 < ... < b_n = k; the
+  // row-run permutation then only moves rows within their group
+  std::vector<int32_t> grp_of;
+  if (row_groups) {
+    if (n_groups < 1 || row_groups[0] != 0 || row_groups[n_groups] != k)
+      return fail(TW_ERR_INVALID_INPUT, "row groups must cover [0, k) from 0 to k");
+    grp_of.resize(k);
+    for (int32_t gi = 0; gi < n_groups; ++gi) {
+      if (row_groups[gi + 1] <= row_groups[gi])
+        return fail(TW_ERR_INVALID_INPUT, "row group bounds must be strictly increasing");
+      for (int32_t r = row_groups[gi]; r < row_groups[gi + 1]; ++r) grp_of[r] = gi;
+    }
+  }
   if (compute_dtype != kF16 && compute_dtype != kBF16)
     return fail(TW_ERR_INVALID_INPUT, "compute dtype must be fp16 or bf16");
   if (schedule != TW_SCHEDULE_LPT && schedule != TW_SCHEDULE_ROUND_ROBIN)
@@ -419,7 +444,7 @@ int tw_plan_create_cto(tw_plan** out, int32_t k, int32_t n, int32_t g, int32_t n
   std::vector<double> tile_cost(nt, 0.0);  // owner split weight (run path)
   // More than one copy (layers with > 6 tiles) measured no faster than the
   // gather on BERT 768x3072 (G = 3: 21.0 vs 20.9 us), so it is opt-in.
-  const int max_copies = std::max(1, std::min(4, env_int("TW_RUN_COPIES", 1)));
+  const int max_copies = grp_of.empty() ? std::max(1, std::min(4, env_int("TW_RUN_COPIES", 1))) : 1;
   const double run_stage_w = env_int("TW_RUN_STAGE_W", 8);
   if (row_runs && k < (1 << 20) && !env_int("TW_NO_RUNS", 0)) {
     const int stride = kp / kBK + 1;
@@ -444,8 +469,15 @@ int tw_plan_create_cto(tw_plan** out, int32_t k, int32_t n, int32_t g, int32_t n
         int32_t* pg = perm.data() + (size_t)gi * k;
         int32_t* ig = inv.data() + (size_t)gi * k;
         std::iota(pg, pg + k, 0);
-        std::stable_sort(pg, pg + k,
-                         [&](int32_t x, int32_t y) { return gray_rank[sig[x]] < gray_rank[sig[y]]; });
+        if (grp_of.empty())
+          std::stable_sort(pg, pg + k, [&](int32_t x, int32_t y) {
+            return gray_rank[sig[x]] < gray_rank[sig[y]];
+          });
+        else  // chained layout: Gray order inside each row group, groups in place
+          std::stable_sort(pg, pg + k, [&](int32_t x, int32_t y) {
+            return grp_of[x] != grp_of[y] ? grp_of[x] < grp_of[y]
+                                           : gray_rank[sig[x]] < gray_rank[sig[y]];
+          });
         for (int32_t q = 0; q < k; ++q) ig[pg[q]] = gi * k + q;  // global layout position
         for (int i = t0; i < t1; ++i) {
           const int32_t h = (int32_t)rows[i].size();
@@ -493,7 +525,7 @@ int tw_plan_create_cto(tw_plan** out, int32_t k, int32_t n, int32_t g, int32_t n
         }
       }
       const double per_stage = stages ? (double)bx.size() / (double)stages : 1e9;
-      if (per_stage > (G == 1 ? 4.0 : 3.0)) continue;
+      if (per_stage > (!grp_of.empty() ? 8.0 : G == 1 ? 4.0 : 3.0)) continue;
       plan->runs = true;
       plan->row_copies = G;
       plan->perm = perm;
@@ -548,6 +580,42 @@ int tw_plan_create_cto(tw_plan** out, int32_t k, int32_t n, int32_t g, int32_t n
     pbase += (int64_t)h * w;
   }
   plan->n_sub = (int32_t)subs.size();
+
+  // Output row order (chained layout): condensed column c is written to
+  // C'^T row out_row_of_cond[c].  Only permutations inside each sub-tile's
+  // row block are allowed -- they cost nothing, the payload rows of the
+  // sub-tile (UMMA M = TMEM lanes = output rows) are reordered instead.
+  std::vector<float> pay_out;
+  if (out_row_of_cond) {
+    const int32_t nc = plan->n_cond;
+    std::vector<int32_t> inv(nc, -1);
+    for (int32_t c = 0; c < nc; ++c) {
+      const int32_t r = out_row_of_cond[c];
+      if (r < 0 || r >= nc || inv[r] >= 0)
+        return fail(TW_ERR_INVALID_INPUT, "output order must be a permutation of the %d columns", nc);
+      inv[r] = c;
+    }
+    pay_out.assign(pay_src, pay_src + pbase);
+    for (size_t si = 0; si < subs.size(); ++si) {
+      const SubTile& st = subs[si];
+      const int i = st.idx_row;
+      const int32_t h = (int32_t)rc[i];
+      const int64_t tile_base = src_base[si] - (int64_t)(st.out_row - tfc[i]) * h;
+      for (int32_t j = 0; j < st.width; ++j) {
+        const int32_t c = inv[st.out_row + j];
+        if (c < st.out_row || c >= st.out_row + st.width)
+          return fail(TW_ERR_INVALID_INPUT,
+                      "output order may only permute rows inside a 128-column sub-tile block");
+        std::copy(pay_src + tile_base + (int64_t)(c - tfc[i]) * h,
+                  pay_src + tile_base + (int64_t)(c - tfc[i] + 1) * h,
+                  pay_out.begin() + tile_base + (int64_t)(st.out_row + j - tfc[i]) * h);
+      }
+    }
+    std::vector<int32_t> cond2(nc);
+    for (int32_t r = 0; r < nc; ++r) cond2[r] = plan->cond_cols[inv[r]];
+    plan->cond_cols.swap(cond2);
+    pay_src = pay_out.data();
+  }
   std::vector<int32_t> order(plan->n_sub);
   std::iota(order.begin(), order.end(), 0);
   if (schedule == TW_SCHEDULE_LPT) {
@@ -831,6 +899,16 @@ int tw_plan_get_info(const tw_plan* p, tw_plan_info* info) {
   return TW_OK;
 }
 
+int tw_plan_output_groups(const tw_plan* p, int32_t* bounds) {
+  if (!p || !bounds) return fail(TW_ERR_INVALID_INPUT, "null argument");
+  std::vector<int32_t> starts;
+  for (const SubTile& st : p->subtiles) starts.push_back(st.out_row);
+  std::sort(starts.begin(), starts.end());
+  for (size_t i = 0; i < starts.size(); ++i) bounds[i] = starts[i];
+  bounds[starts.size()] = p->n_cond;
+  return TW_OK;
+}
+
 int tw_plan_condensed_columns(const tw_plan* p, int32_t* out) {
   if (!p || !out) return fail(TW_ERR_INVALID_INPUT, "null argument");
   std::copy(p->cond_cols.begin(), p->cond_cols.end(), out);
@@ -1020,6 +1098,22 @@ int tw_plan_prepare(const tw_plan* p, const void* a, int32_t a_dtype, int64_t m,
     TW_CUDA(launch_transpose_cast(a, a_dtype, m, p->k, lda, at, p->dtype, ld_at,
                                   p->runs ? p->d_inv + (size_t)gi * p->k : nullptr,
                                   static_cast<cudaStream_t>(stream)));
+  return TW_OK;
+}
+
+int tw_plan_permute_rows(const tw_plan* p, const void* at, int64_t m, int64_t ld_at, void* x,
+                         int64_t ld_x, void* stream) {
+  g_last_error.clear();
+  if (!p || !at || !x) return fail(TW_ERR_INVALID_INPUT, "null argument");
+  if (m < 1 || ld_at < m || ld_x < m) return fail(TW_ERR_INVALID_INPUT, "bad permute geometry");
+  const int64_t rows = (int64_t)p->k * (p->runs ? p->row_copies : 1);
+  if (!p->runs) {
+    TW_CUDA(cudaMemcpy2DAsync(x, ld_x * 2, at, ld_at * 2, m * 2, p->k, cudaMemcpyDeviceToDevice,
+                              static_cast<cudaStream_t>(stream)));
+    return TW_OK;
+  }
+  TW_CUDA(launch_scatter_rows(at, ld_at, p->d_perm, (int32_t)rows, x, ld_x, m, 2,
+                              static_cast<cudaStream_t>(stream)));
   return TW_OK;
 }
 

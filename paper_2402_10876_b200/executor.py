@@ -77,7 +77,7 @@ class TwPlan:
 
     def __init__(self, enc: CtoEncoding, overlay: Optional[SparseOverlay] = None,
                  compute_dtype: str = "fp16", schedule: str = "lpt",
-                 row_layout: str = "natural"):
+                 row_layout: str = "natural", row_groups=None, out_order=None):
         torch = _torch()
         lib = _native.load_library()
         if schedule not in _native.SCHEDULES:
@@ -98,13 +98,18 @@ class TwPlan:
         co = np.ascontiguousarray(enc.col_offsets, dtype=np.uint32)
         pl = np.ascontiguousarray(enc.payload, dtype=np.float32)
         handle = _native._vp()
-        _native.check(lib.tw_plan_create_cto(
+        grp = None if row_groups is None else np.ascontiguousarray(row_groups, dtype=np.int32)
+        oo = None if out_order is None else np.ascontiguousarray(out_order, dtype=np.int32)
+        _native.check(lib.tw_plan_create_cto_ex(
             ctypes_byref(handle), k, n, enc.config.granularity_g, rc.size,
             _native.ptr(rc, _native.ctypes.c_uint32), _native.ptr(cc, _native.ctypes.c_uint32),
             _native.ptr(ro, _native.ctypes.c_uint32), ro.shape[1],
             _native.ptr(co, _native.ctypes.c_uint32), co.shape[1],
             _native.ptr(pl, _native.ctypes.c_float), _DTYPE_CODES[self.compute_dtype],
             _native.SCHEDULES[schedule], 1 if row_layout == "runs" else 0,
+            None if grp is None else _native.ptr(grp, _native.ctypes.c_int32),
+            0 if grp is None else int(grp.size) - 1,
+            None if oo is None else _native.ptr(oo, _native.ctypes.c_int32),
             _native.stream_handle()))
         self._handle = handle
         self._finalizer = weakref.finalize(self, lib.tw_plan_destroy, handle)
@@ -143,6 +148,15 @@ class TwPlan:
         _native.check(lib.tw_plan_row_order(self._handle, _native.ptr(order, _native.ctypes.c_int32)))
         self.row_order = order.astype(np.int64)  # layout position -> original K row
         self._row_order_dev = None
+
+    def output_groups(self) -> np.ndarray:
+        """Ascending bounds of the C'^T row blocks each 128-column sub-tile
+        writes (the groups a chained next plan's row layout may permute in)."""
+        lib = _native.load_library()
+        b = np.empty(int(self.info.n_sub) + 1, dtype=np.int32)
+        _native.check(lib.tw_plan_output_groups(self._handle,
+                                                _native.ptr(b, _native.ctypes.c_int32)))
+        return b.astype(np.int64)
 
     @property
     def uses_row_runs(self) -> bool:
@@ -216,9 +230,22 @@ class TwPlan:
             raise InvalidInputError(f"inner dims disagree: at has {at.shape[0]} rows, "
                                     f"weights have K={k}")
         if self.uses_row_runs:
-            if self._row_order_dev is None:
-                self._row_order_dev = torch.tensor(self.row_order, device=at.device)
-            at = at.index_select(0, self._row_order_dev)
+            # the row permutation into the plan layout runs in the library
+            # (tw_plan_permute_rows); a dtype cast, if needed, comes first
+            if at.dtype != _torch_dtype(self.compute_dtype):
+                at = at.to(_torch_dtype(self.compute_dtype))
+            m = int(at.shape[1])
+            if not _at_ready(at, self.compute_dtype):
+                at = at.contiguous() if m % 8 == 0 else \
+                    torch.nn.functional.pad(at, (0, (-m) % 8))[:, :m]
+            rows = self.layout_rows
+            ld = (m + 7) // 8 * 8
+            x = torch.empty((rows, ld), dtype=at.dtype, device=at.device)
+            lib = _native.load_library()
+            _native.check(lib.tw_plan_permute_rows(
+                self._handle, at.data_ptr(), m, at.stride(0) if at.shape[0] > 1 else ld,
+                x.data_ptr(), ld, _native.stream_handle(stream)))
+            return x[:, :m]
         if _at_ready(at, self.compute_dtype):
             return at
         # (after the row permutation at has layout_rows rows: row_copies x K)

@@ -98,3 +98,45 @@ def test_plan_from_cto1_file(tmp_path):
     p = tw.TwPlan.from_cto1(path)
     out = p.run(p.prepare(a))
     assert tw.relative_error(out.t(), orc.c_gemm_cto_enc(a, e1)) <= 1e-5
+
+
+@pytest.mark.gpu
+def test_chain_plans_write_next_layers_run_layout():
+    """chain_plans (BERT FFN shapes): layer l's epilogue writes C'^T directly
+    in layer l+1's row-run order (payload rows permuted inside sub-tiles), and
+    layer l+1 reads it with dense TMA boxes -- no prepare pass in between.
+    Both products match the oracle on the same (fp16-rounded) values."""
+    import torch
+
+    rng = np.random.default_rng(5)
+    w1 = tw.round_to(rng.normal(size=(768, 3072)).astype(np.float32), "fp16")
+    w2 = tw.round_to(rng.normal(size=(3072, 768)).astype(np.float32), "fp16")
+    _, t1 = tw.prune_tw(w1, 0.75, 128)
+    _, t2 = tw.prune_tw(w2, 0.75, 128)
+    e1, e2 = tw.encode_cto(t1), tw.encode_cto(t2)
+    prev, nxt = tw.chain_plans(e1, e2)
+    assert nxt.uses_row_runs
+    # prev's output rows are a permutation of the condensed columns, inside
+    # each 128-row sub-tile block
+    cols = prev.condensed_columns
+    assert sorted(cols.tolist()) == sorted(t1.column_mask.kept.tolist())
+    b = prev.output_groups()
+    kept = np.asarray(t1.column_mask.kept)
+    for lo, hi in zip(b[:-1], b[1:]):
+        assert sorted(cols[lo:hi].tolist()) == kept[lo:hi].tolist()
+    a = tw.round_to(rng.normal(size=(1000, 768)).astype(np.float32), "fp16")
+    h = prev.run(prev.prepare(a), out_dtype="fp16")             # N1' x M, next's layout
+    ref1 = orc.c_gemm_cto_enc(a, e1)                            # M x N1', condensed order
+    pos = {int(c): i for i, c in enumerate(kept)}
+    perm = np.array([pos[int(c)] for c in cols])
+    assert tw.relative_error(h.float().t().cpu().numpy(), ref1[:, perm]) <= 1e-3
+    y = nxt.run(h)                                              # TMA runs on h in place
+    hn = h.float().t().cpu().numpy()                            # the values layer 2 read
+    full = np.zeros((a.shape[0], 3072), dtype=np.float32)
+    full[:, cols] = hn
+    ref2 = orc.c_gemm_cto_enc(full, e2)
+    assert tw.relative_error(y.t(), ref2) <= 1e-5
+    # the same chain through the natural layouts gives the same numbers
+    y_nat = tw.TwPlan(tw.chain_encoding(e2, kept)).run(
+        tw.TwPlan(e1).run(tw.prepare_activations(a), out_dtype="fp16"))
+    assert tw.relative_error(y.t(), y_nat.t().cpu().numpy()) <= 1e-5
