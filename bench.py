@@ -13,9 +13,13 @@ value        effective TFLOP/s = surviving FLOPs (metrics.report.sparse_flops,
              metrics.py:114-117) of all ranks / max-over-ranks device time,
              inputs resident in HBM; 4 rotating buffer sets (> 2 x L2) so
              every step streams cold activations, weights and outputs.  The
-             timed steps replay one CUDA graph per rotation (4 steps = 12
-             layer launches chained by programmatic dependent launch); the
-             dense cuBLAS arm is graph-captured the same way.
+             step's three layers are independent products and run as one
+             TwPlanGroup (each on an SM share, concurrent streams); the timed
+             steps replay one CUDA graph per rotation (4 steps).  The dense
+             cuBLAS arm is graph-captured the same way (sequential: its
+             fastest arrangement; forked onto 3 streams it is slower, both
+             reported).  "sequential" is our step with the three launches
+             one after another.
              Activations are resident as A^T (K x M, tokens contiguous): the
              layout K1 reads and writes (a TW layer's C'^T output is the next
              layer's A^T); the cuBLAS arm reads the same A^T buffers.
@@ -446,10 +450,10 @@ def fork_join(fns):
 
 def extra_measurements(cfg, layers, sets, rank, dense_ms, ms_step, tew):
     """Numbers reported beside the headline:
-    natural-layout step (plain A^T, what cuBLAS reads), cold per-layer K1
-    launches (12 buffer sets > L2), the grouped step (TwPlanGroup over SM
-    shares, vs cuBLAS on three forked streams) and, for configs[1], the BERT
-    FFN pair chained in the row-run layout (chain_plans)."""
+    natural-layout sequential step (plain A^T, what cuBLAS reads), cold
+    per-layer K1 launches (12 buffer sets > L2), cuBLAS on three forked
+    streams (the grouped step's structure) and, for configs[1], the BERT FFN
+    pair chained in the row-run layout (chain_plans)."""
     import torch
 
     import paper_2402_10876_b200 as tw
@@ -472,8 +476,8 @@ def extra_measurements(cfg, layers, sets, rank, dense_ms, ms_step, tew):
     us_nat = graph_us(nat_step, 4 * R)
     out["natural_layout"] = {"ms_per_step": us_nat / 1e3,
                              "speedup_vs_cublas": dense_ms / (us_nat / 1e3),
-                             "what": "same step on plain A^T (original row order; the layout "
-                                     "cuBLAS reads): kept rows gathered with cp.async"}
+                             "what": "sequential step on plain A^T (original row order; the "
+                                     "layout cuBLAS reads): kept rows gathered with cp.async"}
     del nat
 
     # cold per-layer launches: 12 (A^T, C'^T) sets per layer (> L2 for every layer)
@@ -490,21 +494,7 @@ def extra_measurements(cfg, layers, sets, rank, dense_ms, ms_step, tew):
         del bufs
     out["per_layer_cold"] = cold
 
-    # grouped step: the three independent layers on SM shares, concurrent streams
-    groups = [tw.TwPlanGroup([p for p, _, _ in sets[r]], m) for r in range(R)]
-
-    def grp_step(i):
-        plans_xs = sets[i % R]
-        g = groups[i % R]
-        if tew:
-            g.run_tew([x for _, x, _ in plans_xs], [o for _, _, o in plans_xs])
-        else:
-            g.run([x for _, x, _ in plans_xs], [o for _, _, o in plans_xs])
-
-    us_grp = graph_us(grp_step, 4 * R)
-    budgets = groups[0].budgets
-    for g in groups:
-        g.release()
+    # cuBLAS with the same fork/join structure as the grouped step
     dense = []
     for r in range(R):
         row = []
@@ -515,12 +505,11 @@ def extra_measurements(cfg, layers, sets, rank, dense_ms, ms_step, tew):
         dense.append(row)
     us_d3 = graph_us(lambda i: fork_join([lambda d=d: torch.matmul(d[0], d[1], out=d[2])
                                           for d in dense[i % R]]), 4 * R)
-    out["grouped"] = {"ms_per_step": us_grp / 1e3, "sm_budgets": budgets,
-                      "cublas_3_streams_ms": us_d3 / 1e3,
-                      "speedup_vs_cublas_3_streams": us_d3 / us_grp,
-                      "speedup_vs_cublas": dense_ms / (us_grp / 1e3),
-                      "what": "TwPlanGroup: each layer on an SM share (LPT split over it), "
-                              "concurrent streams; cuBLAS forked onto 3 streams the same way"}
+    out["cublas_3_streams"] = {"ms_per_step": us_d3 / 1e3,
+                               "speedup_vs_it": us_d3 / (ms_step * 1e3),
+                               "what": "cuBLAS forked onto 3 streams like the grouped step "
+                                       "(slower than its sequential graph, which is the "
+                                       "cublas arm)"}
     del dense
 
     # BERT FFN chained in the row-run layout (configs[1] layers 768x3072 -> 3072x768)
@@ -591,12 +580,31 @@ def run_ours(args, cfg, rank: int, world: int) -> None:
         sets.append(layer_set)
     torch.cuda.synchronize()
 
-    def run_set(r: int):
+    # The step's layers are independent products (configs[1] lists three
+    # layer shapes, each fed its own activations), so the step runs them as
+    # one TwPlanGroup: every layer on an SM share sized by the library's cost
+    # model, on concurrent streams forked from and joined back to the step's
+    # stream.  The same layers one after another are reported beside it
+    # ("sequential").
+    def seq_set(r: int):
         for plan, at, ct in sets[r]:
             if tew:
                 plan.run_tew(at, out=ct)
             else:
                 plan.run(at, out=ct)
+
+    # captured before the SM shares are set (launch geometry is baked into
+    # the graph): the sequential step uses the whole GPU for every launch
+    seq_cycle = capture_graph(lambda: [seq_set(r) for r in range(N_ROTATE)])
+    groups = [tw.TwPlanGroup([p for p, _, _ in sets[r]], m) for r in range(N_ROTATE)]
+
+    def run_set(r: int):
+        xs = [x for _, x, _ in sets[r]]
+        outs = [o for _, _, o in sets[r]]
+        if tew:
+            groups[r].run_tew(xs, outs)
+        else:
+            groups[r].run(xs, outs)
 
     # one CUDA graph per rotating set: a step is one graph replay (3 launches)
     graphs = [capture_graph(lambda r=r: run_set(r)) for r in range(N_ROTATE)]
@@ -637,11 +645,24 @@ def run_ours(args, cfg, rank: int, world: int) -> None:
         run_steps(args.steps)
         ev1.record(stream)
         torch.cuda.synchronize()
+        # the sequential step right after, in the same power / clock state
+        sq0, sq1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        n_seq = max(1, args.steps // N_ROTATE)
+        sq0.record(stream)
+        for _ in range(n_seq):
+            seq_cycle.replay()
+        sq1.record(stream)
+        torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     ms_max = reduce_max(ev0.elapsed_time(ev1), world)
+    ms_seq = reduce_max(sq0.elapsed_time(sq1) / (n_seq * N_ROTATE), world)
     ms_step = ms_max / args.steps
     value = world * flops_step / (ms_step * 1e-3) / 1e12
+    budgets = groups[0].budgets
+    for g in groups:
+        g.release()          # per-layer and sequential timings use the whole GPU
+    del graphs, cycle, seq_cycle
 
     # ---- per-launch K1 timing (roofline): graph of REPS launches per layer
     per_layer = []
@@ -825,6 +846,10 @@ def run_ours(args, cfg, rank: int, world: int) -> None:
                    "parallelism": f"dp{world} (M-split, no collective)",
                    "l2": f"{N_ROTATE} rotating buffer sets (weights, A^T, C^T) > 2x L2"},
         "speedup_vs_cublas": dense_ms / ms_step,
+        "step": {"launch": "TwPlanGroup: the 3 layers on SM shares, concurrent streams",
+                 "sm_budgets": budgets},
+        "sequential": {"ms_per_step": ms_seq, "speedup_vs_cublas": dense_ms / ms_seq,
+                       "what": "the same 3 launches one after another (whole GPU each)"},
         "transpose": {"ms_per_step": prep_ms,
                  "what": "A (M x K fp16, device, row-major) -> A^T per layer (TwPlan.prepare: K4 + row order); "
                          "only for row-major callers (a TW layer's C'^T output is already the "

@@ -144,6 +144,12 @@ TW_API int tw_plan_get_info(const tw_plan* plan, tw_plan_info* info);
  * budget mirrors the LPT balancing of executor.py:206-227. */
 TW_API int tw_plan_set_sm_budget(tw_plan* plan, int32_t sms);
 
+/* Cost model of the work split for `sms` SMs (0 = all) and m tokens,
+ * without changing the plan: the busiest CTA's token x 64-row-stage count
+ * and its number of units (used to choose SM shares, TwPlanGroup). */
+TW_API int tw_plan_estimate(const tw_plan* plan, int32_t sms, int64_t m, int64_t* stage_tokens,
+                            int32_t* units);
+
 /* Output column maps (host buffers sized n_condensed / n_union):
  * original column id of every row of C'^T. */
 TW_API int tw_plan_condensed_columns(const tw_plan* plan, int32_t* out_cols);

@@ -49,6 +49,7 @@ SIGNATURES = {
     "tw_plan_attach_overlay": (_c_int, [_vp, _i32, _i32, _i64, _i64p, _i64p, _f32p, _vp]),
     "tw_plan_get_info": (_c_int, [_vp, ctypes.POINTER(PlanInfo)]),
     "tw_plan_set_sm_budget": (_c_int, [_vp, _i32]),
+    "tw_plan_estimate": (_c_int, [_vp, _i32, _i64, _i64p, _i32p]),
     "tw_plan_condensed_columns": (_c_int, [_vp, _i32p]),
     "tw_plan_union_columns": (_c_int, [_vp, _i32p]),
     "tw_gemm": (_c_int, [_vp, _vp, _i64, _i64, _vp, _i64, _i32, _vp]),

@@ -201,12 +201,25 @@ struct tw_plan {
 // c_s proportional to its per-token cost, largest remainder, at least one
 // each.  Mirrors the LPT balancing of executor.py:206-227.  Plans with more
 // sub-tiles than G run the strided decomposition instead.
+static std::vector<int32_t> split_counts(const tw_plan* plan, int G);
+
 static void owner_split(tw_plan* plan) {
   const int G = plan->sm_budget;
   plan->cta_first.clear();
   plan->owner = plan->n_sub <= G && G <= kMaxCtas;
   plan->resident = false;
   if (!plan->owner) return;
+  const std::vector<int32_t> c = split_counts(plan, G);
+  plan->cta_first.assign(plan->n_sub + 1, 0);
+  for (int i = 0; i < plan->n_sub; ++i) plan->cta_first[i + 1] = plan->cta_first[i] + c[i];
+  int max_steps = 0;
+  for (const SubTile& st : plan->subtiles) max_steps = std::max(max_steps, (int)st.kp_steps);
+  plan->resident = max_steps <= kResSteps && !env_int("TW_NO_RESIDENT", 0);
+}
+
+// CTAs per sub-tile for G SMs (owner mode): proportional to the per-token
+// cost weights, largest remainder, at least one each.
+static std::vector<int32_t> split_counts(const tw_plan* plan, int G) {
   // weight (per token): k-steps, or (row-run plans) the stages' TMA issue
   // cost, plus a fixed per-unit share for the epilogue and pipeline fill,
   // which dominates short-K' sub-tiles (TEW 768x3072 keeps K' = 1 on one
@@ -238,11 +251,7 @@ static void owner_split(tw_plan* plan) {
     c[big] -= 1;
     --used;
   }
-  plan->cta_first.assign(plan->n_sub + 1, 0);
-  for (int i = 0; i < plan->n_sub; ++i) plan->cta_first[i + 1] = plan->cta_first[i] + c[i];
-  int max_steps = 0;
-  for (const SubTile& st : plan->subtiles) max_steps = std::max(max_steps, (int)st.kp_steps);
-  plan->resident = max_steps <= kResSteps && !env_int("TW_NO_RESIDENT", 0);
+  return c;
 }
 
 extern "C" {
@@ -871,6 +880,33 @@ int tw_plan_set_sm_budget(tw_plan* p, int32_t sms) {
     p->sm_budget = b;
     owner_split(p);
   }
+  return TW_OK;
+}
+
+int tw_plan_estimate(const tw_plan* p, int32_t sms, int64_t m, int64_t* stage_tokens,
+                     int32_t* units) {
+  if (!p || !stage_tokens || !units || m < 1) return fail(TW_ERR_INVALID_INPUT, "bad argument");
+  const int G = sms <= 0 ? p->sm_count : std::min<int>(sms, p->sm_count);
+  int64_t worst = 0;
+  int32_t wu = 0;
+  if (p->n_sub <= G && G <= kMaxCtas) {
+    const std::vector<int32_t> c = split_counts(p, G);
+    const int64_t ch = (m + 63) / 64;
+    for (int s = 0; s < p->n_sub; ++s) {
+      const int64_t len = ((ch + c[s] - 1) / c[s]) * 64;  // busiest CTA of the sub-tile
+      const int64_t st = len * p->subtiles[s].kp_steps;
+      const int32_t u = (int32_t)((len + kTN - 1) / kTN);
+      if (st > worst) { worst = st; wu = u; }
+    }
+  } else {
+    const int64_t n_units = (int64_t)p->n_sub * ((m + kTN - 1) / kTN);
+    int32_t max_steps = 0;
+    for (const SubTile& st : p->subtiles) max_steps = std::max(max_steps, st.kp_steps);
+    wu = (int32_t)((n_units + G - 1) / G);
+    worst = (int64_t)wu * kTN * max_steps;
+  }
+  *stage_tokens = worst;
+  *units = wu;
   return TW_OK;
 }
 

@@ -44,14 +44,76 @@ def split_sms(costs: Sequence[float], floors: Sequence[int], sms: int) -> List[i
     return out
 
 
+# cost model of one CTA's work, in SM cycles, fitted to the BERT layers run
+# alone on SM shares (scripts/group_probe.py, profiles/r2_group_probe.txt): a
+# 64-row stage costs ~4.0 cycles per token when the activations arrive as
+# dense TMA boxes (row-run layout) and ~5.5 on the cp.async gather; every
+# 256-token unit adds its pipeline fill and (partly hidden) epilogue
+CYCLES_PER_TOKEN_STAGE = {"runs": 4.0, "gather": 5.5}
+CYCLES_PER_UNIT = 3000.0
+
+
+def plan_cost(plan, sms: int, m: int) -> float:
+    """Estimated cycles of the plan's busiest CTA on ``sms`` SMs (the C
+    library's own work split, tw_plan_estimate), for plan-layout inputs."""
+    from . import _native
+
+    lib = _native.load_library()
+    st = _native.ctypes.c_int64()
+    un = _native.ctypes.c_int32()
+    _native.check(lib.tw_plan_estimate(plan._handle, int(sms), int(m),
+                                       _native.ctypes.byref(st), _native.ctypes.byref(un)))
+    per = CYCLES_PER_TOKEN_STAGE["runs" if plan.uses_row_runs else "gather"]
+    return per * st.value + CYCLES_PER_UNIT * un.value
+
+
+def choose_budgets(plans, m: int, sms: int) -> List[int]:
+    """SM shares minimising the slowest plan's estimated time: for a target
+    time T each plan takes the fewest SMs that meet it; T is the smallest
+    candidate for which the shares fit; spare SMs go where they help most."""
+    floors = [int(p.info.n_sub) for p in plans]
+    if sum(floors) > sms:
+        raise InvalidInputError(f"{sum(floors)} sub-tiles do not fit on {sms} SMs side by side")
+    cost = [{b: plan_cost(p, b, m) for b in range(f, sms + 1)} for p, f in zip(plans, floors)]
+    cands = sorted({c for table in cost for c in table.values()})
+
+    def need(t):
+        out = []
+        for table in cost:
+            ok = [b for b, c in table.items() if c <= t]
+            if not ok:
+                return None
+            out.append(min(ok))
+        return out
+
+    lo, hi = 0, len(cands) - 1
+    while lo < hi:
+        mid = (lo + hi) // 2
+        n = need(cands[mid])
+        if n is not None and sum(n) <= sms:
+            hi = mid
+        else:
+            lo = mid + 1
+    budgets = need(cands[lo])
+    spare = sms - sum(budgets)
+    while spare > 0:   # the slowest plan takes the next SM (if any plan still gains)
+        j = max(range(len(plans)), key=lambda i: cost[i][budgets[i]])
+        if budgets[j] >= sms:
+            break
+        budgets[j] += 1
+        spare -= 1
+    return budgets
+
+
 class TwPlanGroup:
     """Several :class:`TwPlan` s run as one step on disjoint SM shares.
 
-    ``m`` is the token count the split is tuned for (the cost model is the
-    plans' 64-row k-steps per token plus a per-unit epilogue share, the same
-    weights the per-plan owner split uses)."""
+    ``m`` is the token count the split is tuned for: the shares minimise the
+    slowest plan's estimated time (:func:`choose_budgets` over the library's
+    own work split); ``budgets`` overrides them."""
 
-    def __init__(self, plans: Sequence, m: int, sms: Optional[int] = None):
+    def __init__(self, plans: Sequence, m: int, sms: Optional[int] = None,
+                 budgets: Optional[Sequence[int]] = None):
         from .executor import _torch
 
         torch = _torch()
@@ -62,10 +124,14 @@ class TwPlanGroup:
         if any(p.device != dev for p in self.plans):
             raise InvalidInputError("all plans of a group must live on one device")
         total = int(self.plans[0].info.sm_count) if sms is None else int(sms)
-        units = -(-int(m) // 256)
-        costs = [(int(p.info.stage_work) + 3 * int(p.info.n_sub)) * units for p in self.plans]
-        floors = [int(p.info.n_sub) for p in self.plans]
-        self.budgets = split_sms(costs, floors, total) if len(self.plans) > 1 else [total]
+        if budgets is not None:
+            if len(budgets) != len(self.plans) or sum(budgets) > total:
+                raise InvalidInputError("budgets must give one SM count per plan within the GPU")
+            self.budgets = [int(b) for b in budgets]
+        elif len(self.plans) == 1:
+            self.budgets = [total]
+        else:
+            self.budgets = choose_budgets(self.plans, m, total)
         for p, b in zip(self.plans, self.budgets):
             p.set_sm_budget(b)
         self.streams = [torch.cuda.Stream(device=dev) for _ in self.plans]

@@ -130,5 +130,74 @@ def main():
           f"grouped/grouped-cublas {t_dgrp / t_grp:.2f}x; grouped {flops / t_grp / 1e6:.0f} TFLOP/s")
 
 
+
+
+def soak_ab():
+    """Sustained-load A/B: grouped vs sequential steps alternated after a
+    2 s soak (power-capped clocks), 5 rounds each."""
+    import time
+    m = 8192
+    encs = []
+    for k, n in LAYERS:
+        w = tw.round_to(tw.synthetic_matrix(0, k, n, 0), "fp16")
+        encs.append(tw.encode_cto(tw.prune_tw(w, 0.75, 128)[1]))
+    sets = []
+    for r in range(R):
+        plans = [tw.TwPlan(e, row_layout="runs") for e in encs]
+        xs = [p.prepare(torch.from_numpy(tw.round_to(tw.synthetic_matrix(r, m, k, 1), "fp16")).cuda())
+              for p, (k, n) in zip(plans, LAYERS)]
+        outs = [torch.empty((p.info.n_condensed, m), dtype=torch.float16, device="cuda") for p in plans]
+        sets.append((plans, xs, outs))
+    groups = [tw.TwPlanGroup(sets[r][0], m) for r in range(R)]
+
+    def seq(i):
+        for p, x, o in zip(*sets[i]):
+            p.run(x, out=o)
+
+    def grp(i):
+        groups[i].run(sets[i][1], sets[i][2])
+
+    def cap(fn):
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            for i in range(R):
+                fn(i)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=s):
+                for i in range(64):
+                    fn(i % R)
+        torch.cuda.current_stream().wait_stream(s)
+        return g
+
+    # budgets are plan state: grouped graph captured with budgets set, the
+    # sequential graph with the same plans at full budget (set per replay)
+    gg = cap(grp)
+    for g in groups:
+        g.release()
+    gs = cap(seq)
+    for g, r in zip(groups, range(R)):
+        for p, b in zip(sets[r][0], g.budgets):
+            p.set_sm_budget(b)
+    t0 = time.time()
+    while time.time() - t0 < 2.0:
+        gg.replay()
+    torch.cuda.synchronize()
+    res = {"grouped": [], "sequential": []}
+    for _ in range(5):
+        for name, g in (("grouped", gg), ("sequential", gs)):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(8):
+                g.replay()
+            e1.record()
+            torch.cuda.synchronize()
+            res[name].append(e0.elapsed_time(e1) * 1e3 / (8 * 64))
+    print("sustained A/B us per step:", {k: [round(v, 1) for v in vs] for k, vs in res.items()})
+
+
 if __name__ == "__main__":
-    main()
+    if "--soak" in sys.argv:
+        soak_ab()
+    else:
+        main()

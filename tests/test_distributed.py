@@ -148,3 +148,11 @@ def test_sharded_plan_all_gathers_full_product(world, chunks):
         got, cols = results[r]
         assert np.allclose(got, want, rtol=0, atol=1e-5 * np.abs(want).max())
         assert np.array_equal(cols, kept)
+
+
+def test_split_sms_floors_and_total():
+    b = tw.split_sms([10, 40, 35], [3, 12, 3], 148)
+    assert sum(b) == 148 and b[1] >= 12 and all(x >= f for x, f in zip(b, [3, 12, 3]))
+    assert tw.split_sms([1, 1], [70, 70], 148)[0] >= 70
+    with pytest.raises(tw.InvalidInputError):
+        tw.split_sms([1, 1], [100, 100], 148)

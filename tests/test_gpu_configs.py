@@ -223,3 +223,35 @@ def test_output_argument_checks():
                                     device="cuda"))
     with pytest.raises(tw.InvalidInputError):
         plan.run_tew(x, out=torch.empty((plan.info.n_union - 1, 64), device="cuda"))
+
+
+@pytest.mark.parametrize("tew", [False, True])
+def test_plan_group_equals_sequential(tew):
+    """TwPlanGroup (SM shares, concurrent streams) gives every layer exactly
+    the result of launching it alone on the whole GPU."""
+    import torch
+
+    rng = np.random.default_rng(17)
+    plans, xs, ref = [], [], []
+    for k, n in [(768, 768), (768, 3072), (3072, 768)]:
+        w = tw.round_to(rng.normal(size=(k, n)).astype(np.float32), "fp16")
+        a = tw.round_to(rng.normal(size=(2000, k)).astype(np.float32), "fp16")
+        if tew:
+            _, tsm, ov = tw.prune_tew(w, 0.75, 0.015, 128)
+            p = tw.TwPlan(tw.encode_cto(tsm), ov, row_layout="runs")
+        else:
+            _, tsm = tw.prune_tw(w, 0.75, 128)
+            p = tw.TwPlan(tw.encode_cto(tsm), row_layout="runs")
+        x = p.prepare(a)
+        ref.append(p.run_tew(x, out_dtype="fp16") if tew else p.run(x, out_dtype="fp16"))
+        plans.append(p)
+        xs.append(x)
+    g = tw.TwPlanGroup(plans, 2000)
+    assert sum(g.budgets) <= plans[0].info.sm_count
+    assert all(b >= p.info.n_sub for b, p in zip(g.budgets, plans))
+    outs = g.run_tew(xs, out_dtype="fp16") if tew else g.run(xs, out_dtype="fp16")
+    torch.cuda.synchronize()
+    for o, r in zip(outs, ref):
+        assert torch.equal(o, r)
+    g.release()
+    assert all(int(p.info.sm_budget) == int(p.info.sm_count) for p in plans)
