@@ -209,3 +209,63 @@ def test_relative_error_conventions():             # test_executor.py:385-390
     z = np.zeros((2, 2))
     assert tw.relative_error(z, z) == 0.0
     assert tw.relative_error(np.ones((2, 2)), z) == np.inf
+
+
+def _big_fingerprint(plan, tsm, enc, ov=None):
+    import hashlib
+
+    def sha(a):
+        return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+    d = {"mask": sha(plan.element_mask),
+         "cols": sha(np.asarray(tsm.column_mask.kept).astype(np.int64)),
+         "rows": sha(np.concatenate([t.kept_rows.kept for t in tsm.tiles]).astype(np.int64)),
+         "row_counts": enc.row_counts.astype(int).tolist(),
+         "col_counts": enc.col_counts.astype(int).tolist(),
+         "row_offsets": sha(enc.row_offsets), "col_offsets": sha(enc.col_offsets),
+         "payload": sha(enc.payload), "achieved": float(plan.achieved_sparsity)}
+    if ov is not None:
+        d.update({"ov_col_ptr": sha(np.asarray(ov.col_ptr).astype(np.int64)),
+                  "ov_row_idx": sha(np.asarray(ov.row_idx).astype(np.int64)),
+                  "ov_values": sha(np.asarray(ov.values).astype(np.float32)),
+                  "ov_nnz": int(ov.nnz)})
+    return d
+
+
+def _big_golden():
+    import json
+    from pathlib import Path
+
+    return json.loads((Path(__file__).parent / "golden" / "big.json").read_text())
+
+
+def test_prune_tw_bit_exact_at_16384():
+    """configs[4]'s 16384 x 16384 weight: masks, kept columns, every tile's
+    kept rows, CTO offsets and payload equal the reference's
+    (tests/golden/make_golden_big.py fingerprints)."""
+    want = _big_golden()["big_tw"]
+    w = tw.round_to(tw.synthetic_matrix(0, 16384, 16384, tw.STREAM_WEIGHTS), "fp16")
+    plan, tsm = tw.prune_tw(w, 0.75, 128)
+    del w
+    assert _big_fingerprint(plan, tsm, tw.encode_cto(tsm)) == want
+
+
+def test_prune_tew_bit_exact_at_4096():
+    want = _big_golden()["tew_4096"]
+    w = tw.round_to(tw.synthetic_matrix(0, 4096, 4096, tw.STREAM_WEIGHTS), "fp16")
+    plan, tsm, ov = tw.prune_tew(w, 0.75, 0.015, 128)
+    assert _big_fingerprint(plan, tsm, tw.encode_cto(tsm), ov) == want
+
+
+def test_prune_tw_bit_exact_vgg_sweep_shapes():
+    """configs[3] VGG-16 im2col weights over the sparsity / G sweep."""
+    gold = _big_golden()
+    shapes = {"conv1_2": (576, 64), "conv2_1": (576, 128), "conv3_2": (2304, 256),
+              "conv4_2": (4608, 512), "conv5_1": (4608, 512)}
+    for name, (k, n) in shapes.items():
+        w = tw.round_to(tw.synthetic_matrix(0, k, n, tw.STREAM_WEIGHTS), "fp16")
+        for s in (0.5, 0.7, 0.9):
+            for g in (64, 128, 256):
+                plan, tsm = tw.prune_tw(w, s, g)
+                got = _big_fingerprint(plan, tsm, tw.encode_cto(tsm))
+                assert got == gold[f"{name}_s{s}_g{g}"], (name, s, g)
