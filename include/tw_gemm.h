@@ -126,6 +126,18 @@ TW_API int tw_plan_create_cto_ex(tw_plan** out, int32_t k, int32_t n, int32_t g,
  * ascending bounds): the groups tw_plan_create_cto_ex may permute within. */
 TW_API int tw_plan_output_groups(const tw_plan* plan, int32_t* bounds);
 
+/* Device-native plan file "TWP1": the plan as the kernels
+ * read it (validated structure, merged tiles, row-run layout and box tables,
+ * fp16/bf16 payload), so tw_plan_load only uploads -- no CTO validation,
+ * merging, row ordering or payload conversion.  The CTO1 artifact
+ * (formats.py:239-304) stays the interchange format.
+ * tw_plan_save: *len in = buffer capacity (buf may be NULL to query), out =
+ * bytes needed; a plan with an overlay cannot be saved (attach it after
+ * loading).  tw_plan_load validates every index against the plan's dims
+ * (TW_ERR_CORRUPT otherwise) and synchronises `stream`. */
+TW_API int tw_plan_save(const tw_plan* plan, void* buf, uint64_t* len);
+TW_API int tw_plan_load(tw_plan** out, const void* buf, uint64_t len, void* stream);
+
 /* Attach a TEW overlay (CSC, int64 like patterns.SparseOverlay,
  * patterns.py:145-214).  Replaces the overlap/dims checks of
  * executor.gemm_tew (executor.py:186-193): dims mismatch -> TW_ERR_INVALID_INPUT,

@@ -46,6 +46,8 @@ SIGNATURES = {
                                        _u32p, _i32, _u32p, _i32, _f32p, _i32, _i32, _i32, _i32p,
                                        _i32, _i32p, _vp]),
     "tw_plan_output_groups": (_c_int, [_vp, _i32p]),
+    "tw_plan_save": (_c_int, [_vp, _vp, ctypes.POINTER(ctypes.c_uint64)]),
+    "tw_plan_load": (_c_int, [ctypes.POINTER(_vp), _vp, ctypes.c_uint64, _vp]),
     "tw_plan_attach_overlay": (_c_int, [_vp, _i32, _i32, _i64, _i64p, _i64p, _f32p, _vp]),
     "tw_plan_get_info": (_c_int, [_vp, ctypes.POINTER(PlanInfo)]),
     "tw_plan_set_sm_budget": (_c_int, [_vp, _i32]),
@@ -103,13 +105,21 @@ def check(status: int) -> None:
         raise_for_status(status, msg.decode() if msg else "")
 
 
+_torch_ok = None
+
+
 def require_cuda():
-    """Return torch with a usable CUDA device, or raise DeviceError."""
+    """Return torch with a usable CUDA device, or raise DeviceError (the
+    device check runs once per process)."""
+    global _torch_ok
+    if _torch_ok is not None:
+        return _torch_ok
     import torch
 
     if not torch.cuda.is_available():
         raise DeviceError("no CUDA device: the TW/TEW matmul runs only on the GPU "
                           "(there is deliberately no CPU fallback)")
+    _torch_ok = torch
     return torch
 
 

@@ -130,6 +130,50 @@ class TwPlan:
 
         return cls(read_cto1(path), overlay, compute_dtype, schedule, row_layout)
 
+    def save(self, path) -> int:
+        """Write the device-native plan file "TWP1": the plan
+        exactly as the kernels read it, so :meth:`load` skips the CTO
+        validation, tile merging, row-run search and payload conversion.
+        Returns the bytes written.  The overlay is not part of the file."""
+        lib = _native.load_library()
+        n = _native.ctypes.c_uint64(0)
+        _native.check(lib.tw_plan_save(self._handle, None, _native.ctypes.byref(n)))
+        buf = np.empty(int(n.value), dtype=np.uint8)
+        _native.check(lib.tw_plan_save(self._handle, buf.ctypes.data, _native.ctypes.byref(n)))
+        from pathlib import Path
+
+        Path(path).write_bytes(buf.tobytes())
+        return int(n.value)
+
+    @classmethod
+    def load(cls, path, overlay: Optional[SparseOverlay] = None) -> "TwPlan":
+        """Plan from a "TWP1" file written by :meth:`save` (uploads only;
+        every index is validated against the plan's dims by the library,
+        CorruptEncodingError otherwise)."""
+        from pathlib import Path
+
+        torch = _torch()
+        lib = _native.load_library()
+        data = np.frombuffer(Path(path).read_bytes(), dtype=np.uint8)
+        handle = _native._vp()
+        _native.check(lib.tw_plan_load(ctypes_byref(handle), data.ctypes.data, data.size,
+                                       _native.stream_handle()))
+        self = cls.__new__(cls)
+        self._handle = handle
+        self._finalizer = weakref.finalize(self, lib.tw_plan_destroy, handle)
+        self.device = torch.cuda.current_device()
+        self._refresh_info()
+        info = self.info
+        self.compute_dtype = {_native.TW_F16: "fp16", _native.TW_BF16: "bf16"}[info.compute_dtype]
+        self.schedule = "lpt"
+        self.row_layout = "runs" if info.row_runs else "natural"
+        self.original_dims = (int(info.k), int(info.n))
+        self.per_tile_kept = []
+        self.per_tile_width = []
+        if overlay is not None:
+            self.attach_overlay(overlay)
+        return self
+
     # -- metadata -------------------------------------------------------
     def _refresh_info(self) -> None:
         lib = _native.load_library()
@@ -148,6 +192,17 @@ class TwPlan:
         _native.check(lib.tw_plan_row_order(self._handle, _native.ptr(order, _native.ctypes.c_int32)))
         self.row_order = order.astype(np.int64)  # layout position -> original K row
         self._row_order_dev = None
+        self._masks = {}
+
+    def column_mask(self, union: bool = False) -> IndexMask:
+        """IndexMask of the output columns (condensed, or the TEW union),
+        built once per plan (GemmOutput.column_map of every call)."""
+        mk = self._masks.get(union)
+        if mk is None:
+            cols = self.union_columns if union else self.condensed_columns
+            mk = IndexMask(self.original_dims[1], cols)
+            self._masks[union] = mk
+        return mk
 
     def output_groups(self) -> np.ndarray:
         """Ascending bounds of the C'^T row blocks each 128-column sub-tile
@@ -622,8 +677,7 @@ def gemm_cto(a, c: CtoEncoding, check_padding: bool = False, *, compute_dtype: s
     """
     plan = plan_for(c, compute_dtype=compute_dtype)
     ct = plan.run(_activations(a, plan), out_dtype=out_dtype)
-    return GemmOutput(condensed=ct.t(), column_map=IndexMask(c.original_dims[1],
-                                                             plan.condensed_columns))
+    return GemmOutput(condensed=ct.t(), column_map=plan.column_mask())
 
 
 def execute_batched(a, b: TileSparseMatrix, workers: int, strategy: str = "lpt", *,
@@ -672,8 +726,7 @@ def gemm_tew(a, b: TileSparseMatrix, ov: SparseOverlay,
             np.array_equal(cols, plan.condensed_columns)
         ct = plan.run_tew_reuse(x, _tile_rows(tile_output, out_dtype),
                                 tile_columns=None if same else cols)
-    return GemmOutput(condensed=ct.t(), column_map=IndexMask(b.original_dims[1],
-                                                             plan.union_columns))
+    return GemmOutput(condensed=ct.t(), column_map=plan.column_mask(union=True))
 
 
 def _tile_rows(out: "GemmOutput", out_dtype: str):

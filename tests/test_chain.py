@@ -140,3 +140,44 @@ def test_chain_plans_write_next_layers_run_layout():
     y_nat = tw.TwPlan(tw.chain_encoding(e2, kept)).run(
         tw.TwPlan(e1).run(tw.prepare_activations(a), out_dtype="fp16"))
     assert tw.relative_error(y.t(), y_nat.t().cpu().numpy()) <= 1e-5
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("layout,overlay", [("runs", False), ("natural", False), ("runs", True)])
+def test_device_plan_file_round_trip(tmp_path, layout, overlay):
+    """TwPlan.save / TwPlan.load ("TWP1", the cached device-native format):
+    the loaded plan computes bit-identical products (TW, and TEW with the
+    overlay attached after loading); a corrupted file raises."""
+    import torch
+
+    rng = np.random.default_rng(9)
+    w = tw.round_to(rng.normal(size=(768, 3072)).astype(np.float32), "fp16")
+    a = tw.round_to(rng.normal(size=(700, 768)).astype(np.float32), "fp16")
+    if overlay:
+        _, tsm, ov = tw.prune_tew(w, 0.75, 0.015, 128)
+    else:
+        _, tsm = tw.prune_tw(w, 0.75, 128)
+        ov = None
+    enc = tw.encode_cto(tsm)
+    p1 = tw.TwPlan(enc, row_layout=layout)
+    n = p1.save(tmp_path / "plan.twp")
+    assert n > 0
+    p2 = tw.TwPlan.load(tmp_path / "plan.twp", overlay=ov)
+    if ov is not None:
+        p1.attach_overlay(ov)
+    assert np.array_equal(p1.condensed_columns, p2.condensed_columns)
+    assert np.array_equal(p1.row_order, p2.row_order)
+    x = p1.prepare(a)
+    if ov is None:
+        assert torch.equal(p1.run(x), p2.run(x))
+    else:
+        assert torch.equal(p1.run_tew(x), p2.run_tew(x))
+        assert np.array_equal(p1.union_columns, p2.union_columns)
+    raw = bytearray((tmp_path / "plan.twp").read_bytes())
+    (tmp_path / "bad.twp").write_bytes(bytes(raw[: len(raw) // 2]))
+    with pytest.raises(tw.CorruptEncodingError):
+        tw.TwPlan.load(tmp_path / "bad.twp")
+    raw[0] ^= 0xFF
+    (tmp_path / "bad2.twp").write_bytes(bytes(raw))
+    with pytest.raises(tw.CorruptEncodingError):
+        tw.TwPlan.load(tmp_path / "bad2.twp")
