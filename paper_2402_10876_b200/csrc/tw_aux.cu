@@ -327,6 +327,30 @@ __global__ void transpose_cast_kernel(const void* a, int32_t a_dtype, int64_t M,
   }
 }
 
+// fp32 plans: A (M x K, any dtype) -> [A_hi^T; A_lo^T] (2K x M fp16),
+// hi = fp16(a), lo = fp16(a - hi): the hi/lo operand pair of the split
+// product (tw_capi.cu, plan creation).
+__global__ void transpose_split_kernel(const void* a, int32_t a_dtype, int64_t M, int64_t K,
+                                       int64_t lda, __half* at, int64_t ld_at) {
+  __shared__ float tile[32][33];
+  const int64_t k0 = static_cast<int64_t>(blockIdx.x) * 32;
+  const int64_t m0 = static_cast<int64_t>(blockIdx.y) * 32;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int64_t m = m0 + i, k = k0 + threadIdx.x;
+    tile[i][threadIdx.x] = (m < M && k < K) ? load_as_float(a, a_dtype, m * lda + k) : 0.f;
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int64_t k = k0 + i, m = m0 + threadIdx.x;
+    if (k < K && m < M) {
+      const float v = tile[threadIdx.x][i];
+      const __half hi = __float2half_rn(v);
+      at[k * ld_at + m] = hi;
+      at[(k + K) * ld_at + m] = __float2half_rn(v - __half2float(hi));
+    }
+  }
+}
+
 // 16-bit -> 16-bit (same type) 64 x 64 tile transpose with 16-byte loads and
 // stores: each thread reads 8 consecutive k of a row of A and writes 8
 // consecutive m of a row of A^T.  Needs M, K, lda, ld_at multiples of 8 and
@@ -487,6 +511,15 @@ cudaError_t launch_scatter_rows(const void* src, int64_t ld_src, const int32_t* 
   dim3 grid(gx, static_cast<unsigned>(n_rows));
   scatter_rows_kernel<<<grid, 256, 0, stream>>>(static_cast<const uint8_t*>(src), ld_src, src_row,
                                                 static_cast<uint8_t*>(dst), ld_dst, M, esz, vec);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_transpose_split(const void* a, int32_t a_dtype, int64_t M, int64_t K,
+                                   int64_t lda, void* at, int64_t ld_at, cudaStream_t stream) {
+  if (M <= 0 || K <= 0) return cudaSuccess;
+  dim3 grid(static_cast<unsigned>((K + 31) / 32), static_cast<unsigned>((M + 31) / 32));
+  transpose_split_kernel<<<grid, dim3(32, 8), 0, stream>>>(a, a_dtype, M, K, lda,
+                                                           static_cast<__half*>(at), ld_at);
   return cudaGetLastError();
 }
 

@@ -146,6 +146,8 @@ struct LaunchEnv;
 struct tw_plan {
   int32_t k = 0, n = 0, g = 0, n_tiles = 0, n_sub = 0, bn = 0, kp = 0, n_cond = 0;
   int32_t dtype = kF16, schedule = TW_SCHEDULE_LPT, sm_count = 0;
+  bool split = false;  // fp32 compute as fp16 hi/lo pairs: A^T has 2k rows
+  int32_t k_rows() const { return split ? 2 * k : k; }  // rows of the kernels' A^T
   std::vector<SubTile> subtiles;
   std::vector<int32_t> cond_cols;        // condensed col -> original col
   std::vector<int32_t> tile_of_col;      // original col -> tile (or -1)
@@ -362,8 +364,11 @@ int tw_plan_create_cto_ex(tw_plan** out, int32_t k, int32_t n, int32_t g, int32_
       for (int32_t r = row_groups[gi]; r < row_groups[gi + 1]; ++r) grp_of[r] = gi;
     }
   }
-  if (compute_dtype != kF16 && compute_dtype != kBF16)
-    return fail(TW_ERR_INVALID_INPUT, "compute dtype must be fp16 or bf16");
+  if (compute_dtype != kF16 && compute_dtype != kBF16 && compute_dtype != kF32)
+    return fail(TW_ERR_INVALID_INPUT, "compute dtype must be fp16, bf16 or fp32");
+  const bool split = compute_dtype == kF32;  // fp32 operands as fp16 hi + lo pairs
+  if (split && (row_groups || out_row_of_cond))
+    return fail(TW_ERR_INVALID_INPUT, "chained layouts need fp16 / bf16 compute");
   if (schedule != TW_SCHEDULE_LPT && schedule != TW_SCHEDULE_ROUND_ROBIN)
     return fail(TW_ERR_INVALID_INPUT, "unknown schedule %d", schedule);
   // CtoEncoding.__post_init__ (formats.py:94-127)
@@ -388,7 +393,8 @@ int tw_plan_create_cto_ex(tw_plan** out, int32_t k, int32_t n, int32_t g, int32_
   plan->n = n;
   plan->g = g;
   plan->n_tiles = n_tiles;
-  plan->dtype = compute_dtype;
+  plan->dtype = split ? kF16 : compute_dtype;  // what the kernels read
+  plan->split = split;
   plan->schedule = schedule;
   if (int st = sm_count_of_current_device(&plan->sm_count)) return st;
   TW_CUDA(configure_gemm_kernels());
@@ -447,12 +453,48 @@ int tw_plan_create_cto_ex(tw_plan** out, int32_t k, int32_t n, int32_t g, int32_
   std::vector<int32_t> tfc = plan->tile_first_cond;
   const float* pay_in = payload;
   std::vector<float> pay_merged;
+  // fp32 operands (compute dtype TW_F32): every value is split into an fp16
+  // pair, hi = fp16(v) and lo = fp16(v - hi), and the product runs on the
+  // fp16 tensor cores as A.W ~ A_hi.W_hi + A_hi.W_lo + A_lo.W_hi (the dropped
+  // A_lo.W_lo is ~2^-22 relative): the activations enter as 2K rows
+  // [A_hi^T; A_lo^T] (tw_plan_prepare) and every tile gathers its kept rows
+  // three times -- row r with W_hi, row r again with W_lo, row K + r with
+  // W_hi.  Same kernels; 3x the MACs; fp32-class accuracy on fp32 inputs.
+  std::vector<float> pay_split;
+  if (split) {
+    if (2 * (int64_t)k >= (1 << 30)) return fail(TW_ERR_INVALID_INPUT, "k too large for fp32 split");
+    int64_t pb = 0, total = 0;
+    for (int i = 0; i < n_tiles; ++i) total += 3 * (int64_t)row_counts[i] * col_counts[i];
+    pay_split.resize(std::max<int64_t>(total, 1));
+    int64_t ob = 0;
+    for (int i = 0; i < n_tiles; ++i) {
+      const int32_t h = (int32_t)row_counts[i], w = (int32_t)col_counts[i];
+      for (int32_t c = 0; c < w; ++c)
+        for (int32_t j = 0; j < h; ++j) {
+          const float v = payload[pb + (int64_t)c * h + j];
+          const float hi = __half2float(__float2half_rn(v));
+          const float lo = __half2float(__float2half_rn(v - hi));
+          float* dst = pay_split.data() + ob + (int64_t)c * 3 * h;
+          dst[j] = hi;
+          dst[h + j] = lo;
+          dst[2 * h + j] = hi;
+        }
+      std::vector<int32_t> r3(rows[i]);
+      r3.insert(r3.end(), rows[i].begin(), rows[i].end());
+      for (int32_t r : rows[i]) r3.push_back(r + k);
+      rows[i].swap(r3);
+      rc[i] = 3 * (uint32_t)h;
+      pb += (int64_t)h * w;
+      ob += 3 * (int64_t)h * w;
+    }
+    pay_in = pay_split.data();
+  }
   {
     uint32_t wmax = 0;
     for (int i = 0; i < n_tiles; ++i) wmax = std::max(wmax, col_counts[i]);
     int gs = 1;
     while (gs * 2 * (int)wmax <= kBN) gs *= 2;
-    if (gs > 1 && n_tiles > 1 && !env_int("TW_NO_MERGE", 0)) {
+    if (gs > 1 && n_tiles > 1 && !split && !env_int("TW_NO_MERGE", 0)) {
       std::vector<int64_t> pb(n_tiles + 1, 0);
       for (int i = 0; i < n_tiles; ++i) pb[i + 1] = pb[i] + (int64_t)row_counts[i] * col_counts[i];
       const int nv = (n_tiles + gs - 1) / gs;
@@ -523,7 +565,7 @@ int tw_plan_create_cto_ex(tw_plan** out, int32_t k, int32_t n, int32_t g, int32_
   // gather on BERT 768x3072 (G = 3: 21.0 vs 20.9 us), so it is opt-in.
   const int max_copies = grp_of.empty() ? std::max(1, std::min(4, env_int("TW_RUN_COPIES", 1))) : 1;
   const double run_stage_w = env_int("TW_RUN_STAGE_W", 8);
-  if (row_runs && k < (1 << 20) && !env_int("TW_NO_RUNS", 0)) {
+  if (row_runs && !split && k < (1 << 20) && !env_int("TW_NO_RUNS", 0)) {
     const int stride = kp / kBK + 1;
     for (int G = (nt + 5) / 6; G <= max_copies && G <= nt; ++G) {
       const int per = (nt + G - 1) / G;  // tiles per group
@@ -753,13 +795,13 @@ int tw_plan_create_cto_ex(tw_plan** out, int32_t k, int32_t n, int32_t g, int32_
   const size_t pay_bytes = (size_t)plan->n_sub * bn * kp * 2;
   TW_CUDA(cudaMalloc(&plan->d_payload, pay_bytes));
   PayloadArgs pa{d_src, d_src_base, d_src_ld, plan->d_subtiles, plan->d_payload,
-                 compute_dtype, bn, kp, plan->n_sub};
+                 plan->dtype, bn, kp, plan->n_sub};
   TW_CUDA(launch_build_payload(pa, s));
   TW_CUDA(cudaStreamSynchronize(s));
   cudaFree(d_src);
   cudaFree(d_src_base);
   cudaFree(d_src_ld);
-  if (int st = make_map_2d(&plan->map_pay, plan->d_payload, compute_dtype, kp,
+  if (int st = make_map_2d(&plan->map_pay, plan->d_payload, plan->dtype, kp,
                            (uint64_t)plan->n_sub * bn, kp, kBK, bn))
     return st;
   plan->union_cols = plan->cond_cols;
@@ -784,7 +826,8 @@ int tw_plan_save(const tw_plan* p, void* buf, uint64_t* len) {
   w.pod(kTwpMagic);
   w.pod(kTwpVersion);
   for (int32_t v : {p->k, p->n, p->g, p->n_tiles, p->n_sub, p->bn, p->kp, p->n_cond, p->dtype,
-                    p->schedule, (int32_t)p->runs, p->row_copies, p->box_stride})
+                    p->schedule, (int32_t)p->runs, p->row_copies, p->box_stride,
+                    (int32_t)p->split})
     w.pod(v);
   w.pod(p->kept_macs);
   w.vec(p->subtiles);
@@ -828,12 +871,13 @@ int tw_plan_load(tw_plan** out, const void* buf, uint64_t len, void* stream) {
   if (r.pod<uint32_t>() != kTwpVersion) return fail(TW_ERR_CORRUPT, "unsupported TWP1 version");
   auto plan = new tw_plan();
   std::unique_ptr<tw_plan> guard(plan);
-  int32_t runs = 0;
+  int32_t runs = 0, split = 0;
   for (int32_t* f : {&plan->k, &plan->n, &plan->g, &plan->n_tiles, &plan->n_sub, &plan->bn,
                      &plan->kp, &plan->n_cond, &plan->dtype, &plan->schedule, &runs,
-                     &plan->row_copies, &plan->box_stride})
+                     &plan->row_copies, &plan->box_stride, &split})
     *f = r.pod<int32_t>();
   plan->runs = runs != 0;
+  plan->split = split != 0;
   plan->kept_macs = r.pod<int64_t>();
   plan->subtiles = r.vec<SubTile>();
   plan->cond_cols = r.vec<int32_t>();
@@ -867,7 +911,7 @@ int tw_plan_load(tw_plan** out, const void* buf, uint64_t len, void* stream) {
         st.pay_row < 0 || st.pay_row + kBN > plan->n_sub * kBN)
       return fail(TW_ERR_CORRUPT, "TWP1 sub-tile table out of range");
   for (int32_t v : plan->h_gidx)
-    if (v < -1 || v >= plan->k) return fail(TW_ERR_CORRUPT, "TWP1 gather list out of range");
+    if (v < -1 || v >= plan->k_rows()) return fail(TW_ERR_CORRUPT, "TWP1 gather list out of range");
   if (plan->runs) {
     const int64_t rows_l = (int64_t)plan->k * plan->row_copies;
     if ((int64_t)plan->perm.size() != rows_l || (int64_t)plan->inv.size() != rows_l ||
@@ -980,6 +1024,20 @@ int tw_plan_attach_overlay(tw_plan* p, int32_t k, int32_t n, int64_t nnz, const 
       rows.push_back((int32_t)row_idx[e]);
       vals.push_back(values[e]);
     }
+    if (p->split) {
+      // fp32 plans: v.a ~ v_hi.a_hi + v_lo.a_hi + v_hi.a_lo (rows r, r, k + r)
+      const size_t b = rows.size() - (size_t)(col_ptr[c + 1] - col_ptr[c]);
+      const size_t e1 = rows.size();
+      for (size_t e = b; e < e1; ++e) {
+        const float hi = __half2float(__float2half_rn(vals[e]));
+        const float lo = __half2float(__float2half_rn(vals[e] - hi));
+        vals[e] = hi;
+        rows.push_back(rows[e]);
+        vals.push_back(lo);
+        rows.push_back(rows[e] + k);
+        vals.push_back(hi);
+      }
+    }
     start.push_back((int32_t)rows.size());
     out_rows.push_back(pos_of[c]);
     acc.push_back(p->tile_of_col[c] >= 0 ? 1 : 0);
@@ -1014,9 +1072,10 @@ int tw_plan_attach_overlay(tw_plan* p, int32_t k, int32_t n, int64_t nnz, const 
   // one 4-byte load (1 instead of 2 per lane: less padding, 11.5 entries per
   // column on BERT).
   int32_t new_block_tokens = 0, new_ctas_per_sm = 0;
-  if (k < 65535 && !ov_cols.empty() && !env_int("TW_RESIDUAL_DIRECT", 0)) {
+  const int32_t kr = p->k_rows();  // rows of the kernels' A^T (2k for fp32 plans)
+  if (kr < 65535 && !ov_cols.empty() && !env_int("TW_RESIDUAL_DIRECT", 0)) {
     int cps = 0;
-    const int T = residual_block_tokens(k, &cps);
+    const int T = residual_block_tokens(kr, &cps);
     if (T > 0) {
       new_block_tokens = T;
       new_ctas_per_sm = cps;
@@ -1060,14 +1119,14 @@ int tw_plan_attach_overlay(tw_plan* p, int32_t k, int32_t n, int64_t nnz, const 
         for (int32_t e : order)
           rv.push_back(((uint32_t)rows[e] << 16) |
                        (p->dtype == kBF16 ? float_to_bf16_bits(vals[e]) : float_to_half_bits(vals[e])));
-        while (rv.size() % G) rv.push_back((uint32_t)k << 16);  // zero row, value 0
+        while (rv.size() % G) rv.push_back((uint32_t)kr << 16);  // zero row, value 0
       }
       // A lane group keeps prefetching (two groups ahead) until the longest
       // list of its warp is done, so the lists at the end need that much
       // zero-row padding behind them.
       int32_t max_len = 0;
       for (size_t i = 0; i < ov_cols.size(); ++i) max_len = std::max(max_len, start[i + 1] - start[i]);
-      rv.resize(rv.size() + ((size_t)(max_len + G - 1) / G + 2) * G, (uint32_t)k << 16);
+      rv.resize(rv.size() + ((size_t)(max_len + G - 1) / G + 2) * G, (uint32_t)kr << 16);
       // device form: value << 16 | row offset in 16-byte units of the staged
       // block (row * T * 2 / 16 = row * G < 2^16 since the block is <= 200 KB),
       // so K2 forms the shared-memory address with one mask and one shift-add
@@ -1149,13 +1208,13 @@ int tw_plan_get_info(const tw_plan* p, tw_plan_info* info) {
   info->kp = p->kp;
   info->n_condensed = p->n_cond;
   info->n_union = (int32_t)p->union_cols.size();
-  info->compute_dtype = p->dtype;
+  info->compute_dtype = p->split ? kF32 : p->dtype;
   info->nnz = p->nnz;
   info->kept_macs_per_token = p->kept_macs + p->nnz;
   info->sm_count = p->sm_count;
   info->has_overlay = p->has_overlay ? 1 : 0;
   info->row_runs = p->runs ? 1 : 0;
-  info->row_copies = p->runs ? p->row_copies : 1;
+  info->row_copies = p->runs ? p->row_copies : p->split ? 2 : 1;
   info->sm_budget = p->sm_budget;
   int64_t steps = 0;
   for (const SubTile& st : p->subtiles) steps += st.kp_steps;
@@ -1416,6 +1475,11 @@ int tw_plan_prepare(const tw_plan* p, const void* a, int32_t a_dtype, int64_t m,
   if (!p || !a || !at) return fail(TW_ERR_INVALID_INPUT, "null argument");
   if (m < 1 || lda < p->k || ld_at < m) return fail(TW_ERR_INVALID_INPUT, "bad prepare geometry");
   if (int st = check_dtype(a_dtype)) return st;
+  if (p->split) {  // A -> [A_hi^T; A_lo^T]
+    TW_CUDA(launch_transpose_split(a, a_dtype, m, p->k, lda, at, ld_at,
+                                   static_cast<cudaStream_t>(stream)));
+    return TW_OK;
+  }
   for (int gi = 0; gi < (p->runs ? p->row_copies : 1); ++gi)
     TW_CUDA(launch_transpose_cast(a, a_dtype, m, p->k, lda, at, p->dtype, ld_at,
                                   p->runs ? p->d_inv + (size_t)gi * p->k : nullptr,
@@ -1428,6 +1492,7 @@ int tw_plan_permute_rows(const tw_plan* p, const void* at, int64_t m, int64_t ld
   g_last_error.clear();
   if (!p || !at || !x) return fail(TW_ERR_INVALID_INPUT, "null argument");
   if (m < 1 || ld_at < m || ld_x < m) return fail(TW_ERR_INVALID_INPUT, "bad permute geometry");
+  if (p->split) return fail(TW_ERR_INVALID_INPUT, "fp32 plans take A (m x k), see tw_plan_prepare");
   const int64_t rows = (int64_t)p->k * (p->runs ? p->row_copies : 1);
   if (!p->runs) {
     TW_CUDA(cudaMemcpy2DAsync(x, ld_x * 2, at, ld_at * 2, m * 2, p->k, cudaMemcpyDeviceToDevice,
@@ -1471,7 +1536,7 @@ static int launch_k2(const tw_plan* p, const void* x, int64_t m, int64_t ld_x, v
   r.n_cols = n_cols;
   r.src = src;
   r.ld_src = ld_src;
-  r.K = p->k;
+  r.K = p->k_rows();
   r.acc_all = acc_all ? 1 : 0;
   const int esz = out_dtype == kF32 ? 4 : 2;
   auto al16 = [](const void* q, int64_t ld, int e) {

@@ -144,6 +144,10 @@ cudaError_t launch_transpose_cast(const void* a, int32_t a_dtype, int64_t M, int
                                   int64_t lda, void* at, int32_t at_dtype, int64_t ld_at,
                                   const int32_t* out_row, cudaStream_t stream);
 
+// fp32 plans: A (M x K) -> [fp16(A)^T; fp16(A - fp16(A))^T] (2K x M fp16).
+cudaError_t launch_transpose_split(const void* a, int32_t a_dtype, int64_t M, int64_t K,
+                                   int64_t lda, void* at, int64_t ld_at, cudaStream_t stream);
+
 // Payload build: packed transposed fp32 CTO payload -> padded [n_sub*kBN][Kp] fp16/bf16
 // (kept-row order, as formats.py:200 stores it).
 struct PayloadArgs {

@@ -86,8 +86,10 @@ class TwPlan:
             raise InvalidInputError(f"row_layout must be 'natural' or 'runs', got {row_layout!r}")
         self.row_layout = row_layout
         self.compute_dtype = _dtype_name(compute_dtype)
-        if self.compute_dtype == "fp32":
-            raise InvalidInputError("compute_dtype must be fp16 or bf16 (tensor-core inputs)")
+        # fp32: the operands are split into fp16 hi + lo pairs (three fp16
+        # products, fp32-class accuracy); the kernels read fp16
+        self.split = self.compute_dtype == "fp32"
+        self.operand_dtype = "fp16" if self.split else self.compute_dtype
         self.schedule = schedule
         self.device = torch.cuda.current_device()
         self.original_dims = enc.original_dims
@@ -164,7 +166,10 @@ class TwPlan:
         self.device = torch.cuda.current_device()
         self._refresh_info()
         info = self.info
-        self.compute_dtype = {_native.TW_F16: "fp16", _native.TW_BF16: "bf16"}[info.compute_dtype]
+        self.compute_dtype = {_native.TW_F16: "fp16", _native.TW_BF16: "bf16",
+                              _native.TW_F32: "fp32"}[info.compute_dtype]
+        self.split = self.compute_dtype == "fp32"
+        self.operand_dtype = "fp16" if self.split else self.compute_dtype
         self.schedule = "lpt"
         self.row_layout = "runs" if info.row_runs else "natural"
         self.original_dims = (int(info.k), int(info.n))
@@ -276,9 +281,11 @@ class TwPlan:
             if len(m_k) != 2 or m_k[1] != k:
                 raise InvalidInputError(
                     f"inner dims disagree: a has {m_k[-1]} cols, weights have K={k}")
-            if not self.uses_row_runs:
+            if not self.uses_row_runs and not self.split:
                 return prepare_activations(a, self.compute_dtype, stream=stream, out=out)
             return self._prepare_runs(a, stream, out)
+        if self.split:
+            raise InvalidInputError("fp32 plans split A into fp16 hi / lo rows: pass a (M x K)")
         if not isinstance(at, torch.Tensor) or not at.is_cuda or at.dim() != 2:
             raise InvalidInputError("at must be a 2-D CUDA tensor (K x M)")
         if at.shape[0] != k:
@@ -287,10 +294,10 @@ class TwPlan:
         if self.uses_row_runs:
             # the row permutation into the plan layout runs in the library
             # (tw_plan_permute_rows); a dtype cast, if needed, comes first
-            if at.dtype != _torch_dtype(self.compute_dtype):
-                at = at.to(_torch_dtype(self.compute_dtype))
+            if at.dtype != _torch_dtype(self.operand_dtype):
+                at = at.to(_torch_dtype(self.operand_dtype))
             m = int(at.shape[1])
-            if not _at_ready(at, self.compute_dtype):
+            if not _at_ready(at, self.operand_dtype):
                 at = at.contiguous() if m % 8 == 0 else \
                     torch.nn.functional.pad(at, (0, (-m) % 8))[:, :m]
             rows = self.layout_rows
@@ -301,12 +308,12 @@ class TwPlan:
                 self._handle, at.data_ptr(), m, at.stride(0) if at.shape[0] > 1 else ld,
                 x.data_ptr(), ld, _native.stream_handle(stream)))
             return x[:, :m]
-        if _at_ready(at, self.compute_dtype):
+        if _at_ready(at, self.operand_dtype):
             return at
         # (after the row permutation at has layout_rows rows: row_copies x K)
         rows, m = int(at.shape[0]), int(at.shape[1])
         ld = (m + 7) // 8 * 8
-        buf = torch.zeros((rows, ld), dtype=_torch_dtype(self.compute_dtype), device=at.device)
+        buf = torch.zeros((rows, ld), dtype=_torch_dtype(self.operand_dtype), device=at.device)
         buf[:, :m].copy_(at)
         return buf[:, :m]
 
@@ -324,12 +331,12 @@ class TwPlan:
         m = int(src.shape[0])
         rows = self.layout_rows
         if out is not None:
-            if tuple(out.shape) != (rows, m) or not _at_ready(out, self.compute_dtype):
+            if tuple(out.shape) != (rows, m) or not _at_ready(out, self.operand_dtype):
                 raise InvalidInputError(f"out must be a {rows} x M A^T view in the compute dtype")
             at, ld = out, out.stride(0)
         else:
             ld = (m + 7) // 8 * 8
-            at = torch.empty((rows, ld), dtype=_torch_dtype(self.compute_dtype), device=src.device)
+            at = torch.empty((rows, ld), dtype=_torch_dtype(self.operand_dtype), device=src.device)
         lib = _native.load_library()
         _native.check(lib.tw_plan_prepare(self._handle, src.data_ptr(),
                                           _DTYPE_CODES[_dtype_name(src.dtype)], m, src.stride(0),
@@ -341,7 +348,7 @@ class TwPlan:
     def layout_rows(self) -> int:
         """Rows of run()'s input: K, or row_copies x K in the row-run layout."""
         k = self.original_dims[0]
-        return k * int(self.info.row_copies) if self.uses_row_runs else k
+        return k * int(self.info.row_copies) if (self.uses_row_runs or self.split) else k
 
     def _check_x(self, x, rows=None):
         torch = _torch()
@@ -351,10 +358,10 @@ class TwPlan:
         if x.dim() != 2 or x.shape[0] != k:
             raise InvalidInputError(f"x must be {k} x M (plan layout rows x tokens), "
                                     f"got {tuple(x.shape)}")
-        if x.dtype != _torch_dtype(self.compute_dtype):
+        if x.dtype != _torch_dtype(self.operand_dtype):
             raise InvalidInputError(f"x dtype {x.dtype} != plan compute dtype "
-                                    f"{self.compute_dtype}")
-        if not _at_ready(x, self.compute_dtype):
+                                    f"{self.operand_dtype}")
+        if not _at_ready(x, self.operand_dtype):
             raise InvalidInputError("x must have unit token stride, a token pitch that is a "
                                     "multiple of 8 and a 16-byte aligned base "
                                     "(use TwPlan.prepare)")
@@ -392,7 +399,7 @@ class TwPlan:
         use_plan = self.uses_row_runs if x_layout is None else x_layout == "plan"
         if use_plan and not self.info.row_runs:
             raise InvalidInputError("this plan has no row-run layout")
-        rows = self.original_dims[0] * int(self.info.row_copies) if use_plan else None
+        rows = self.layout_rows if (use_plan or self.split) else None
         m, ld = self._check_x(x, rows)
         ct = self._out(self.info.n_condensed, m, out, out_dtype)
         lib = _native.load_library()
@@ -415,8 +422,7 @@ class TwPlan:
         if use_plan and not self.info.row_runs:
             raise InvalidInputError("this plan has no row-run layout")
         torch = _torch()
-        m, ld = self._check_x(x, self.original_dims[0] * int(self.info.row_copies)
-                              if use_plan else None)
+        m, ld = self._check_x(x, self.layout_rows if (use_plan or self.split) else None)
         ct = self._out(self.info.n_union, m, out, out_dtype)
         lib = _native.load_library()
         code = _DTYPE_CODES[_dtype_name(ct.dtype)]
@@ -452,8 +458,7 @@ class TwPlan:
             raise InvalidInputError(f"unknown x_layout {x_layout!r}")
         use_plan = self.uses_row_runs if x_layout is None else x_layout == "plan"
         torch = _torch()
-        m, ld = self._check_x(x, self.original_dims[0] * int(self.info.row_copies)
-                              if use_plan else None)
+        m, ld = self._check_x(x, self.layout_rows if (use_plan or self.split) else None)
         if not isinstance(tile_ct, torch.Tensor) or not tile_ct.is_cuda or tile_ct.dim() != 2 \
                 or tile_ct.shape[1] != m or (m > 1 and tile_ct.stride(1) != 1):
             raise InvalidInputError("tile_ct must be a CUDA (columns x M) tensor with unit "

@@ -26,6 +26,10 @@ TOL = {"fp32": 1e-5, "fp16": 1e-3, "bf16": 8e-3}
 # fp32 inputs rounded once to fp16 (both operands, K' ~ 500): measured
 # 4-6e-4 against the fp64 reference on the unrounded values
 TOL_FP16_ROUNDED_INPUTS = 2e-3
+# compute_dtype="fp32" (fp16 hi/lo operand pairs, 3 K' products accumulated
+# in the tensor cores' fp32): measured 1.1e-5 at K' = 1536 (4608 terms),
+# ~4e-6 at K' ~ 400
+TOL_FP32_SPLIT = 3e-5
 
 
 def test_configs0_full_size():
@@ -52,6 +56,38 @@ def test_configs0_full_size():
     for od in ("fp16", "bf16"):
         o = tw.gemm_cto(a16, enc16, out_dtype=od)
         assert tw.relative_error(o.condensed, orc.c_gemm_cto_enc(a16, enc16)) <= TOL[od]
+    # fp32 compute (fp16 hi / lo operand pairs): the reference's fp32 inputs
+    # as they are, fp32-class accuracy against its fp64 result
+    o32 = tw.gemm_cto(a, enc, compute_dtype="fp32")
+    assert tw.relative_error(o32.condensed, exact) <= TOL_FP32_SPLIT
+    t32, _ = tw.execute_batched(a, tsm, workers=4, compute_dtype="fp32")
+    assert np.array_equal(t32.condensed.cpu().numpy(), o32.condensed.cpu().numpy())
+
+
+@pytest.mark.parametrize("k,n,m,s,g,delta", [
+    (768, 768, 500, 0.75, 128, 0.0),
+    (1000, 700, 333, 0.6, 64, 0.02),    # ragged + TEW through K2 (2K-row staged block)
+    (3072, 768, 256, 0.75, 128, 0.015),
+])
+def test_fp32_compute_on_unrounded_inputs(k, n, m, s, g, delta):
+    """compute_dtype='fp32' on fp32 data that is NOT fp16-representable:
+    within TOL_FP32_SPLIT of the fp64 oracle (fp16 rounding alone costs ~1e-3)."""
+    rng = np.random.default_rng(k + n)
+    w = rng.normal(size=(k, n)).astype(np.float32)
+    a = rng.normal(size=(m, k)).astype(np.float32)
+    if delta:
+        _, tsm, ov = tw.prune_tew(w, s, delta, g)
+        out = tw.gemm_tew(a, tsm, ov, compute_dtype="fp32")
+        ref, union = orc.tew_reference(a, tw.encode_cto(tsm), ov.col_ptr, ov.row_idx, ov.values, n)
+        assert np.array_equal(out.column_map.kept, union)
+        h = tw.gemm_tew(a, tsm, ov)                     # fp16 operands, for contrast
+    else:
+        _, tsm = tw.prune_tw(w, s, g)
+        out = tw.gemm_tile_sparse(a, tsm, compute_dtype="fp32")
+        ref = orc.c_gemm_cto_enc(a, tw.encode_cto(tsm))
+        h = tw.gemm_tile_sparse(a, tsm)
+    assert tw.relative_error(out.condensed, ref) <= TOL_FP32_SPLIT
+    assert tw.relative_error(h.condensed, ref) > 1e-4      # the split is what buys it
 
 
 @pytest.mark.parametrize("layer", [0, 1, 2])
