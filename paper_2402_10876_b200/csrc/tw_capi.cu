@@ -13,6 +13,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -1377,6 +1378,31 @@ static int build_tw_launch(const tw_plan* p, const void* x, int64_t m, int64_t l
     a.owner = 0;
     a.n_units = (int32_t)(p->n_sub * ((m + kTN - 1) / kTN));
     grid = std::min(a.n_units, p->sm_budget);
+    // L2-aware unit order: a wave of `grid` units touches sg payloads and
+    // about grid / sg token blocks of A^T; choose the largest sg whose
+    // working set fits in ~3/4 of L2 (126 MB), so payloads and A^T blocks
+    // are fetched from DRAM about once per group instead of once per wave
+    // (configs[4]: 64 payloads of 2 MB = all of L2 when every wave touches
+    // every sub-tile)
+    const double l2 = 0.85 * 126e6;
+    const double pay_b = (double)kBN * p->kp * 2;                 // one sub-tile's payload
+    const double blk_b = (double)p->k * p->row_copies * kTN * 2;  // one token block of A^T
+    int sg = p->n_sub;
+    if (!env_int("TW_NO_SUBGROUP", 0)) {
+      // working set of one wave: sg payloads + the ~grid / sg token blocks
+      auto ws = [&](int g) { return g * pay_b + (std::ceil((double)grid / g) + 1.0) * blk_b; };
+      int best = p->n_sub;
+      for (int g = p->n_sub; g >= 1; --g)
+        if (ws(g) < ws(best)) best = g;
+      while (sg > 1 && ws(sg) > l2) --sg;  // the largest group that fits ...
+      if (ws(sg) > l2) sg = best;          // ... else the smallest working set
+      // prefer whole waves of distinct sub-tiles: round down to a divisor-friendly size
+      if (sg < p->n_sub) {
+        const int ngrp = (p->n_sub + sg - 1) / sg;
+        sg = (p->n_sub + ngrp - 1) / ngrp;
+      }
+    }
+    a.sub_group = std::max(1, sg);
   }
   bool& resident = L.resident;
   resident = a.owner && p->resident;

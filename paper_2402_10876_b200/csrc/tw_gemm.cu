@@ -137,8 +137,16 @@ struct Walker {
       return true;
     }
     if (u >= a.n_units) return false;
-    const int mb = u / a.n_sub;
-    g.sub = u - mb * a.n_sub;
+    // units in sub-tile groups of a.sub_group (host: the group's payloads
+    // plus the token blocks one wave touches fit in L2), token-block-major
+    // inside a group; one group = the whole layer when sub_group >= n_sub
+    const int n_mb = (a.M + kTileN - 1) / kTileN;
+    const int sg = a.sub_group;
+    const int grp = u / (n_mb * sg);
+    const int local = u - grp * n_mb * sg;
+    const int sz = min(sg, a.n_sub - grp * sg);
+    const int mb = local / sz;
+    g.sub = grp * sg + (local - mb * sz);
     g.ub = mb * kTileN;
     g.ue = min(a.M, g.ub + kTileN);
     g.d = tab[g.sub];

@@ -58,6 +58,7 @@ struct GemmArgs {
   int32_t M;
   int32_t n_sub;
   int32_t n_units;          // strided mode: n_sub * ceil(M / kTN)
+  int32_t sub_group;        // strided mode: sub-tiles per L2-resident group (>= 1)
   int32_t owner;            // 1 = one sub-tile + token range per CTA (WorkTable), 0 = strided units
   int32_t flags;            // diagnostics (kFlag*); 0 in production
   int32_t vec_ok;           // output rows 16-byte aligned: vector stores allowed
