@@ -729,22 +729,17 @@ def run_ours(args, cfg, rank: int, world: int) -> None:
     del dense, dense_graphs
 
     # ---- row-major callers: A (M x K, fp16, device) -> A^T per layer (K4)
-    a_dev = [torch.from_numpy(activations(cfg, L["k"], li, rank)).to(dev, torch.float16)
-             for li, L in enumerate(layers)]
+    # (one row-major A per rotating set, so every transpose reads cold data)
+    a_dev = [[torch.from_numpy(activations(cfg, L["k"], li, rank)).to(dev, torch.float16)
+              for li, L in enumerate(layers)] for _ in range(N_ROTATE)]
 
-    def prep_set(r: int):
+    def prep_set(i: int):
+        r = i % N_ROTATE
         for li, (plan, at, _) in enumerate(sets[r]):
-            plan.prepare(a_dev[li], out=at)
+            plan.prepare(a_dev[r][li], out=at)
 
-    prep_graphs = [capture_graph(lambda r=r: prep_set(r)) for r in range(N_ROTATE)]
-    p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    p0.record(stream)
-    for i in range(args.steps):
-        prep_graphs[i % N_ROTATE].replay()
-    p1.record(stream)
-    torch.cuda.synchronize()
-    prep_ms = p0.elapsed_time(p1) / args.steps
-    del prep_graphs
+    prep_ms = reduce_max(graph_us(prep_set, 4 * N_ROTATE) / 1e3, world)
+    a_dev = a_dev[0]
 
     # ---- e2e through the public API from pinned host memory: per layer
     # H2D of A (M x K fp16, the reference layout) -> prepare (K4) -> run (K1

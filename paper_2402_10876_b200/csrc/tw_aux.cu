@@ -11,6 +11,7 @@
 #include <cuda_fp16.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 namespace tw {
 
@@ -351,31 +352,42 @@ __global__ void transpose_split_kernel(const void* a, int32_t a_dtype, int64_t M
   }
 }
 
-// 16-bit -> 16-bit (same type) 64 x 64 tile transpose with 16-byte loads and
-// stores: each thread reads 8 consecutive k of a row of A and writes 8
-// consecutive m of a row of A^T.  Needs M, K, lda, ld_at multiples of 8 and
-// 16-byte aligned bases.
+// 16-bit -> 16-bit (same type) tile transpose, 64 tokens x KT k per CTA,
+// 16-byte loads and stores: each thread first issues all its row loads
+// (KT / 32 of them, in flight together), then writes 8 consecutive m of a
+// row of A^T per 16-byte store.  Needs M, K, lda, ld_at multiples of 8 and
+// 16-byte aligned bases.  out_row (optional) permutes the A^T rows (the
+// plan's row-run layout).
+template <int KT>
 __global__ void __launch_bounds__(256) transpose16_kernel(const uint16_t* a, int64_t M, int64_t K,
                                                           int64_t lda, uint16_t* at,
                                                           int64_t ld_at, const int32_t* out_row) {
-  // [m][k] with the 8-element k-chunk index XOR-swizzled by (m / 8) % 8, so
-  // the column reads of the second phase hit 8 different banks
-  __shared__ __align__(16) uint16_t tile[64][64];
-  const int64_t k0 = static_cast<int64_t>(blockIdx.x) * 64;
+  constexpr int kChunks = KT / 8;                 // 16-byte chunks per tile row of A
+  constexpr int kItems = 64 * kChunks / 256;      // per thread, both phases
+  // [m][k] with the 8-element k-chunk index XOR-swizzled by m / 8, so the
+  // column reads of the second phase hit 8 different banks
+  __shared__ __align__(16) uint16_t tile[64][KT];
+  const int64_t k0 = static_cast<int64_t>(blockIdx.x) * KT;
   const int64_t m0 = static_cast<int64_t>(blockIdx.y) * 64;
   const int t = threadIdx.x;
+  uint4 v[kItems];
 #pragma unroll
-  for (int r = 0; r < 2; ++r) {
+  for (int r = 0; r < kItems; ++r) {
     const int idx = t + r * 256;
-    const int mi = idx >> 3, kc = idx & 7;
+    const int mi = idx / kChunks, kc = idx % kChunks;
     const int64_t m = m0 + mi, k = k0 + kc * 8;
-    uint4 v = make_uint4(0u, 0u, 0u, 0u);
-    if (m < M && k < K) v = *reinterpret_cast<const uint4*>(a + m * lda + k);
-    *reinterpret_cast<uint4*>(&tile[mi][(kc ^ ((mi >> 3) & 7)) * 8]) = v;
+    v[r] = (m < M && k < K) ? *reinterpret_cast<const uint4*>(a + m * lda + k)
+                            : make_uint4(0u, 0u, 0u, 0u);
+  }
+#pragma unroll
+  for (int r = 0; r < kItems; ++r) {
+    const int idx = t + r * 256;
+    const int mi = idx / kChunks, kc = idx % kChunks;
+    *reinterpret_cast<uint4*>(&tile[mi][(kc ^ (mi >> 3)) * 8]) = v[r];
   }
   __syncthreads();
 #pragma unroll
-  for (int r = 0; r < 2; ++r) {
+  for (int r = 0; r < kItems; ++r) {
     const int idx = t + r * 256;
     const int ki = idx >> 3, mc = idx & 7;
     const int64_t k = k0 + ki, m = m0 + mc * 8;
@@ -486,9 +498,17 @@ cudaError_t launch_transpose_cast(const void* a, int32_t a_dtype, int64_t M, int
                     lda % 8 == 0 && ld_at % 8 == 0 &&
                     reinterpret_cast<uintptr_t>(a) % 16 == 0 && reinterpret_cast<uintptr_t>(at) % 16 == 0;
   if (fast) {
-    dim3 grid(static_cast<unsigned>((K + 63) / 64), static_cast<unsigned>((M + 63) / 64));
-    transpose16_kernel<<<grid, 256, 0, stream>>>(static_cast<const uint16_t*>(a), M, K, lda,
-                                                  static_cast<uint16_t*>(at), ld_at, out_row);
+    // 64 x 128 tiles (4 loads in flight per thread) unless K is small
+    if (K >= 128 && !getenv("TW_T64")) {
+      dim3 grid(static_cast<unsigned>((K + 127) / 128), static_cast<unsigned>((M + 63) / 64));
+      transpose16_kernel<128><<<grid, 256, 0, stream>>>(static_cast<const uint16_t*>(a), M, K,
+                                                        lda, static_cast<uint16_t*>(at), ld_at,
+                                                        out_row);
+    } else {
+      dim3 grid(static_cast<unsigned>((K + 63) / 64), static_cast<unsigned>((M + 63) / 64));
+      transpose16_kernel<64><<<grid, 256, 0, stream>>>(static_cast<const uint16_t*>(a), M, K, lda,
+                                                       static_cast<uint16_t*>(at), ld_at, out_row);
+    }
     return cudaGetLastError();
   }
   dim3 grid(static_cast<unsigned>((K + 31) / 32), static_cast<unsigned>((M + 31) / 32));
