@@ -1,0 +1,22 @@
+"""One K1+K2 (legacy) and one K1+K2m launch on a BERT TEW layer, for ncu
+(-k regex:tw_residual).  LAYER=768x3072 by default."""
+import os
+import sys
+from pathlib import Path
+
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import paper_2402_10876_b200 as tw  # noqa: E402
+
+k, n = (int(v) for v in os.environ.get("LAYER", "768x3072").split("x"))
+m = 8192
+w = tw.round_to(tw.synthetic_matrix(0, k, n, tw.STREAM_WEIGHTS), "fp16")
+a = tw.round_to(tw.synthetic_matrix(0, m, k, tw.STREAM_INPUT), "fp16")
+_, tsm, ov = tw.prune_tew(w, 0.75, 0.015, 128)
+plan = tw.TwPlan(tw.encode_cto(tsm), ov)
+x = plan.prepare(a)
+for legacy in ("1", "0"):
+    os.environ["TW_K2_LEGACY"] = legacy
+    plan.run_tew(x, out_dtype="fp16")
+    torch.cuda.synchronize()
