@@ -82,6 +82,10 @@ typedef struct tw_plan_info {
   int32_t sm_budget;          /* SMs K1 uses (tw_plan_set_sm_budget)     */
   int64_t stage_work;         /* sum over sub-tiles of 64-row k-steps: the
                                  per-token cost model of the work split     */
+  int32_t sparse_payload;     /* 1: every tile's payload is 2:4 along K'
+                                 (TVW, patterns.py:645-717) and K1 runs it on
+                                 tcgen05.mma.sp from a compressed resident
+                                 copy (TW_NO_SPARSE=1: dense tensor cores)  */
 } tw_plan_info;
 
 /* Build a device plan from a CTO encoding held in host memory.

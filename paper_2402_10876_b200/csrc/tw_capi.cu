@@ -139,6 +139,8 @@ struct TwLaunch {  // everything a K1 launch needs besides the plan constants
   CUtensorMap map_out;
   int grid = 0;
   bool resident = false;
+  bool sparse = false;  // tcgen05.mma.sp on the compressed payload
+  bool sparse_resident = false;
 };
 
 struct tw_plan;
@@ -167,7 +169,8 @@ struct tw_plan {
   struct Key {
     const void* x; int64_t m, ld_x; void* ct; int64_t ld_ct; int32_t out_dtype;
     const int32_t* rowmap; int64_t out_rows; bool plan_layout; int32_t budget;
-    int flags, no_tma_store, strided, force_owner, gran, split1, run_max_units;
+    int flags, no_tma_store, strided, force_owner, gran, split1, run_max_units, no_sparse,
+        sparse_resident;
     long long* trace;
     bool operator==(const Key& o) const { return std::memcmp(this, &o, sizeof(Key)) == 0; }
   };
@@ -191,6 +194,15 @@ struct tw_plan {
   int32_t* d_gidx = nullptr;  // [n_tiles][kp] kept rows, -1 padded
   void* d_payload = nullptr;
   CUtensorMap map_pay;
+  // TVW on the sparse tensor cores: every tile's payload is 2:4 along K'
+  // (two nonzeros in each group of four kept rows, K' order); compressed
+  // payload [n_sub * bn][kpc] and per-MMA metadata (tw_gemm.cu, sparse MMA)
+  bool sparse = false;
+  int32_t kpc = 0, meta_cols = 0;
+  void* d_payload_sp = nullptr;
+  uint32_t* d_meta = nullptr;
+  CUtensorMap map_pay_sp;               // resident kernel: 64-column boxes (2 stages), SW128
+  CUtensorMap map_pay_sp64;             // streamed kernel: 32-column slices (1 stage), SW64
   // TEW overlay
   bool has_overlay = false;
   int64_t nnz = 0;
@@ -222,7 +234,8 @@ struct tw_plan {
 
   ~tw_plan() {
     for (void* p : {(void*)d_subtiles, (void*)d_gidx, d_payload, (void*)d_perm, (void*)d_inv,
-                    (void*)d_box_first, (void*)d_boxes, (void*)d_gidx_pos})
+                    (void*)d_box_first, (void*)d_boxes, (void*)d_gidx_pos, d_payload_sp,
+                    (void*)d_meta})
       if (p) cudaFree(p);
     ov.release();
   }
@@ -329,7 +342,7 @@ extern "C" {
 
 const char* tw_last_error(void) { return g_last_error.c_str(); }
 
-int32_t tw_abi_version(void) { return 410; }
+int32_t tw_abi_version(void) { return 420; }
 
 int tw_plan_create_cto(tw_plan** out, int32_t k, int32_t n, int32_t g, int32_t n_tiles,
                        const uint32_t* row_counts, const uint32_t* col_counts,
@@ -566,7 +579,29 @@ int tw_plan_create_cto_ex(tw_plan** out, int32_t k, int32_t n, int32_t g, int32_
   // gather on BERT 768x3072 (G = 3: 21.0 vs 20.9 us), so it is opt-in.
   const int max_copies = grp_of.empty() ? std::max(1, std::min(4, env_int("TW_RUN_COPIES", 1))) : 1;
   const double run_stage_w = env_int("TW_RUN_STAGE_W", 8);
-  if (row_runs && !split && k < (1 << 20) && !env_int("TW_NO_RUNS", 0)) {
+  // TVW payloads (prune_tvw, patterns.py:645-717: 2:4 down every payload
+  // column in K' order) can run on tcgen05.mma.sp (TW_SPARSE=1 at plan
+  // creation) when the metadata fits its 32 TMEM columns (K' <= 1024: 2
+  // sparse MMAs per 64-row stage).  The 2:4 groups are defined in K' order,
+  // so such plans keep the natural row order (no row-run permutation).  Opt-in:
+  // the kernel is bound by activation ingress, so halving the payload bytes
+  // does not pay for losing the row-run TMA boxes or 256-token units on the
+  // BERT shapes (profiles/r2_tvw_sparse.txt)
+  bool sp_ok = !split && kp / kBK <= 16 && env_int("TW_SPARSE", 0) && !env_int("TW_NO_SPARSE", 0);
+  for (int i = 0; i < nt && sp_ok; ++i) {
+    const int32_t h = (int32_t)rc[i], w = (int32_t)cc[i];
+    const float* t = pay_in;
+    int64_t off = 0;
+    for (int j = 0; j < i; ++j) off += (int64_t)rc[j] * cc[j];
+    t += off;
+    for (int32_t c = 0; c < w && sp_ok; ++c)
+      for (int32_t g0 = 0; g0 < h && sp_ok; g0 += 4) {
+        int nz = 0;
+        for (int32_t j = g0; j < std::min(h, g0 + 4); ++j) nz += t[(int64_t)c * h + j] != 0.0f;
+        sp_ok = nz <= 2;
+      }
+  }
+  if (row_runs && !split && !sp_ok && k < (1 << 20) && !env_int("TW_NO_RUNS", 0)) {
     const int stride = kp / kBK + 1;
     for (int G = (nt + 5) / 6; G <= max_copies && G <= nt; ++G) {
       const int per = (nt + G - 1) / G;  // tiles per group
@@ -805,6 +840,61 @@ int tw_plan_create_cto_ex(tw_plan** out, int32_t k, int32_t n, int32_t g, int32_
   if (int st = make_map_2d(&plan->map_pay, plan->d_payload, plan->dtype, kp,
                            (uint64_t)plan->n_sub * bn, kp, kBK, bn))
     return st;
+  if (sp_ok && bn == kBN) {
+    // Compressed payload: per output column, the two values of each group of
+    // four K' rows in K' order (a group with fewer nonzeros keeps zeros at
+    // unused positions), K-major like the dense payload, kpc = K'_max / 2
+    // rounded to whole 64-column boxes (one box = 2 stages).  Metadata: one
+    // u32 per (sparse MMA i = 32 K' rows, TMEM lane); lane m % 8 + 16 (m / 16)
+    // + 8 (k / 16) of row m = output column holds the 4-bit group codes
+    // idx0 | idx1 << 2 of 16 K' rows at bit 16 ((m / 8) % 2) + k % 16
+    // (scripts/sp_probe.cu, exact against a dense product).
+    const int32_t kpc = round_up(kp / 2, kBK);
+    const int32_t mcols = 2 * (kp / kBK);
+    const bool bf = plan->dtype == kBF16;
+    std::vector<uint16_t> pay_sp((size_t)plan->n_sub * bn * kpc, 0);
+    std::vector<uint32_t> meta((size_t)plan->n_sub * mcols * 128, 0);
+    for (int i = 0; i < plan->n_sub; ++i) {
+      const SubTile& st = plan->subtiles[i];
+      const int32_t h = ld2[i];
+      for (int32_t c = 0; c < bn; ++c) {
+        const float* col = c < st.width ? pay_src + base2[i] + (int64_t)c * h : nullptr;
+        uint16_t* dst = pay_sp.data() + ((size_t)i * bn + c) * kpc;
+        for (int32_t g0 = 0; g0 < kp; g0 += 4) {
+          int pos[2] = {0, 1}, np = 0;
+          for (int32_t j = 0; j < 4 && col; ++j)
+            if (g0 + j < h && col[g0 + j] != 0.0f) pos[np++] = j;
+          if (np == 1) {  // pair the nonzero with an unused position, idx0 < idx1
+            if (pos[0] == 3) { pos[1] = 3; pos[0] = 2; } else { pos[1] = pos[0] + 1; }
+          }
+          for (int e = 0; e < 2; ++e) {
+            const int32_t j = g0 + pos[e];
+            const float v = col && j < h ? col[j] : 0.0f;
+            dst[g0 / 2 + e] = (uint16_t)(bf ? float_to_bf16_bits(v) : float_to_half_bits(v));
+          }
+          const uint32_t nib = (uint32_t)pos[0] | (uint32_t)pos[1] << 2;
+          const int32_t mi = g0 / 32, kk = g0 % 32;
+          const int lane = c % 8 + 16 * (c / 16) + 8 * (kk / 16);
+          const int bit = 16 * ((c / 8) % 2) + kk % 16;
+          meta[((size_t)i * mcols + mi) * 128 + lane] |= nib << bit;
+        }
+      }
+    }
+    TW_CUDA(cudaMalloc(&plan->d_payload_sp, pay_sp.size() * 2));
+    TW_CUDA(cudaMemcpyAsync(plan->d_payload_sp, pay_sp.data(), pay_sp.size() * 2,
+                            cudaMemcpyHostToDevice, s));
+    if (int st = upload(&plan->d_meta, meta, s)) return st;
+    TW_CUDA(cudaStreamSynchronize(s));
+    if (int st = make_map_2d(&plan->map_pay_sp, plan->d_payload_sp, plan->dtype, kpc,
+                             (uint64_t)plan->n_sub * bn, kpc, kBK, bn))
+      return st;
+    if (int st = make_map_2d(&plan->map_pay_sp64, plan->d_payload_sp, plan->dtype, kpc,
+                             (uint64_t)plan->n_sub * bn, kpc, kBK / 2, bn, 64))
+      return st;
+    plan->sparse = true;
+    plan->kpc = kpc;
+    plan->meta_cols = mcols;
+  }
   plan->union_cols = plan->cond_cols;
   *out = guard.release();
   return TW_OK;
@@ -1217,6 +1307,7 @@ int tw_plan_get_info(const tw_plan* p, tw_plan_info* info) {
   info->row_runs = p->runs ? 1 : 0;
   info->row_copies = p->runs ? p->row_copies : p->split ? 2 : 1;
   info->sm_budget = p->sm_budget;
+  info->sparse_payload = p->sparse ? 1 : 0;
   int64_t steps = 0;
   for (const SubTile& st : p->subtiles) steps += st.kp_steps;
   info->stage_work = steps;
@@ -1267,12 +1358,14 @@ static int check_io(const tw_plan* p, const void* x, int64_t m, int64_t ld_x, co
 // Diagnostic environment switches that shape a launch,
 // read on every call (getenv is cheap) so tests can flip them per call.
 struct LaunchEnv {
-  int flags, no_tma_store, strided, force_owner, gran, split1, run_max_units;
+  int flags, no_tma_store, strided, force_owner, gran, split1, run_max_units, no_sparse,
+      sparse_resident;
   long long* trace;
   bool operator==(const LaunchEnv& o) const {
     return flags == o.flags && no_tma_store == o.no_tma_store && strided == o.strided &&
            force_owner == o.force_owner && gran == o.gran && split1 == o.split1 &&
-           run_max_units == o.run_max_units && trace == o.trace;
+           run_max_units == o.run_max_units && no_sparse == o.no_sparse &&
+           sparse_resident == o.sparse_resident && trace == o.trace;
   }
 };
 
@@ -1285,6 +1378,9 @@ static LaunchEnv read_launch_env() {
   e.gran = env_int("TW_GRAN", 64);
   e.split1 = env_int("TW_SPLIT1", 0) != 0;
   e.run_max_units = env_int("TW_RUN_MAX_UNITS", 16);
+  // bit 0: TW_NO_SPARSE; bit 1: TW_SPARSE_SW128 (diagnostic payload variant)
+  e.no_sparse = (env_int("TW_NO_SPARSE", 0) ? 1 : 0) | (env_int("TW_SPARSE_SW128", 0) ? 2 : 0);
+  e.sparse_resident = env_int("TW_SPARSE_RESIDENT", 0);
   e.trace = g_trace;
   return e;
 }
@@ -1327,7 +1423,17 @@ static int build_tw_launch(const tw_plan* p, const void* x, int64_t m, int64_t l
   int& grid = L.grid;
   WorkTable& work = L.work;
   bool owner = p->owner && !env.strided;
-  if (owner && !p->resident && !env.force_owner) {
+  // sparse tensor-core path: owner mode with the compressed payload resident
+  int max_steps_all = 0;
+  for (const SubTile& st : p->subtiles) max_steps_all = std::max(max_steps_all, (int)st.kp_steps);
+  // (metadata: 2 TMEM columns per stage, loaded once per CTA -> owner mode);
+  // the compressed payload streams with each stage (4-stage ring) unless
+  // TW_SPARSE_RESIDENT=1 keeps it resident (3 stages: measured slower)
+  const bool sparse = p->sparse && owner && !(env.no_sparse & 1);
+  L.sparse = sparse;
+  L.sparse_resident = sparse && env.sparse_resident &&
+                      (max_steps_all + 1) / 2 <= kResSteps;
+  if (owner && !p->resident && !sparse && !env.force_owner) {
     // Streamed payload: both modes re-stream a sub-tile's payload per unit,
     // so pick the one whose busiest CTA does less (k-steps x tokens).
     int64_t own = 0, max_steps = 0;
@@ -1366,11 +1472,16 @@ static int build_tw_launch(const tw_plan* p, const void* x, int64_t m, int64_t l
         const int64_t b = (int64_t)j * ch / c * gran;
         const int64_t e = std::min<int64_t>(m, (int64_t)(j + 1) * ch / c * gran);
         const int64_t len = std::max<int64_t>(0, e - b);
-        int64_t n = (len + kTN - 1) / kTN;
+        // sparse: the metadata sits in TMEM columns 480-511, inside the second
+        // accumulator buffer (256-511), so units that can land there (every
+        // odd unit of a CTA with two or more) stop at kSparseMaxTokens; a
+        // one-unit range keeps the full 256 tokens in buffer 0
+        const int64_t cap = sparse && len > kTN ? kSparseMaxTokens : kTN;
+        int64_t n = (len + cap - 1) / cap;
         if (split_single && n == 1 && len >= 2 * gran) n = 2;
         w.b = (int32_t)b;
         w.e = (int32_t)std::max(b, e);
-        w.usz = n > 0 ? (int32_t)std::min<int64_t>(kTN, ((len + n - 1) / n + gran - 1) / gran * gran)
+        w.usz = n > 0 ? (int32_t)std::min<int64_t>(cap, ((len + n - 1) / n + gran - 1) / gran * gran)
                       : 0;
       }
     }
@@ -1405,7 +1516,14 @@ static int build_tw_launch(const tw_plan* p, const void* x, int64_t m, int64_t l
     a.sub_group = std::max(1, sg);
   }
   bool& resident = L.resident;
-  resident = a.owner && p->resident;
+  resident = a.owner && (sparse ? L.sparse_resident : p->resident);
+  if (sparse) {
+    // 1: 32-column SW64 payload slices per stage; 2 (TW_SPARSE_SW128=1,
+    // diagnostics): the 64-column SW128 box per stage, half of it used
+    a.sparse = (env.no_sparse & 2) ? 2 : 1;
+    a.meta = p->d_meta;
+    a.meta_cols = p->meta_cols;
+  }
   // Plan-layout input: TMA row runs unless a CTA has many units.  Runs win
   // where the gather is L2->SM-bound (3072x768 21.4 -> 17.3 us; VGG conv4_2
   // at 6 units per CTA 218 -> 160 us); on long HBM-streaming ranges (VGG
@@ -1462,7 +1580,8 @@ static int run_tw(const tw_plan* p, const void* x, int64_t m, int64_t ld_x, void
   key.plan_layout = plan_layout; key.budget = p->sm_budget;
   key.flags = env.flags; key.no_tma_store = env.no_tma_store; key.strided = env.strided;
   key.force_owner = env.force_owner; key.gran = env.gran; key.split1 = env.split1;
-  key.run_max_units = env.run_max_units; key.trace = env.trace;
+  key.run_max_units = env.run_max_units; key.no_sparse = env.no_sparse;
+  key.sparse_resident = env.sparse_resident; key.trace = env.trace;
   if (!(p->cache_valid && p->cache_key == key)) {
     p->cache_valid = false;
     if (int st = build_tw_launch(p, x, m, ld_x, ct, ld_ct, out_dtype, rowmap, out_rows,
@@ -1473,7 +1592,10 @@ static int run_tw(const tw_plan* p, const void* x, int64_t m, int64_t ld_x, void
   }
   const TwLaunch& L = p->cache;
   if (env.flags & 64) return TW_OK;  // diagnostics: host work only, no launch
-  TW_CUDA(launch_tw_gemm(p->map_pay, L.map_out, L.maps, L.a, L.work, L.resident, L.grid, s));
+  const CUtensorMap& mp = !L.sparse                       ? p->map_pay
+                          : (L.resident || L.a.sparse == 2) ? p->map_pay_sp
+                                                            : p->map_pay_sp64;
+  TW_CUDA(launch_tw_gemm(mp, L.map_out, L.maps, L.a, L.work, L.resident, L.grid, s));
   return TW_OK;
 }
 

@@ -89,7 +89,7 @@ struct Cfg {
                                     kEpilogueWarps * kStgBytes + kBarrierBytes + kSubBytes +
                                     kIdxBytes + 1024;
   static_assert(kSmemBytes <= 227 * 1024, "shared memory budget");
-  static_assert(2 * kStages + kResSteps + 4 + 2 <= kBarrierBytes / 8, "barrier region");
+  static_assert(2 * kStages + kResSteps + 4 + 3 <= kBarrierBytes / 8, "barrier region");
 };
 
 // One unit of work: sub-tile d over tokens [ub, ue).
@@ -307,6 +307,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   // gather warps then join that unit's epilogue (a parity wait on tfull could
   // alias an earlier phase)
   uint64_t* jbar = pfull + kResSteps + 1;
+  // sparse plans: the four metadata writers (one per TMEM lane quadrant) are done
+  uint64_t* mfull = jbar + 1;
   SubTile* sub_smem = reinterpret_cast<SubTile*>(bar_region + C::kBarrierBytes);
   int32_t* sIdx = reinterpret_cast<int32_t*>(bar_region + C::kBarrierBytes + C::kSubBytes);
   long long* trace = args.trace ? args.trace + static_cast<int64_t>(blockIdx.x) * 4096 : nullptr;
@@ -325,6 +327,20 @@ __global__ void __launch_bounds__(kThreads, 1)
   // lists, payload), so it overlaps the previous kernel's tail under
   // programmatic dependent launch; activations are read and outputs written
   // only after grid_dependency_wait() in the gather and epilogue roles.
+  // sparse plans: the metadata writers (epilogue warps 0-3, one per TMEM
+  // lane quadrant) load the owned sub-tile's metadata now, so the loads
+  // overlap the prologue (and, under PDL, the previous kernel's tail)
+  uint32_t meta_v[32];
+  const bool meta_writer = args.sparse && !(args.flags & kFlagSkipMeta) && warp >= kEpilogueWarp0 &&
+                           warp < kEpilogueWarp0 + 4;
+  if (meta_writer) {
+    const CtaWork& w = work.w[blockIdx.x];
+    const int n = w.usz > 0 ? 2 * w.kp_steps : 0;
+    const uint32_t* mp = args.meta + static_cast<int64_t>(w.pay_row / kBN) * args.meta_cols * 128 +
+                         (warp & 3) * 32 + lane;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) meta_v[i] = i < n ? __ldg(mp + i * 128) : 0u;
+  }
   const SubTile* tab = args.subtiles;
   if (!kRes && !args.owner && args.n_sub <= kMaxSmemSub) {
     for (int i = threadIdx.x; i < args.n_sub; i += kThreads) sub_smem[i] = args.subtiles[i];
@@ -345,6 +361,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int k = 0; k < kResSteps; ++k) mbar_init(&pfull[k], 1);
     mbar_init(jbar, 1);
+    mbar_init(mfull, 4);
     fence_barrier_init();
     fence_proxy_async_smem();
   }
@@ -382,7 +399,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       Seg s0;
       if (w0.next(args, s0)) {
         const bool skip_p = flags & kFlagSkipP;
-        for (int ks = 0; ks < s0.d.kp_steps; ++ks) {
+        // sparse payload: one 64-column box holds 2 stages (128 K' rows, 2:4)
+        const int nbox = args.sparse ? (s0.d.kp_steps + 1) / 2 : s0.d.kp_steps;
+        for (int ks = 0; ks < nbox; ++ks) {
           if (!args.runs) mbar_wait(&empty[ks % kStages], ((ks / kStages) & 1) ^ 1u);
           if (skip_p) {
             mbar_arrive(&pfull[ks]);
@@ -446,8 +465,16 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_arrive(&full[stage]);
             continue;
           }
-          mbar_arrive_expect_tx(&full[stage], kPBytes);
-          tma_load_2d(sP + stage * kPBytes, &map_pay, &full[stage], ks * kBK, sg.d.pay_row);
+          if (args.sparse == 1) {  // the stage's 32 compressed columns (2:4), 64-B swizzle
+            mbar_arrive_expect_tx(&full[stage], kPBytes / 2);
+            tma_load_2d(sP + stage * kPBytes, &map_pay, &full[stage], ks * (kBK / 2), sg.d.pay_row);
+          } else if (args.sparse == 2) {  // the 64-column SW128 box holding this stage's half
+            mbar_arrive_expect_tx(&full[stage], kPBytes);
+            tma_load_2d(sP + stage * kPBytes, &map_pay, &full[stage], (ks >> 1) * kBK, sg.d.pay_row);
+          } else {
+            mbar_arrive_expect_tx(&full[stage], kPBytes);
+            tma_load_2d(sP + stage * kPBytes, &map_pay, &full[stage], ks * kBK, sg.d.pay_row);
+          }
         }
       }
     }
@@ -610,25 +637,49 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ---------------------------------------------------------- MMA issuer
     if (lane == 0) {
       const uint32_t in_fmt = args.in_dtype == kBF16 ? 1u : 0u;
+      const bool sparse = args.sparse;
       int gs = 0;
       int j = 0;
+      if (sparse && !(flags & kFlagSkipMeta)) {  // the CTA's metadata is in tensor memory
+        mbar_wait(mfull, 0);
+        tc_fence_after();
+      }
       while (walk.next(args, sg)) {
         const int acc = j & 1;
         const uint32_t idesc = umma_idesc_f16(kBN, (sg.ue - sg.ub + 15) & ~15, in_fmt,
-                                              /*a (payload) K-major*/ 0u, /*b (A^T) MN-major*/ 1u);
+                                              /*a (payload) K-major*/ 0u, /*b (A^T) MN-major*/ 1u) |
+                               (sparse ? 4u : 0u);
         mbar_wait(&tempty[acc], ((j >> 1) & 1) ^ 1u);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * kTileN;
         for (int ks = 0; ks < sg.d.kp_steps; ++ks, ++gs) {
           const int stage = gs % kStages;
-          if (kRes) mbar_wait(&pfull[ks], 0);
+          if (kRes) mbar_wait(&pfull[sparse ? ks >> 1 : ks], 0);
           mbar_wait(&full[stage], (gs / kStages) & 1);
           if (trace && gs < 1024) trace[1024 + gs] = clock64();
           tc_fence_after();
           if (!args.runs) fence_proxy_async_smem();  // cp.async (generic proxy) writes -> tcgen05 reads
-          const uint32_t p0 = smem_u32(sP + (kRes ? ks : stage) * kPBytes);
           const uint32_t x0 = smem_u32(sX + stage * kXBytes);
-          if (!(flags & kFlagSkipMma)) {
+          if (sparse && !(flags & kFlagSkipMma)) {
+            // two tcgen05.mma.sp of K = 32 logical rows: A = this stage's 32
+            // compressed columns (64 B of the 128-B SW128 row of box ks / 2,
+            // 32 B = 16 compressed per MMA), B = 32 gathered rows (4 KB),
+            // metadata in column kMetaCol0 + 2 ks + h (pair base + id2 = h)
+            // (streamed: the stage's own 64-B swizzled slice, 512-B atoms)
+            const uint32_t pa = kRes ? smem_u32(sP + (ks >> 1) * kPBytes) + (ks & 1) * 64
+                                : args.sparse == 2 ? smem_u32(sP + stage * kPBytes) + (ks & 1) * 64
+                                                   : smem_u32(sP + stage * kPBytes);
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const uint64_t adesc = (kRes || args.sparse == 2) ? umma_desc_sw128(pa + h * 32, 16, 1024)
+                                                                : umma_desc_sw64(pa + h * 32, 16, 512);
+              const uint64_t bdesc = umma_desc_sw128(x0 + h * 4096, kChunkBytes, 1024);
+              umma_f16_sp(d_tmem, adesc, bdesc, idesc | static_cast<uint32_t>(h),
+                          tmem_base + kMetaCol0 + 2 * ks, (ks != 0) || (h != 0));
+            }
+          }
+          const uint32_t p0 = smem_u32(sP + (kRes ? ks : stage) * kPBytes);
+          if (!sparse && !(flags & kFlagSkipMma)) {
 #pragma unroll
             for (int kk = 0; kk < kBK / 16; ++kk) {
               // A = payload: K-major SW128, SBO = 1 KB between 8-column groups,
@@ -663,6 +714,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint8_t* stg = dbl ? sStg + ew * kStgBytes
                        : reinterpret_cast<uint8_t*>(sIdx) + (ew - kEpilogueWarps) * 1024;
     int sbuf = 0;
+    if (meta_writer) {
+      // sparse MMA metadata of the owned sub-tile (loaded before the prologue,
+      // plan constants): column kMetaCol0 + i for MMA i, this warp's 32 TMEM
+      // lanes, all 32 columns in one store; one arrival per quadrant on mfull
+      tmem_st_32x32b_x32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + kMetaCol0, meta_v);
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(mfull);
+    }
     grid_dependency_wait();  // the previous kernel may still read our output buffer
     int j = 0;
     Walker ahead = walk;  // one unit ahead: is the current unit the last?

@@ -71,7 +71,16 @@ struct GemmArgs {
   const int32_t* box_first; // [n_tiles][box_stride]
   const uint32_t* boxes;    // slot | log2(rows) << 6 | position << 9
   int32_t box_stride;
+  // TVW on the sparse tensor cores (owner mode, resident payload): the payload
+  // holds two of every four K' rows per output column (2:4 along K'), and
+  // every tcgen05.mma.sp (K = 32 logical) reads its metadata from one TMEM
+  // column kMetaCol0 + i, loaded once per CTA from meta
+  int32_t sparse;
+  const uint32_t* meta;     // [n_sub][meta_cols][128] u32, TMEM lane order (tw_capi.cu)
+  int32_t meta_cols;        // sparse MMAs per sub-tile (2 per 64-row stage)
 };
+constexpr int kSparseMaxTokens = 224;  // sparse units: accumulators at 0 / 256, metadata at 480
+constexpr int kMetaCol0 = 480;         // 4-aligned; 32 columns = 16 stages (K' <= 1024)
 
 // Tensor maps over the permuted A^T for box heights 1, 2, 4, ..., 64 rows
 // (64 tokens wide, 128-byte swizzle).
@@ -86,6 +95,7 @@ constexpr int32_t kFlagSkipStore = 2;   // do not write the output
 constexpr int32_t kFlagSkipMma = 4;     // do not issue tcgen05.mma
 constexpr int32_t kFlagNoPdl = 8;       // launch without programmatic dependent launch (timing only)
 constexpr int32_t kFlagSkipP = 16;      // do not load the payload
+constexpr int32_t kFlagSkipMeta = 32;   // sparse: no metadata load / wait
 
 // K1: persistent warp-specialised TW GEMM (tcgen05 + TMA + cp.async gather).
 //   map_pay : payload [n_sub * kBN][Kp], box {64 k, kBN rows}, 128-B swizzle

@@ -83,3 +83,41 @@ def test_tvw_gemm_matches_golden_and_oracle(layout):
     assert tw.relative_error(got, orc.c_gemm_cto_enc(a, enc, threads=8)) <= TOL["fp32"]
     out = tw.gemm_cto(a, enc, out_dtype="fp16")
     assert tw.relative_error(out.condensed.float(), got) <= TOL["fp16"]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("k,n,m,compute", [(768, 768, 8192, "fp16"), (768, 3072, 1000, "fp16"),
+                                           (512, 384, 333, "bf16"), (1024, 1024, 128, "fp16")])
+def test_tvw_sparse_tensor_cores_match_oracle(k, n, m, compute, monkeypatch):
+    """TVW through tcgen05.mma.sp (TW_SPARSE=1): the compressed 2:4 payload
+    and the TMEM metadata (layout pinned by scripts/sp_probe.cu) give the
+    oracle's product; the dense tensor-core path on the same plan agrees."""
+    monkeypatch.setenv("TW_SPARSE", "1")
+    rng = np.random.default_rng(k + n + m)
+    w = tw.round_to(rng.normal(size=(k, n)).astype(np.float32), compute)
+    a = tw.round_to(rng.normal(size=(m, k)).astype(np.float32), compute)
+    _, tsm, _ = tw.prune_tvw(w, 0.75, 128)
+    enc = tw.encode_cto(tsm)
+    plan = tw.TwPlan(enc, compute_dtype=compute)
+    assert plan.info.sparse_payload == 1
+    x = plan.prepare(a)
+    got = plan.run(x).t()
+    idx = np.arange(0, m, max(1, m // 512))
+    ref = orc.c_gemm_cto_enc(a[idx], enc, threads=8)
+    import torch
+    sel = torch.as_tensor(idx, device=got.device)
+    assert tw.relative_error(got[sel].cpu().numpy(), ref) <= TOL["fp32"]
+    monkeypatch.setenv("TW_NO_SPARSE", "1")
+    dense = plan.run(x).t()
+    assert tw.relative_error(got, dense) <= TOL["fp32"]
+
+
+@pytest.mark.gpu
+def test_tvw_sparse_declines_non_24_payloads(monkeypatch):
+    """A TW payload (no 2:4 structure) never takes the sparse path."""
+    monkeypatch.setenv("TW_SPARSE", "1")
+    rng = np.random.default_rng(3)
+    w = tw.round_to(rng.normal(size=(256, 256)).astype(np.float32), "fp16")
+    _, tsm = tw.prune_tw(w, 0.5, 128)
+    plan = tw.TwPlan(tw.encode_cto(tsm))
+    assert plan.info.sparse_payload == 0
