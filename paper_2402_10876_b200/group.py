@@ -173,7 +173,62 @@ class TwPlanGroup:
         """TEW products of every plan (each must carry an overlay)."""
         return self._launch("run_tew", xs, outs, out_dtype)
 
+    def set_budgets(self, budgets: Sequence[int]) -> None:
+        """New SM shares (one per plan, each >= its sub-tile count, summing
+        to at most the GPU).  Launches captured earlier keep their geometry."""
+        floors = [int(p.info.n_sub) for p in self.plans]
+        total = int(self.plans[0].info.sm_count)
+        if len(budgets) != len(self.plans) or sum(budgets) > total or any(
+                b < f for b, f in zip(budgets, floors)):
+            raise InvalidInputError(f"invalid SM shares {list(budgets)} (floors {floors}, {total} SMs)")
+        self.budgets = [int(b) for b in budgets]
+        for p, b in zip(self.plans, self.budgets):
+            p.set_sm_budget(b)
+
     def release(self) -> None:
         """Give every plan the whole GPU again."""
         for p in self.plans:
             p.set_sm_budget(0)
+
+
+def tune_budgets(groups: Sequence["TwPlanGroup"], time_fn, moves=(8, 4, 2), rounds: int = 2):
+    """Measured refinement of the cost model's SM shares (an autotuner):
+    coordinate moves of ``moves`` SMs between every ordered pair of plans,
+    hill-climbing from the current shares, applied to every group in
+    ``groups`` (same plan structure, e.g. rotating buffer sets).  ``time_fn()``
+    must return the time of the caller's step with the groups' current shares
+    (it is called after every change; capture any CUDA graph inside it).
+    Returns (budgets, time, {budgets: time})."""
+    g0 = groups[0]
+    floors = [int(p.info.n_sub) for p in g0.plans]
+    n = len(floors)
+    seen = {}
+
+    def measure(b):
+        key = tuple(b)
+        if key not in seen:
+            for g in groups:
+                g.set_budgets(b)
+            seen[key] = float(time_fn())
+        return seen[key]
+
+    best = list(g0.budgets)
+    best_t = measure(best)
+    for _ in range(rounds):
+        improved = False
+        for d in moves:
+            for i in range(n):
+                for j in range(n):
+                    if i == j or best[i] - d < floors[i]:
+                        continue
+                    cand = list(best)
+                    cand[i] -= d
+                    cand[j] += d
+                    t = measure(cand)
+                    if t < best_t:
+                        best, best_t, improved = cand, t, True
+        if not improved:
+            break
+    for g in groups:
+        g.set_budgets(best)
+    return best, best_t, {k: v for k, v in seen.items()}

@@ -156,3 +156,34 @@ def test_split_sms_floors_and_total():
     assert tw.split_sms([1, 1], [70, 70], 148)[0] >= 70
     with pytest.raises(tw.InvalidInputError):
         tw.split_sms([1, 1], [100, 100], 148)
+
+
+def test_tune_budgets_hill_climbs_to_measured_minimum():
+    """tune_budgets (the measured refinement of TwPlanGroup's SM shares)
+    walks coordinate moves from the model's shares to the fastest measured
+    candidate, respecting every plan's sub-tile floor and the SM total."""
+    from types import SimpleNamespace
+
+    from paper_2402_10876_b200.group import tune_budgets
+
+    class FakeGroup:
+        def __init__(self, budgets, floors):
+            self.budgets = list(budgets)
+            self.plans = [SimpleNamespace(info=SimpleNamespace(n_sub=f)) for f in floors]
+
+        def set_budgets(self, b):
+            assert all(x >= p.info.n_sub for x, p in zip(b, self.plans))
+            assert sum(b) <= 148
+            self.budgets = list(b)
+
+    groups = [FakeGroup([16, 84, 48], [3, 12, 3]) for _ in range(2)]
+    target = (22, 80, 46)
+
+    def time_fn():
+        b = groups[0].budgets
+        assert groups[1].budgets == b          # every group moves together
+        return sum(abs(x - t) for x, t in zip(b, target)) + 10.0
+
+    best, t, seen = tune_budgets(groups, time_fn, moves=(4, 2), rounds=4)
+    assert tuple(best) == target and t == 10.0
+    assert groups[0].budgets == best and all(sum(k) == 148 for k in seen)
