@@ -149,7 +149,6 @@ __global__ void __launch_bounds__(kResThreads, 1)
   const int sub = lane / L;
   const int tl = lane - sub * L;
   const int tok = tl * 8;
-  const int gbase = sub * L;
   const int64_t t0 = static_cast<int64_t>(blockIdx.x) * T;
   const int64_t rem = args.M - t0;
   const int ntok = rem < T ? static_cast<int>(rem) : T;
@@ -219,7 +218,7 @@ __global__ void __launch_bounds__(kResThreads, 1)
       if (eo >= m.y) c = zrow;
 #pragma unroll
       for (int j = 0; j < G; ++j) {
-        const uint32_t q = L == 1 ? c : __shfl_sync(0xffffffffu, c, gbase + j);
+        const uint32_t q = L == 1 ? c : __shfl_sync(0xffffffffu, c, j, L);  // lane j of the group (immediate)
         // PRMT (zero-extended low half) + LEA: two instructions per address
         fma8<kBf>(ac, *reinterpret_cast<const uint4*>(sAb + __byte_perm(q, 0u, 0x4410) * 16u),
                   static_cast<uint16_t>(q >> 16));
@@ -232,9 +231,21 @@ __global__ void __launch_bounds__(kResThreads, 1)
     if (eo < maxlen) {
       if (eo >= m.y) c = zrow;
       const int cnt = maxlen - eo;
+      int j = 0;
+      if (L >= 4 && cnt >= 4) {
+        // four entries unrolled (their shared loads in flight together), the
+        // rest one by one
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) {
+          const uint32_t q = __shfl_sync(0xffffffffu, c, jj, L);
+          fma8<kBf>(ac, *reinterpret_cast<const uint4*>(sAb + __byte_perm(q, 0u, 0x4410) * 16u),
+                    static_cast<uint16_t>(q >> 16));
+        }
+        j = 4;
+      }
 #pragma unroll 1
-      for (int j = 0; j < cnt; ++j) {
-        const uint32_t q = L == 1 ? c : __shfl_sync(0xffffffffu, c, gbase + j);
+      for (; j < cnt; ++j) {
+        const uint32_t q = L == 1 ? c : __shfl_sync(0xffffffffu, c, j, L);  // lane j of the group
         // PRMT (zero-extended low half) + LEA: two instructions per address
         fma8<kBf>(ac, *reinterpret_cast<const uint4*>(sAb + __byte_perm(q, 0u, 0x4410) * 16u),
                   static_cast<uint16_t>(q >> 16));

@@ -1,4 +1,4 @@
-"""One K1+K2 (legacy) and one K1+K2m launch on a BERT TEW layer, for ncu
+"""One TEW launch (K1 + K2) on a BERT TEW layer, for an ncu capture of K2
 (-k regex:tw_residual).  LAYER=768x3072 by default."""
 import os
 import sys
@@ -16,7 +16,5 @@ a = tw.round_to(tw.synthetic_matrix(0, m, k, tw.STREAM_INPUT), "fp16")
 _, tsm, ov = tw.prune_tew(w, 0.75, 0.015, 128)
 plan = tw.TwPlan(tw.encode_cto(tsm), ov)
 x = plan.prepare(a)
-for legacy in ("1", "0"):
-    os.environ["TW_K2_LEGACY"] = legacy
-    plan.run_tew(x, out_dtype="fp16")
-    torch.cuda.synchronize()
+plan.run_tew(x, out_dtype="fp16")
+torch.cuda.synchronize()
