@@ -178,6 +178,16 @@ TW_API int tw_plan_union_columns(const tw_plan* plan, int32_t* out_cols);
 TW_API int tw_gemm(const tw_plan* plan, const void* at, int64_t m, int64_t ld_at, void* ct,
                    int64_t ld_ct, int32_t out_dtype, void* stream);
 
+/* Several independent TW layers in ONE K1 launch (TwPlanGroup): plan i
+   runs on its SM share (tw_plan_set_sm_budget; the shares must sum to at
+   most the GPU) over xs[i] (layout x_layouts[i], NULL = all natural) into
+   cts[i]; all with M tokens and out_dtype.  Bit-identical to n tw_gemm_ex
+   calls.  Replaces the reference's threaded lanes over independent products
+   (execute_batched, executor.py:230-265) at the step level. */
+TW_API int tw_gemm_group(const tw_plan* const* plans, int32_t n, const void* const* xs,
+                         const int64_t* ld_xs, const int32_t* x_layouts, void* const* cts,
+                         const int64_t* ld_cts, int64_t m, int32_t out_dtype, void* stream);
+
 /* tw_gemm with the activation row layout given: TW_LAYOUT_NATURAL (A^T rows
  * in K order, kept rows gathered with cp.async) or TW_LAYOUT_PLAN (A^T as
  * tw_plan_prepare writes it; on plans with row_runs, every stage is a few

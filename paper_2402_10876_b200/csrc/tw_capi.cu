@@ -1568,11 +1568,11 @@ static int build_tw_launch(const tw_plan* p, const void* x, int64_t m, int64_t l
 // work table, the row-run decision) cached per plan for the last geometry:
 // repeated calls on the same buffers (a serving loop, the reference API in a
 // loop) pay only the launch.
-static int run_tw(const tw_plan* p, const void* x, int64_t m, int64_t ld_x, void* ct,
-                  int64_t ld_ct, int32_t out_dtype, const int32_t* rowmap, int64_t out_rows,
-                  cudaStream_t s, bool plan_layout = false) {
-  const LaunchEnv env = read_launch_env();
-  std::lock_guard<std::mutex> lock(p->launch_mu);
+// The plan's cached launch for this geometry (built on a key miss); the
+// caller holds p->launch_mu.
+static int get_launch(const tw_plan* p, const void* x, int64_t m, int64_t ld_x, void* ct,
+                      int64_t ld_ct, int32_t out_dtype, const int32_t* rowmap, int64_t out_rows,
+                      bool plan_layout, const LaunchEnv& env, const TwLaunch** out) {
   tw_plan::Key key;
   std::memset(&key, 0, sizeof(key));  // padding too: keys compare with memcmp
   key.x = x; key.m = m; key.ld_x = ld_x; key.ct = ct; key.ld_ct = ld_ct;
@@ -1590,12 +1590,30 @@ static int run_tw(const tw_plan* p, const void* x, int64_t m, int64_t ld_x, void
     p->cache_key = key;
     p->cache_valid = true;
   }
-  const TwLaunch& L = p->cache;
+  *out = &p->cache;
+  return TW_OK;
+}
+
+// The payload tensor map a launch reads (dense, or the compressed sparse one).
+static const CUtensorMap& launch_payload_map(const tw_plan* p, const TwLaunch& L) {
+  return !L.sparse                         ? p->map_pay
+         : (L.resident || L.a.sparse == 2) ? p->map_pay_sp
+                                           : p->map_pay_sp64;
+}
+
+static int run_tw(const tw_plan* p, const void* x, int64_t m, int64_t ld_x, void* ct,
+                  int64_t ld_ct, int32_t out_dtype, const int32_t* rowmap, int64_t out_rows,
+                  cudaStream_t s, bool plan_layout = false) {
+  const LaunchEnv env = read_launch_env();
+  std::lock_guard<std::mutex> lock(p->launch_mu);
+  const TwLaunch* Lp = nullptr;
+  if (int st = get_launch(p, x, m, ld_x, ct, ld_ct, out_dtype, rowmap, out_rows, plan_layout, env,
+                          &Lp))
+    return st;
+  const TwLaunch& L = *Lp;
   if (env.flags & 64) return TW_OK;  // diagnostics: host work only, no launch
-  const CUtensorMap& mp = !L.sparse                       ? p->map_pay
-                          : (L.resident || L.a.sparse == 2) ? p->map_pay_sp
-                                                            : p->map_pay_sp64;
-  TW_CUDA(launch_tw_gemm(mp, L.map_out, L.maps, L.a, L.work, L.resident, L.grid, s));
+  TW_CUDA(launch_tw_gemm(launch_payload_map(p, L), L.map_out, L.maps, L.a, L.work, L.resident,
+                         L.grid, s));
   return TW_OK;
 }
 
@@ -1605,6 +1623,55 @@ int tw_gemm(const tw_plan* p, const void* x, int64_t m, int64_t ld_x, void* ct, 
   if (int st = check_io(p, x, m, ld_x, ct, ld_ct, out_dtype)) return st;
   return run_tw(p, x, m, ld_x, ct, ld_ct, out_dtype, nullptr, p->n_cond,
                 static_cast<cudaStream_t>(stream));
+}
+
+int tw_gemm_group(const tw_plan* const* plans, int32_t n, const void* const* xs,
+                  const int64_t* ld_xs, const int32_t* x_layouts, void* const* cts,
+                  const int64_t* ld_cts, int64_t m, int32_t out_dtype, void* stream) {
+  g_last_error.clear();
+  if (!plans || !xs || !ld_xs || !cts || !ld_cts || n < 1)
+    return fail(TW_ERR_INVALID_INPUT, "null argument");
+  if (n > kMaxGroup) return fail(TW_ERR_INVALID_INPUT, "at most %d plans per group launch", kMaxGroup);
+  const LaunchEnv env = read_launch_env();
+  GroupArgs g;
+  std::memset(&g, 0, sizeof(g));
+  WorkTable work;
+  std::memset(&work, 0, sizeof(work));
+  int grid = 0;
+  for (int i = 0; i < n; ++i) {
+    const tw_plan* p = plans[i];
+    if (int st = check_io(p, xs[i], m, ld_xs[i], cts[i], ld_cts[i], out_dtype)) return st;
+    const int32_t lay = x_layouts ? x_layouts[i] : TW_LAYOUT_NATURAL;
+    if (lay != TW_LAYOUT_NATURAL && lay != TW_LAYOUT_PLAN)
+      return fail(TW_ERR_INVALID_INPUT, "unknown activation layout %d", lay);
+    if (lay == TW_LAYOUT_PLAN && !p->runs)
+      return fail(TW_ERR_INVALID_INPUT, "plan %d has no row-run layout", i);
+    for (int j = 0; j < i; ++j)
+      if (plans[j] == p) return fail(TW_ERR_INVALID_INPUT, "a plan may appear once per group launch");
+    std::lock_guard<std::mutex> lock(p->launch_mu);
+    const TwLaunch* Lp = nullptr;
+    if (int st = get_launch(p, xs[i], m, ld_xs[i], cts[i], ld_cts[i], out_dtype, nullptr, p->n_cond,
+                            lay == TW_LAYOUT_PLAN, env, &Lp))
+      return st;
+    const TwLaunch& L = *Lp;
+    if (grid + L.grid > kMaxCtas)
+      return fail(TW_ERR_INVALID_INPUT, "group launch needs %d CTAs (> %d): set SM budgets",
+                  grid + L.grid, kMaxCtas);
+    g.map_pay[i] = launch_payload_map(p, L);
+    g.map_out[i] = L.map_out;
+    g.run_maps[i] = L.maps;
+    g.args[i] = L.a;
+    g.resident[i] = L.resident ? 1 : 0;
+    g.cta0[i] = grid;
+    if (L.a.owner)
+      for (int c = 0; c < L.grid; ++c) work.w[grid + c] = L.work.w[c];
+    grid += L.grid;
+  }
+  g.n = n;
+  g.cta0[n] = grid;
+  if (env.flags & 64) return TW_OK;
+  TW_CUDA(launch_tw_gemm_group(g, work, grid, static_cast<cudaStream_t>(stream)));
+  return TW_OK;
 }
 
 int tw_gemm_ex(const tw_plan* p, const void* x, int64_t m, int64_t ld_x, void* ct, int64_t ld_ct,

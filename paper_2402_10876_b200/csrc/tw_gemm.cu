@@ -107,12 +107,15 @@ struct Walker {
   int u;
   const SubTile* tab;
 
-  __device__ __forceinline__ void init(const GemmArgs& a, const WorkTable& work,
+  int ncta;  // CTAs of this launch (strided mode stride)
+
+  __device__ __forceinline__ void init(const GemmArgs& a, const CtaWork* work, int cta, int nctas,
                                        const SubTile* table) {
     tab = table;
     i = 0;
+    ncta = nctas;
     if (a.owner) {
-      const CtaWork& w = work.w[blockIdx.x];
+      const CtaWork& w = work[cta];
       d.kp_steps = w.kp_steps;
       d.idx_row = w.idx_row;
       d.pay_row = w.pay_row;
@@ -123,7 +126,7 @@ struct Walker {
       usz = w.usz;
       nu = usz > 0 ? (e - b + usz - 1) / usz : 0;
     } else {
-      u = blockIdx.x;
+      u = cta;
     }
   }
   __device__ __forceinline__ bool next(const GemmArgs& a, Seg& g) {
@@ -150,7 +153,7 @@ struct Walker {
     g.ub = mb * kTileN;
     g.ue = min(a.M, g.ub + kTileN);
     g.d = tab[g.sub];
-    u += gridDim.x;
+    u += ncta;
     return true;
   }
 };
@@ -280,12 +283,14 @@ __device__ __forceinline__ void epilogue_unit(const GemmArgs& args, const CUtens
                 sg.d.out_row + q * 32, sg.ub + tlo, ntok, sg.ue);
 }
 
+// The kernel body for one CTA of one layer: CTA `cta` of `ncta`, its
+// owner-mode work in work[cta].  Called by tw_gemm_kernel (one layer per
+// launch) and tw_gemm_group_kernel (several independent layers in one
+// launch); the tensor maps and args live in kernel parameter space.
 template <bool kRes>
-__global__ void __launch_bounds__(kThreads, 1)
-    tw_gemm_kernel(const __grid_constant__ CUtensorMap map_pay,
-                   const __grid_constant__ CUtensorMap map_out,
-                   const __grid_constant__ RunMaps run_maps, const __grid_constant__ GemmArgs args,
-                   const __grid_constant__ WorkTable work) {
+__device__ __forceinline__ void gemm_body(const CUtensorMap& map_pay, const CUtensorMap& map_out,
+                                          const RunMaps& run_maps, const GemmArgs& args,
+                                          const CtaWork* work, const int cta, const int ncta) {
   using C = Cfg<kRes>;
   constexpr int kStages = C::kStages;
   extern __shared__ uint8_t smem_raw[];
@@ -311,7 +316,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* mfull = jbar + 1;
   SubTile* sub_smem = reinterpret_cast<SubTile*>(bar_region + C::kBarrierBytes);
   int32_t* sIdx = reinterpret_cast<int32_t*>(bar_region + C::kBarrierBytes + C::kSubBytes);
-  long long* trace = args.trace ? args.trace + static_cast<int64_t>(blockIdx.x) * 4096 : nullptr;
+  long long* trace = args.trace ? args.trace + static_cast<int64_t>(cta) * 4096 : nullptr;
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -334,7 +339,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const bool meta_writer = args.sparse && !(args.flags & kFlagSkipMeta) && warp >= kEpilogueWarp0 &&
                            warp < kEpilogueWarp0 + 4;
   if (meta_writer) {
-    const CtaWork& w = work.w[blockIdx.x];
+    const CtaWork& w = work[cta];
     const int n = w.usz > 0 ? 2 * w.kp_steps : 0;
     const uint32_t* mp = args.meta + static_cast<int64_t>(w.pay_row / kBN) * args.meta_cols * 128 +
                          (warp & 3) * 32 + lane;
@@ -385,7 +390,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 
   Walker walk;
-  walk.init(args, work, tab);
+  walk.init(args, work, cta, ncta, tab);
   Seg sg;
 
   if (warp == kPayloadWarp) {
@@ -763,15 +768,69 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+template <bool kRes>
+__global__ void __launch_bounds__(kThreads, 1)
+    tw_gemm_kernel(const __grid_constant__ CUtensorMap map_pay,
+                   const __grid_constant__ CUtensorMap map_out,
+                   const __grid_constant__ RunMaps run_maps, const __grid_constant__ GemmArgs args,
+                   const __grid_constant__ WorkTable work) {
+  gemm_body<kRes>(map_pay, map_out, run_maps, args, work.w, blockIdx.x, gridDim.x);
+}
+
+// Several independent layers in ONE launch (TwPlanGroup): layer p owns CTAs
+// [cta0[p], cta0[p + 1]) -- its SM share -- and runs the resident or the
+// streamed body as it would alone.  One launch per step instead of a fork /
+// join over streams, so programmatic dependent launch chains consecutive
+// steps like consecutive layers.
+__global__ void __launch_bounds__(kThreads, 1)
+    tw_gemm_group_kernel(const __grid_constant__ GroupArgs g, const __grid_constant__ WorkTable work) {
+  int p = 0;
+  while (p + 1 < g.n && static_cast<int>(blockIdx.x) >= g.cta0[p + 1]) ++p;
+  const int cta = static_cast<int>(blockIdx.x) - g.cta0[p];
+  const int ncta = g.cta0[p + 1] - g.cta0[p];
+  if (g.resident[p])
+    gemm_body<true>(g.map_pay[p], g.map_out[p], g.run_maps[p], g.args[p], work.w + g.cta0[p], cta,
+                    ncta);
+  else
+    gemm_body<false>(g.map_pay[p], g.map_out[p], g.run_maps[p], g.args[p], work.w + g.cta0[p], cta,
+                     ncta);
+}
+
 }  // namespace
+
+constexpr int kGroupSmemBytes =
+    Cfg<true>::kSmemBytes > Cfg<false>::kSmemBytes ? Cfg<true>::kSmemBytes : Cfg<false>::kSmemBytes;
 
 cudaError_t configure_gemm_kernels() {
   cudaError_t e = cudaFuncSetAttribute(tw_gemm_kernel<true>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        Cfg<true>::kSmemBytes);
   if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute(tw_gemm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              Cfg<false>::kSmemBytes);
+  e = cudaFuncSetAttribute(tw_gemm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           Cfg<false>::kSmemBytes);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(tw_gemm_group_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              kGroupSmemBytes);
+}
+
+cudaError_t launch_tw_gemm_group(const GroupArgs& g, const WorkTable& work, int grid,
+                                 cudaStream_t stream) {
+  if (grid <= 0) return cudaSuccess;
+  if (g.n < 1 || g.n > kMaxGroup || grid > kMaxCtas || g.cta0[g.n] != grid)
+    return cudaErrorInvalidValue;
+  for (int p = 0; p < g.n; ++p)
+    if (g.resident[p] && !g.args[p].owner) return cudaErrorInvalidValue;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = kGroupSmemBytes;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = g.args[0].flags & kFlagNoPdl ? 0 : 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, tw_gemm_group_kernel, g, work);
 }
 
 cudaError_t launch_tw_gemm(const CUtensorMap& map_pay, const CUtensorMap& map_out,

@@ -165,9 +165,58 @@ class TwPlanGroup:
             cur.wait_event(e)
         return outs
 
-    def run(self, xs, outs=None, out_dtype: str = "fp32"):
-        """TW products of every plan (``xs[i]`` in plan i's row layout)."""
-        return self._launch("run", xs, outs, out_dtype)
+    def run(self, xs, outs=None, out_dtype: str = "fp32", fused: Optional[bool] = None):
+        """TW products of every plan (``xs[i]`` in plan i's row layout).
+
+        ``fused`` (default: up to 4 plans) runs all of them in ONE K1 launch
+        on the caller's stream (``tw_gemm_group``: plan i's CTAs on its SM
+        share), so consecutive steps chain through programmatic dependent
+        launch; otherwise one launch per plan on concurrent streams.  Both
+        give the sequential launches' results bit for bit."""
+        if fused is None:
+            fused = len(self.plans) <= 4
+        if not fused:
+            return self._launch("run", xs, outs, out_dtype)
+        return self._run_fused(xs, outs, out_dtype)
+
+    def _run_fused(self, xs, outs, out_dtype):
+        import ctypes
+
+        from . import _native
+        from .executor import _DTYPE_CODES, _dtype_name
+
+        n = len(self.plans)
+        if len(xs) != n:
+            raise InvalidInputError(f"expected {n} inputs, got {len(xs)}")
+        outs = list(outs) if outs is not None else [None] * n
+        m = None
+        layouts, lds = [], []
+        for i, (p, x) in enumerate(zip(self.plans, xs)):
+            use_plan = p.uses_row_runs
+            rows = p.layout_rows if (use_plan or p.split) else None
+            mi, ld = p._check_x(x, rows)
+            if m is None:
+                m = mi
+            elif mi != m:
+                raise InvalidInputError("a fused group launch needs the same M for every plan")
+            outs[i] = p._out(p.info.n_condensed, m, outs[i], out_dtype)
+            layouts.append(_native.TW_LAYOUT_PLAN if use_plan else _native.TW_LAYOUT_NATURAL)
+            lds.append(ld)
+        codes = {_DTYPE_CODES[_dtype_name(o.dtype)] for o in outs}
+        if len(codes) != 1:
+            raise InvalidInputError("a fused group launch needs one output dtype")
+        vp = ctypes.c_void_p
+        handles = (vp * n)(*[p._handle.value if isinstance(p._handle, vp) else p._handle
+                             for p in self.plans])
+        xp = (vp * n)(*[x.data_ptr() for x in xs])
+        cp = (vp * n)(*[o.data_ptr() for o in outs])
+        ldx = (ctypes.c_int64 * n)(*lds)
+        ldc = (ctypes.c_int64 * n)(*[o.stride(0) for o in outs])
+        lay = (ctypes.c_int32 * n)(*layouts)
+        lib = _native.load_library()
+        _native.check(lib.tw_gemm_group(handles, n, xp, ldx, lay, cp, ldc, m, codes.pop(),
+                                        _native.stream_handle()))
+        return outs
 
     def run_tew(self, xs, outs=None, out_dtype: str = "fp32"):
         """TEW products of every plan (each must carry an overlay)."""
