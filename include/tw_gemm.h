@@ -188,6 +188,17 @@ TW_API int tw_gemm_group(const tw_plan* const* plans, int32_t n, const void* con
                          const int64_t* ld_xs, const int32_t* x_layouts, void* const* cts,
                          const int64_t* ld_cts, int64_t m, int32_t out_dtype, void* stream);
 
+/* TEW for several independent plans (each with an overlay): K1 of all of
+   them in one launch (into workspaces[i] when tw_plan_tew_workspace_bytes
+   asks for one, else straight into the union rows), then every plan's K2 on
+   the same stream.  Bit-identical to n tw_gemm_tew_ex calls with the same
+   workspaces. */
+TW_API int tw_gemm_tew_group(const tw_plan* const* plans, int32_t n, const void* const* xs,
+                             const int64_t* ld_xs, const int32_t* x_layouts, void* const* cts,
+                             const int64_t* ld_cts, void* const* workspaces,
+                             const uint64_t* ws_bytes, int64_t m, int32_t out_dtype,
+                             void* stream);
+
 /* tw_gemm with the activation row layout given: TW_LAYOUT_NATURAL (A^T rows
  * in K order, kept rows gathered with cp.async) or TW_LAYOUT_PLAN (A^T as
  * tw_plan_prepare writes it; on plans with row_runs, every stage is a few

@@ -59,6 +59,9 @@ SIGNATURES = {
     "tw_gemm_ex": (_c_int, [_vp, _vp, _i64, _i64, _vp, _i64, _i32, _i32, _vp]),
     "tw_gemm_group": (_c_int, [ctypes.POINTER(_vp), _i32, ctypes.POINTER(_vp), _i64p, _i32p,
                                ctypes.POINTER(_vp), _i64p, _i64, _i32, _vp]),
+    "tw_gemm_tew_group": (_c_int, [ctypes.POINTER(_vp), _i32, ctypes.POINTER(_vp), _i64p, _i32p,
+                                   ctypes.POINTER(_vp), _i64p, ctypes.POINTER(_vp),
+                                   ctypes.POINTER(ctypes.c_uint64), _i64, _i32, _vp]),
     "tw_plan_prepare": (_c_int, [_vp, _vp, _i32, _i64, _i64, _vp, _i64, _vp]),
     "tw_plan_row_order": (_c_int, [_vp, _i32p]),
     "tw_plan_permute_rows": (_c_int, [_vp, _vp, _i64, _i64, _vp, _i64, _vp]),

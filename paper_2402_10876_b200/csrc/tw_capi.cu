@@ -1625,11 +1625,14 @@ int tw_gemm(const tw_plan* p, const void* x, int64_t m, int64_t ld_x, void* ct, 
                 static_cast<cudaStream_t>(stream));
 }
 
-int tw_gemm_group(const tw_plan* const* plans, int32_t n, const void* const* xs,
-                  const int64_t* ld_xs, const int32_t* x_layouts, void* const* cts,
-                  const int64_t* ld_cts, int64_t m, int32_t out_dtype, void* stream) {
-  g_last_error.clear();
-  if (!plans || !xs || !ld_xs || !cts || !ld_cts || n < 1)
+// K1 of n independent plans in one launch; outs[i] (ld_outs[i]) receive plan
+// i's condensed C'^T, or with tew_scatter its union rows (the overlay's
+// rowmap), exactly as run_tw would write them.
+static int group_k1(const tw_plan* const* plans, int32_t n, const void* const* xs,
+                    const int64_t* ld_xs, const int32_t* x_layouts, void* const* outs,
+                    const int64_t* ld_outs, const bool* tew_scatter, int64_t m, int32_t out_dtype,
+                    cudaStream_t stream) {
+  if (!plans || !xs || !ld_xs || !outs || !ld_outs || n < 1)
     return fail(TW_ERR_INVALID_INPUT, "null argument");
   if (n > kMaxGroup) return fail(TW_ERR_INVALID_INPUT, "at most %d plans per group launch", kMaxGroup);
   const LaunchEnv env = read_launch_env();
@@ -1640,7 +1643,7 @@ int tw_gemm_group(const tw_plan* const* plans, int32_t n, const void* const* xs,
   int grid = 0;
   for (int i = 0; i < n; ++i) {
     const tw_plan* p = plans[i];
-    if (int st = check_io(p, xs[i], m, ld_xs[i], cts[i], ld_cts[i], out_dtype)) return st;
+    if (int st = check_io(p, xs[i], m, ld_xs[i], outs[i], ld_outs[i], out_dtype)) return st;
     const int32_t lay = x_layouts ? x_layouts[i] : TW_LAYOUT_NATURAL;
     if (lay != TW_LAYOUT_NATURAL && lay != TW_LAYOUT_PLAN)
       return fail(TW_ERR_INVALID_INPUT, "unknown activation layout %d", lay);
@@ -1648,9 +1651,12 @@ int tw_gemm_group(const tw_plan* const* plans, int32_t n, const void* const* xs,
       return fail(TW_ERR_INVALID_INPUT, "plan %d has no row-run layout", i);
     for (int j = 0; j < i; ++j)
       if (plans[j] == p) return fail(TW_ERR_INVALID_INPUT, "a plan may appear once per group launch");
+    const bool scatter = tew_scatter && tew_scatter[i];
     std::lock_guard<std::mutex> lock(p->launch_mu);
     const TwLaunch* Lp = nullptr;
-    if (int st = get_launch(p, xs[i], m, ld_xs[i], cts[i], ld_cts[i], out_dtype, nullptr, p->n_cond,
+    if (int st = get_launch(p, xs[i], m, ld_xs[i], outs[i], ld_outs[i], out_dtype,
+                            scatter ? p->ov.union_rowmap : nullptr,
+                            scatter ? (int64_t)p->union_cols.size() : p->n_cond,
                             lay == TW_LAYOUT_PLAN, env, &Lp))
       return st;
     const TwLaunch& L = *Lp;
@@ -1670,7 +1676,66 @@ int tw_gemm_group(const tw_plan* const* plans, int32_t n, const void* const* xs,
   g.n = n;
   g.cta0[n] = grid;
   if (env.flags & 64) return TW_OK;
-  TW_CUDA(launch_tw_gemm_group(g, work, grid, static_cast<cudaStream_t>(stream)));
+  TW_CUDA(launch_tw_gemm_group(g, work, grid, stream));
+  return TW_OK;
+}
+
+int tw_gemm_group(const tw_plan* const* plans, int32_t n, const void* const* xs,
+                  const int64_t* ld_xs, const int32_t* x_layouts, void* const* cts,
+                  const int64_t* ld_cts, int64_t m, int32_t out_dtype, void* stream) {
+  g_last_error.clear();
+  return group_k1(plans, n, xs, ld_xs, x_layouts, cts, ld_cts, nullptr, m, out_dtype,
+                  static_cast<cudaStream_t>(stream));
+}
+
+static int launch_k2(const tw_plan* p, const void* x, int64_t m, int64_t ld_x, void* ct,
+                     int64_t ld_ct, int32_t out_dtype, const void* src, int64_t ld_src,
+                     int32_t n_cols, const int4* meta, bool acc_all, cudaStream_t s,
+                     bool plan_layout);
+
+int tw_gemm_tew_group(const tw_plan* const* plans, int32_t n, const void* const* xs,
+                      const int64_t* ld_xs, const int32_t* x_layouts, void* const* cts,
+                      const int64_t* ld_cts, void* const* workspaces, const uint64_t* ws_bytes,
+                      int64_t m, int32_t out_dtype, void* stream) {
+  g_last_error.clear();
+  if (!plans || !cts || !ld_cts || n < 1 || n > kMaxGroup)
+    return fail(TW_ERR_INVALID_INPUT, "bad group arguments");
+  // K1 of every plan in one launch -- into its workspace (condensed, TMA
+  // epilogue) when it needs one, else straight into its union rows -- then
+  // K2 of every plan, one after another on the same stream (each K2 takes
+  // the whole GPU; programmatic dependent launch chains them)
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  std::vector<void*> k1_out(n);
+  std::vector<int64_t> k1_ld(n);
+  std::vector<uint8_t> scatter(n);
+  for (int i = 0; i < n; ++i) {
+    const tw_plan* p = plans[i];
+    if (!p || !p->has_overlay) return fail(TW_ERR_INVALID_INPUT, "plan %d has no overlay", i);
+    uint64_t need = 0;
+    if (int st = tw_plan_tew_workspace_bytes(p, m, out_dtype, &need)) return st;
+    void* ws = need && workspaces ? workspaces[i] : nullptr;
+    if (need && (!ws || !ws_bytes || ws_bytes[i] < need || reinterpret_cast<uintptr_t>(ws) % 16))
+      return fail(TW_ERR_INVALID_INPUT, "plan %d: workspace must hold %llu bytes, 16-byte aligned",
+                  i, (unsigned long long)need);
+    k1_out[i] = ws ? ws : cts[i];
+    k1_ld[i] = ws ? (m + 7) / 8 * 8 : ld_cts[i];
+    scatter[i] = ws ? 0 : 1;
+  }
+  bool scb[kMaxGroup];
+  for (int i = 0; i < n; ++i) scb[i] = scatter[i] != 0;
+  if (int st = group_k1(plans, n, xs, ld_xs, x_layouts, k1_out.data(), k1_ld.data(), scb, m,
+                        out_dtype, s))
+    return st;
+  for (int i = 0; i < n; ++i) {
+    const tw_plan* p = plans[i];
+    if (int st = check_io(p, xs[i], m, ld_xs[i], cts[i], ld_cts[i], out_dtype)) return st;
+    const bool plan_layout = x_layouts && x_layouts[i] == TW_LAYOUT_PLAN;
+    const bool ws = !scatter[i];
+    if (int st = launch_k2(p, xs[i], m, ld_xs[i], cts[i], ld_cts[i], out_dtype,
+                           ws ? k1_out[i] : nullptr, ws ? k1_ld[i] : 0,
+                           ws ? p->n_ov_cols_all : p->n_ov_cols, nullptr, false, s, plan_layout))
+      return st;
+  }
   return TW_OK;
 }
 

@@ -179,7 +179,7 @@ class TwPlanGroup:
             return self._launch("run", xs, outs, out_dtype)
         return self._run_fused(xs, outs, out_dtype)
 
-    def _run_fused(self, xs, outs, out_dtype):
+    def _run_fused(self, xs, outs, out_dtype, tew: bool = False):
         import ctypes
 
         from . import _native
@@ -199,7 +199,10 @@ class TwPlanGroup:
                 m = mi
             elif mi != m:
                 raise InvalidInputError("a fused group launch needs the same M for every plan")
-            outs[i] = p._out(p.info.n_condensed, m, outs[i], out_dtype)
+            rows_out = p.info.n_union if tew else p.info.n_condensed
+            if tew and not p.has_overlay:
+                raise InvalidInputError(f"plan {i} has no overlay attached")
+            outs[i] = p._out(rows_out, m, outs[i], out_dtype)
             layouts.append(_native.TW_LAYOUT_PLAN if use_plan else _native.TW_LAYOUT_NATURAL)
             lds.append(ld)
         codes = {_DTYPE_CODES[_dtype_name(o.dtype)] for o in outs}
@@ -214,13 +217,38 @@ class TwPlanGroup:
         ldc = (ctypes.c_int64 * n)(*[o.stride(0) for o in outs])
         lay = (ctypes.c_int32 * n)(*layouts)
         lib = _native.load_library()
-        _native.check(lib.tw_gemm_group(handles, n, xp, ldx, lay, cp, ldc, m, codes.pop(),
-                                        _native.stream_handle()))
+        code = codes.pop()
+        if not tew:
+            _native.check(lib.tw_gemm_group(handles, n, xp, ldx, lay, cp, ldc, m, code,
+                                            _native.stream_handle()))
+            return outs
+        # per-plan K1 workspaces (stream-ordered caching allocator, as run_tew)
+        from .executor import _torch
+
+        torch = _torch()
+        wss, sizes = [], []
+        for p, o in zip(self.plans, outs):
+            need = ctypes.c_uint64()
+            _native.check(lib.tw_plan_tew_workspace_bytes(p._handle, m, code, ctypes.byref(need)))
+            ws = torch.empty(int(need.value), dtype=torch.uint8, device=o.device) if need.value else None
+            wss.append(ws)
+            sizes.append(int(need.value))
+        wp = (vp * n)(*[w.data_ptr() if w is not None else None for w in wss])
+        wb = (ctypes.c_uint64 * n)(*sizes)
+        _native.check(lib.tw_gemm_tew_group(handles, n, xp, ldx, lay, cp, ldc, wp, wb, m, code,
+                                            _native.stream_handle()))
         return outs
 
-    def run_tew(self, xs, outs=None, out_dtype: str = "fp32"):
-        """TEW products of every plan (each must carry an overlay)."""
-        return self._launch("run_tew", xs, outs, out_dtype)
+    def run_tew(self, xs, outs=None, out_dtype: str = "fp32", fused: Optional[bool] = None):
+        """TEW products of every plan (each must carry an overlay).  ``fused``
+        (default: up to 4 plans): K1 of every plan in one launch, then each
+        plan's K2 (``tw_gemm_tew_group``); else K1 + K2 per plan on
+        concurrent streams."""
+        if fused is None:
+            fused = len(self.plans) <= 4
+        if not fused:
+            return self._launch("run_tew", xs, outs, out_dtype)
+        return self._run_fused(xs, outs, out_dtype, tew=True)
 
     def set_budgets(self, budgets: Sequence[int]) -> None:
         """New SM shares (one per plan, each >= its sub-tile count, summing

@@ -289,17 +289,17 @@ def test_plan_group_equals_sequential(tew):
     torch.cuda.synchronize()
     for o, r in zip(outs, ref):
         assert torch.equal(o, r)
-    if not tew:
-        # one launch for all layers (tw_gemm_group) and one launch per layer on
-        # concurrent streams both equal the lone launches bit for bit, also on
-        # tight shares (one SM per sub-tile)
-        for fused in (True, False):
-            outs = g.run(xs, out_dtype="fp16", fused=fused)
-            torch.cuda.synchronize()
-            assert all(torch.equal(o, r) for o, r in zip(outs, ref)), fused
-        g.set_budgets([int(p.info.n_sub) for p in plans])
-        outs = g.run(xs, out_dtype="fp16", fused=True)
+    # one launch for all layers' K1 (tw_gemm_group / tw_gemm_tew_group) and
+    # one launch per layer on concurrent streams both equal the lone launches
+    # bit for bit, also on tight shares (one SM per sub-tile)
+    run = g.run_tew if tew else g.run
+    for fused in (True, False):
+        outs = run(xs, out_dtype="fp16", fused=fused)
         torch.cuda.synchronize()
-        assert all(torch.equal(o, r) for o, r in zip(outs, ref))
+        assert all(torch.equal(o, r) for o, r in zip(outs, ref)), fused
+    g.set_budgets([int(p.info.n_sub) for p in plans])
+    outs = run(xs, out_dtype="fp16", fused=True)
+    torch.cuda.synchronize()
+    assert all(torch.equal(o, r) for o, r in zip(outs, ref))
     g.release()
     assert all(int(p.info.sm_budget) == int(p.info.sm_count) for p in plans)
