@@ -290,7 +290,8 @@ __device__ __forceinline__ void epilogue_unit(const GemmArgs& args, const CUtens
 template <bool kRes>
 __device__ __forceinline__ void gemm_body(const CUtensorMap& map_pay, const CUtensorMap& map_out,
                                           const RunMaps& run_maps, const GemmArgs& args,
-                                          const CtaWork* work, const int cta, const int ncta) {
+                                          const CtaWork* work, const int cta, const int ncta,
+                                          const int tslot) {
   using C = Cfg<kRes>;
   constexpr int kStages = C::kStages;
   extern __shared__ uint8_t smem_raw[];
@@ -316,7 +317,7 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& map_pay, const CUte
   uint64_t* mfull = jbar + 1;
   SubTile* sub_smem = reinterpret_cast<SubTile*>(bar_region + C::kBarrierBytes);
   int32_t* sIdx = reinterpret_cast<int32_t*>(bar_region + C::kBarrierBytes + C::kSubBytes);
-  long long* trace = args.trace ? args.trace + static_cast<int64_t>(cta) * 4096 : nullptr;
+  long long* trace = args.trace ? args.trace + static_cast<int64_t>(tslot) * 4096 : nullptr;
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -774,7 +775,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                    const __grid_constant__ CUtensorMap map_out,
                    const __grid_constant__ RunMaps run_maps, const __grid_constant__ GemmArgs args,
                    const __grid_constant__ WorkTable work) {
-  gemm_body<kRes>(map_pay, map_out, run_maps, args, work.w, blockIdx.x, gridDim.x);
+  gemm_body<kRes>(map_pay, map_out, run_maps, args, work.w, blockIdx.x, gridDim.x, blockIdx.x);
 }
 
 // Several independent layers in ONE launch (TwPlanGroup): layer p owns CTAs
@@ -790,10 +791,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int ncta = g.cta0[p + 1] - g.cta0[p];
   if (g.resident[p])
     gemm_body<true>(g.map_pay[p], g.map_out[p], g.run_maps[p], g.args[p], work.w + g.cta0[p], cta,
-                    ncta);
+                    ncta, blockIdx.x);
   else
     gemm_body<false>(g.map_pay[p], g.map_out[p], g.run_maps[p], g.args[p], work.w + g.cta0[p], cta,
-                     ncta);
+                     ncta, blockIdx.x);
 }
 
 }  // namespace
