@@ -15,6 +15,6 @@ echo "ref rc=$?"; tail -c 300 gpurun_out/r2_bench_reference_arm.json; echo
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
     --log-file gpurun_out/r2_launches.csv python bench.py --steps 4 --warmup 3 > /dev/null 2>&1
 echo "ncu launches rc=$?"
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:tw_gemm_kernel \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:tw_gemm_group_kernel \
     -s 12 -c 3 -o gpurun_out/r2_prof_k1 -f python bench.py --steps 4 --warmup 3 > gpurun_out/r2_ncu_full.log 2>&1
 echo "ncu full rc=$?"; tail -2 gpurun_out/r2_ncu_full.log
