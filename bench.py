@@ -598,6 +598,7 @@ def run_ours(args, cfg, rank: int, world: int) -> None:
     # captured before the SM shares are set (launch geometry is baked into
     # the graph): the sequential step uses the whole GPU for every launch
     seq_cycle = capture_graph(lambda: [seq_set(r) for r in range(N_ROTATE)])
+    seq_graphs = [capture_graph(lambda r=r: seq_set(r)) for r in range(N_ROTATE)]
     groups = [tw.TwPlanGroup([p for p, _, _ in sets[r]], m) for r in range(N_ROTATE)]
     groups_fused = len(groups[0].plans) <= 4   # TwPlanGroup.run's default: one launch
 
@@ -641,8 +642,6 @@ def run_ours(args, cfg, rank: int, world: int) -> None:
     # faster one runs the timed region (the library's SM-share cost model was
     # fitted on the TW layers; TVW's longer K' and the one-layer configs[0]
     # run faster sequentially).  Both times are reported.
-    seq_graphs = [capture_graph(lambda r=r: seq_set(r)) for r in range(N_ROTATE)]
-
     def cycle_ms(g, n=6):
         for _ in range(2):
             g.replay()
