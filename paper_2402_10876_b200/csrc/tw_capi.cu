@@ -1641,6 +1641,13 @@ static int group_k1(const tw_plan* const* plans, int32_t n, const void* const* x
   WorkTable work;
   std::memset(&work, 0, sizeof(work));
   int grid = 0;
+  // (plan, local CTA, estimated work): CTAs are launched heaviest first, so
+  // under programmatic dependent launch -- where a step's CTAs take SMs in
+  // launch order as the previous step's free them -- the longest ones start
+  // earliest
+  struct CtaRef { int p, c; double w; };
+  std::vector<CtaRef> ctas;
+  std::vector<const TwLaunch*> launches(n);
   for (int i = 0; i < n; ++i) {
     const tw_plan* p = plans[i];
     if (int st = check_io(p, xs[i], m, ld_xs[i], outs[i], ld_outs[i], out_dtype)) return st;
@@ -1660,21 +1667,37 @@ static int group_k1(const tw_plan* const* plans, int32_t n, const void* const* x
                             lay == TW_LAYOUT_PLAN, env, &Lp))
       return st;
     const TwLaunch& L = *Lp;
-    if (grid + L.grid > kMaxCtas)
+    if (grid + L.grid > kMaxCtas || L.grid > 255)
       return fail(TW_ERR_INVALID_INPUT, "group launch needs %d CTAs (> %d): set SM budgets",
                   grid + L.grid, kMaxCtas);
+    launches[i] = Lp;
     g.map_pay[i] = launch_payload_map(p, L);
     g.map_out[i] = L.map_out;
     g.run_maps[i] = L.maps;
     g.args[i] = L.a;
     g.resident[i] = L.resident ? 1 : 0;
-    g.cta0[i] = grid;
-    if (L.a.owner)
-      for (int c = 0; c < L.grid; ++c) work.w[grid + c] = L.work.w[c];
+    g.plan_ctas[i] = L.grid;
+    for (int c = 0; c < L.grid; ++c) {
+      double w = 0.0;
+      if (L.a.owner) {
+        const CtaWork& cw = L.work.w[c];
+        const int units = cw.usz > 0 ? (cw.e - cw.b + cw.usz - 1) / cw.usz : 0;
+        w = (double)(cw.e - cw.b) * cw.kp_steps + 3000.0 / 4.0 * units;  // group.py cost model
+      }
+      ctas.push_back({i, c, w});
+    }
     grid += L.grid;
   }
+  if (!env_int("TW_GROUP_PLAN_ORDER", 0))
+    std::stable_sort(ctas.begin(), ctas.end(),
+                     [](const CtaRef& a, const CtaRef& b) { return a.w > b.w; });
+  for (int b = 0; b < grid; ++b) {
+    const CtaRef& r = ctas[b];
+    g.cta_plan[b] = (int8_t)r.p;
+    g.cta_local[b] = (uint8_t)r.c;
+    if (launches[r.p]->a.owner) work.w[b] = launches[r.p]->work.w[r.c];
+  }
   g.n = n;
-  g.cta0[n] = grid;
   if (env.flags & 64) return TW_OK;
   TW_CUDA(launch_tw_gemm_group(g, work, grid, stream));
   return TW_OK;

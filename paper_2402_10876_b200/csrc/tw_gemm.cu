@@ -109,13 +109,13 @@ struct Walker {
 
   int ncta;  // CTAs of this launch (strided mode stride)
 
-  __device__ __forceinline__ void init(const GemmArgs& a, const CtaWork* work, int cta, int nctas,
+  __device__ __forceinline__ void init(const GemmArgs& a, const CtaWork* mine, int cta, int nctas,
                                        const SubTile* table) {
     tab = table;
     i = 0;
     ncta = nctas;
     if (a.owner) {
-      const CtaWork& w = work[cta];
+      const CtaWork& w = *mine;
       d.kp_steps = w.kp_steps;
       d.idx_row = w.idx_row;
       d.pay_row = w.pay_row;
@@ -284,7 +284,7 @@ __device__ __forceinline__ void epilogue_unit(const GemmArgs& args, const CUtens
 }
 
 // The kernel body for one CTA of one layer: CTA `cta` of `ncta`, its
-// owner-mode work in work[cta].  Called by tw_gemm_kernel (one layer per
+// owner-mode work entry at `work` (this CTA's own).  Called by tw_gemm_kernel (one layer per
 // launch) and tw_gemm_group_kernel (several independent layers in one
 // launch); the tensor maps and args live in kernel parameter space.
 template <bool kRes>
@@ -340,7 +340,7 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& map_pay, const CUte
   const bool meta_writer = args.sparse && !(args.flags & kFlagSkipMeta) && warp >= kEpilogueWarp0 &&
                            warp < kEpilogueWarp0 + 4;
   if (meta_writer) {
-    const CtaWork& w = work[cta];
+    const CtaWork& w = *work;
     const int n = w.usz > 0 ? 2 * w.kp_steps : 0;
     const uint32_t* mp = args.meta + static_cast<int64_t>(w.pay_row / kBN) * args.meta_cols * 128 +
                          (warp & 3) * 32 + lane;
@@ -775,7 +775,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                    const __grid_constant__ CUtensorMap map_out,
                    const __grid_constant__ RunMaps run_maps, const __grid_constant__ GemmArgs args,
                    const __grid_constant__ WorkTable work) {
-  gemm_body<kRes>(map_pay, map_out, run_maps, args, work.w, blockIdx.x, gridDim.x, blockIdx.x);
+  gemm_body<kRes>(map_pay, map_out, run_maps, args, work.w + blockIdx.x, blockIdx.x, gridDim.x,
+                  blockIdx.x);
 }
 
 // Several independent layers in ONE launch (TwPlanGroup): layer p owns CTAs
@@ -785,16 +786,16 @@ __global__ void __launch_bounds__(kThreads, 1)
 // steps like consecutive layers.
 __global__ void __launch_bounds__(kThreads, 1)
     tw_gemm_group_kernel(const __grid_constant__ GroupArgs g, const __grid_constant__ WorkTable work) {
-  int p = 0;
-  while (p + 1 < g.n && static_cast<int>(blockIdx.x) >= g.cta0[p + 1]) ++p;
-  const int cta = static_cast<int>(blockIdx.x) - g.cta0[p];
-  const int ncta = g.cta0[p + 1] - g.cta0[p];
+  // CTA b runs CTA cta_local[b] of plan cta_plan[b]; its owner work entry is
+  // work.w[b] (the host orders the CTAs heaviest first across plans)
+  const int b = static_cast<int>(blockIdx.x);
+  const int p = g.cta_plan[b];
+  const int cta = g.cta_local[b];
+  const int ncta = g.plan_ctas[p];
   if (g.resident[p])
-    gemm_body<true>(g.map_pay[p], g.map_out[p], g.run_maps[p], g.args[p], work.w + g.cta0[p], cta,
-                    ncta, blockIdx.x);
+    gemm_body<true>(g.map_pay[p], g.map_out[p], g.run_maps[p], g.args[p], work.w + b, cta, ncta, b);
   else
-    gemm_body<false>(g.map_pay[p], g.map_out[p], g.run_maps[p], g.args[p], work.w + g.cta0[p], cta,
-                     ncta, blockIdx.x);
+    gemm_body<false>(g.map_pay[p], g.map_out[p], g.run_maps[p], g.args[p], work.w + b, cta, ncta, b);
 }
 
 }  // namespace
@@ -817,8 +818,7 @@ cudaError_t configure_gemm_kernels() {
 cudaError_t launch_tw_gemm_group(const GroupArgs& g, const WorkTable& work, int grid,
                                  cudaStream_t stream) {
   if (grid <= 0) return cudaSuccess;
-  if (g.n < 1 || g.n > kMaxGroup || grid > kMaxCtas || g.cta0[g.n] != grid)
-    return cudaErrorInvalidValue;
+  if (g.n < 1 || g.n > kMaxGroup || grid > kMaxCtas) return cudaErrorInvalidValue;
   for (int p = 0; p < g.n; ++p)
     if (g.resident[p] && !g.args[p].owner) return cudaErrorInvalidValue;
   cudaLaunchConfig_t cfg{};

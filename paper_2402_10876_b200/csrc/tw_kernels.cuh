@@ -109,18 +109,20 @@ cudaError_t launch_tw_gemm(const CUtensorMap& map_pay, const CUtensorMap& map_ou
 // device before launching or capturing).
 cudaError_t configure_gemm_kernels();
 
-// K1 for several independent layers in one launch (TwPlanGroup): layer p
-// owns CTAs [cta0[p], cta0[p + 1]) and its owner-mode work entries at the
-// same positions of the shared work table.
+// K1 for several independent layers in one launch (TwPlanGroup): CTA b
+// runs CTA cta_local[b] of layer cta_plan[b] (plan_ctas[p] CTAs in all), its
+// owner-mode work entry at position b of the shared work table.
 constexpr int kMaxGroup = 4;
 struct GroupArgs {
   CUtensorMap map_pay[kMaxGroup];
   CUtensorMap map_out[kMaxGroup];
   RunMaps run_maps[kMaxGroup];
   GemmArgs args[kMaxGroup];
-  int32_t cta0[kMaxGroup + 1];
+  int32_t plan_ctas[kMaxGroup];
   int32_t resident[kMaxGroup];
   int32_t n;
+  int8_t cta_plan[kMaxCtas];
+  uint8_t cta_local[kMaxCtas];
 };
 cudaError_t launch_tw_gemm_group(const GroupArgs& g, const WorkTable& work, int grid,
                                  cudaStream_t stream);
