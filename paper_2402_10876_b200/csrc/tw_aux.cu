@@ -136,9 +136,10 @@ __device__ __forceinline__ void residual_store4(const ResidualArgs& args, int64_
   }
 }
 
+// One CTA of K2: token block bx, column split by.
 template <int T, bool kBf>
-__global__ void __launch_bounds__(kResThreads, 1)
-    tw_residual_kernel(const __grid_constant__ ResidualArgs args) {
+__device__ __forceinline__ void residual_body(const ResidualArgs& args, const int bx,
+                                              const int by) {
   extern __shared__ __align__(16) uint8_t res_smem[];
   uint16_t* sA = reinterpret_cast<uint16_t*>(res_smem);  // [K][T]
   constexpr int L = T / 8;        // lanes per column (8 tokens each)
@@ -149,11 +150,11 @@ __global__ void __launch_bounds__(kResThreads, 1)
   const int sub = lane / L;
   const int tl = lane - sub * L;
   const int tok = tl * 8;
-  const int64_t t0 = static_cast<int64_t>(blockIdx.x) * T;
+  const int64_t t0 = static_cast<int64_t>(bx) * T;
   const int64_t rem = args.M - t0;
   const int ntok = rem < T ? static_cast<int>(rem) : T;
   // this CTA's columns: split y of the descending-nnz order (by nnz)
-  const int c0 = args.group_first[blockIdx.y], c1 = args.group_first[blockIdx.y + 1];
+  const int c0 = args.group_first[by], c1 = args.group_first[by + 1];
   // launched with programmatic dependent launch after K1: the TW result (and,
   // in a chain, A^T) is complete and visible only after this wait
   grid_dependency_wait();
@@ -278,6 +279,30 @@ __global__ void __launch_bounds__(kResThreads, 1)
       }
     }
     m = mn;
+  }
+}
+
+template <int T, bool kBf>
+__global__ void __launch_bounds__(kResThreads, 1)
+    tw_residual_kernel(const __grid_constant__ ResidualArgs args) {
+  residual_body<T, kBf>(args, blockIdx.x, blockIdx.y);
+}
+
+// K2 of several layers in one launch (the TEW grouped step): layer p owns
+// CTAs [cta0[p], cta0[p + 1]), n_blocks x n_groups of them; its token block
+// size picks the body (64 for K <= 1536, 32 up to K = 3072).
+template <bool kBf>
+__global__ void __launch_bounds__(kResThreads, 1)
+    tw_residual_group_kernel(const __grid_constant__ ResidualGroupArgs g) {
+  int p = 0;
+  while (p + 1 < g.n && static_cast<int>(blockIdx.x) >= g.cta0[p + 1]) ++p;
+  const ResidualArgs& a = g.args[p];
+  const int local = static_cast<int>(blockIdx.x) - g.cta0[p];
+  const int bx = local % a.n_blocks, by = local / a.n_blocks;
+  switch (a.block_tokens) {
+    case 64: residual_body<64, kBf>(a, bx, by); break;
+    case 32: residual_body<32, kBf>(a, bx, by); break;
+    default: residual_body<16, kBf>(a, bx, by); break;
   }
 }
 
@@ -486,6 +511,44 @@ template <int T>
 static cudaError_t launch_res(const ResidualArgs& args, cudaStream_t stream) {
   return args.in_dtype == kBF16 ? launch_res_t<T, true>(args, stream)
                                 : launch_res_t<T, false>(args, stream);
+}
+
+cudaError_t launch_tw_residual_group(const ResidualGroupArgs& g, cudaStream_t stream) {
+  if (g.n < 1 || g.n > kMaxResGroup) return cudaErrorInvalidValue;
+  size_t smem = 0;
+  bool bf = false;
+  for (int p = 0; p < g.n; ++p) {
+    const ResidualArgs& a = g.args[p];
+    if (!a.rv || a.block_tokens <= 0) return cudaErrorInvalidValue;  // staged kernels only
+    smem = std::max(smem, static_cast<size_t>(a.K + 1) * a.block_tokens * 2);
+    bf = a.in_dtype == kBF16;
+    if ((a.in_dtype == kBF16) != (g.args[0].in_dtype == kBF16)) return cudaErrorInvalidValue;
+  }
+  const int grid = g.cta0[g.n];
+  if (grid <= 0) return cudaSuccess;
+  static uint64_t configured = 0;  // bit per device ordinal (both dtypes)
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev >= 64 || !(configured >> dev & 1u)) {
+    for (auto* k : {tw_residual_group_kernel<false>, tw_residual_group_kernel<true>}) {
+      e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024 + 128);
+      if (e != cudaSuccess) return e;
+    }
+    if (dev < 64) configured |= uint64_t{1} << dev;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(grid));
+  cfg.blockDim = dim3(kResThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return bf ? cudaLaunchKernelEx(&cfg, tw_residual_group_kernel<true>, g)
+            : cudaLaunchKernelEx(&cfg, tw_residual_group_kernel<false>, g);
 }
 
 cudaError_t launch_tw_residual(const ResidualArgs& args, cudaStream_t stream) {

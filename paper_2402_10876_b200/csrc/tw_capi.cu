@@ -1715,6 +1715,10 @@ static int launch_k2(const tw_plan* p, const void* x, int64_t m, int64_t ld_x, v
                      int64_t ld_ct, int32_t out_dtype, const void* src, int64_t ld_src,
                      int32_t n_cols, const int4* meta, bool acc_all, cudaStream_t s,
                      bool plan_layout);
+static void build_k2_args(const tw_plan* p, const void* x, int64_t m, int64_t ld_x, void* ct,
+                          int64_t ld_ct, int32_t out_dtype, const void* src, int64_t ld_src,
+                          int32_t n_cols, const int4* meta, bool acc_all, bool plan_layout,
+                          ResidualArgs& r);
 
 int tw_gemm_tew_group(const tw_plan* const* plans, int32_t n, const void* const* xs,
                       const int64_t* ld_xs, const int32_t* x_layouts, void* const* cts,
@@ -1749,16 +1753,32 @@ int tw_gemm_tew_group(const tw_plan* const* plans, int32_t n, const void* const*
   if (int st = group_k1(plans, n, xs, ld_xs, x_layouts, k1_out.data(), k1_ld.data(), scb, m,
                         out_dtype, s))
     return st;
+  // K2 of every plan: one launch over all of them when every plan has the
+  // staged kernel (CTAs of all layers fill the waves together), else one
+  // launch per plan
+  ResidualGroupArgs rg;
+  std::memset(&rg, 0, sizeof(rg));
+  bool grouped = n <= kMaxResGroup && !env_int("TW_K2_PER_LAYER", 0);
   for (int i = 0; i < n; ++i) {
     const tw_plan* p = plans[i];
     if (int st = check_io(p, xs[i], m, ld_xs[i], cts[i], ld_cts[i], out_dtype)) return st;
     const bool plan_layout = x_layouts && x_layouts[i] == TW_LAYOUT_PLAN;
     const bool ws = !scatter[i];
-    if (int st = launch_k2(p, xs[i], m, ld_xs[i], cts[i], ld_cts[i], out_dtype,
-                           ws ? k1_out[i] : nullptr, ws ? k1_ld[i] : 0,
-                           ws ? p->n_ov_cols_all : p->n_ov_cols, nullptr, false, s, plan_layout))
-      return st;
+    build_k2_args(p, xs[i], m, ld_xs[i], cts[i], ld_cts[i], out_dtype, ws ? k1_out[i] : nullptr,
+                  ws ? k1_ld[i] : 0, ws ? p->n_ov_cols_all : p->n_ov_cols, nullptr, false,
+                  plan_layout, rg.args[i]);
+    const ResidualArgs& a = rg.args[i];
+    if (!a.rv || a.block_tokens <= 0 || a.n_cols <= 0 ||
+        (a.in_dtype == kBF16) != (rg.args[0].in_dtype == kBF16))
+      grouped = false;
+    rg.cta0[i + 1] = rg.cta0[i] + (a.n_cols > 0 ? a.n_blocks * a.n_groups : 0);
   }
+  rg.n = n;
+  if (grouped) {
+    TW_CUDA(launch_tw_residual_group(rg, s));
+    return TW_OK;
+  }
+  for (int i = 0; i < n; ++i) TW_CUDA(launch_tw_residual(rg.args[i], s));
   return TW_OK;
 }
 
@@ -1818,11 +1838,13 @@ int tw_plan_row_order(const tw_plan* p, int32_t* out_rows) {
 // condensed TW result the kept columns read (workspace mode), nullptr = the
 // out rows themselves; meta overrides the plan's per-column table; acc_all:
 // every column adds onto its out row.
-static int launch_k2(const tw_plan* p, const void* x, int64_t m, int64_t ld_x, void* ct,
-                     int64_t ld_ct, int32_t out_dtype, const void* src, int64_t ld_src,
-                     int32_t n_cols, const int4* meta, bool acc_all, cudaStream_t s,
-                     bool plan_layout) {
-  ResidualArgs r{};
+// K2's arguments for n_cols columns of the plan's overlay lists (see
+// launch_k2).
+static void build_k2_args(const tw_plan* p, const void* x, int64_t m, int64_t ld_x, void* ct,
+                          int64_t ld_ct, int32_t out_dtype, const void* src, int64_t ld_src,
+                          int32_t n_cols, const int4* meta, bool acc_all, bool plan_layout,
+                          ResidualArgs& r) {
+  r = ResidualArgs{};
   r.at = x;
   r.ld_at = ld_x;
   r.in_dtype = p->dtype;
@@ -1880,6 +1902,15 @@ static int launch_k2(const tw_plan* p, const void* x, int64_t m, int64_t ld_x, v
     }
     r.group_first[r.n_groups] = r.n_cols;
   }
+}
+
+static int launch_k2(const tw_plan* p, const void* x, int64_t m, int64_t ld_x, void* ct,
+                     int64_t ld_ct, int32_t out_dtype, const void* src, int64_t ld_src,
+                     int32_t n_cols, const int4* meta, bool acc_all, cudaStream_t s,
+                     bool plan_layout) {
+  ResidualArgs r;
+  build_k2_args(p, x, m, ld_x, ct, ld_ct, out_dtype, src, ld_src, n_cols, meta, acc_all,
+                plan_layout, r);
   TW_CUDA(launch_tw_residual(r, s));
   return TW_OK;
 }

@@ -158,6 +158,16 @@ struct ResidualArgs {
 };
 cudaError_t launch_tw_residual(const ResidualArgs& args, cudaStream_t stream);
 
+// K2 of several layers in one launch: layer p owns CTAs [cta0[p], cta0[p+1])
+// (its n_blocks x n_groups grid, flattened); staged (block_tokens > 0) only.
+constexpr int kMaxResGroup = 4;
+struct ResidualGroupArgs {
+  ResidualArgs args[kMaxResGroup];
+  int32_t cta0[kMaxResGroup + 1];
+  int32_t n;
+};
+cudaError_t launch_tw_residual_group(const ResidualGroupArgs& g, cudaStream_t stream);
+
 // ct[u] = src[src_row[u]] (or 0 where src_row[u] < 0) for u < n_rows, M tokens,
 // element size esz (the caller's tile product scattered to the union rows).
 cudaError_t launch_scatter_rows(const void* src, int64_t ld_src, const int32_t* src_row,
