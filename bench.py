@@ -944,9 +944,10 @@ def run_ours(args, cfg, rank: int, world: int) -> None:
                          "port_matches_reference": port_ok},
         **extra,
         # K1 launches per step: one for the whole grouped step (tw_gemm_group),
-        # one per layer sequentially; plus one K2 per layer for TEW
-        "gpu_launches": args.steps * ((1 if schedule == "grouped" and groups_fused else len(layers))
-                                      + (len(layers) if tew else 0)),
+        # one per layer sequentially; TEW adds as many K2 launches (grouped:
+        # one tw_residual_group_kernel)
+        "gpu_launches": args.steps * (1 if schedule == "grouped" and groups_fused else len(layers))
+                        * (2 if tew else 1),
         "launch": "CUDA graph per step (one graph per rotating buffer set)",
         "clocks": clocks,
     }
