@@ -1645,9 +1645,8 @@ static int group_k1(const tw_plan* const* plans, int32_t n, const void* const* x
   // under programmatic dependent launch -- where a step's CTAs take SMs in
   // launch order as the previous step's free them -- the longest ones start
   // earliest
-  struct CtaRef { int p, c; double w; };
+  struct CtaRef { int p, c; double w; CtaWork work; bool owner; };
   std::vector<CtaRef> ctas;
-  std::vector<const TwLaunch*> launches(n);
   for (int i = 0; i < n; ++i) {
     const tw_plan* p = plans[i];
     if (int st = check_io(p, xs[i], m, ld_xs[i], outs[i], ld_outs[i], out_dtype)) return st;
@@ -1670,7 +1669,6 @@ static int group_k1(const tw_plan* const* plans, int32_t n, const void* const* x
     if (grid + L.grid > kMaxCtas || L.grid > 255)
       return fail(TW_ERR_INVALID_INPUT, "group launch needs %d CTAs (> %d): set SM budgets",
                   grid + L.grid, kMaxCtas);
-    launches[i] = Lp;
     g.map_pay[i] = launch_payload_map(p, L);
     g.map_out[i] = L.map_out;
     g.run_maps[i] = L.maps;
@@ -1684,7 +1682,8 @@ static int group_k1(const tw_plan* const* plans, int32_t n, const void* const* x
         const int units = cw.usz > 0 ? (cw.e - cw.b + cw.usz - 1) / cw.usz : 0;
         w = (double)(cw.e - cw.b) * cw.kp_steps + 3000.0 / 4.0 * units;  // group.py cost model
       }
-      ctas.push_back({i, c, w});
+      // the work entry is copied while the plan's launch cache is locked
+      ctas.push_back({i, c, w, L.a.owner ? L.work.w[c] : CtaWork{}, L.a.owner != 0});
     }
     grid += L.grid;
   }
@@ -1695,7 +1694,7 @@ static int group_k1(const tw_plan* const* plans, int32_t n, const void* const* x
     const CtaRef& r = ctas[b];
     g.cta_plan[b] = (int8_t)r.p;
     g.cta_local[b] = (uint8_t)r.c;
-    if (launches[r.p]->a.owner) work.w[b] = launches[r.p]->work.w[r.c];
+    if (r.owner) work.w[b] = r.work;
   }
   g.n = n;
   if (env.flags & 64) return TW_OK;
