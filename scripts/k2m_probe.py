@@ -3,7 +3,9 @@
 Per layer: K2 alone (TW_TEW_PARTS=2) and K1 + K2 timed in a 32-launch CUDA
 graph for both kernels (TW_K2_LEGACY selects per launch), the two results
 compared with each other and sampled tokens against the oracle.
-Diagnostic only (python scripts/k2m_probe.py on a GPU box).
+Diagnostic only (python scripts/k2m_probe.py on a GPU box).  K2m was
+reverted; apply profiles/r2_k2m_experiment.patch first (it restores
+TW_K2_LEGACY and the K2m kernel).
 """
 import os
 import sys
