@@ -91,6 +91,17 @@ __device__ __forceinline__ void fma8(float (&acc)[8], const uint4& a, uint16_t v
 }
 
 
+// two fp32 values rounded to a packed 16-bit pair (x: low half)
+template <bool kBf>
+__device__ __forceinline__ uint32_t pack2(float x, float y) {
+  if (kBf) {
+    const __nv_bfloat162 h = __floats2bfloat162_rn(x, y);
+    return *reinterpret_cast<const uint32_t*>(&h);
+  }
+  const __half2 h = __floats2half2_rn(x, y);
+  return *reinterpret_cast<const uint32_t*>(&h);
+}
+
 // 4 outputs out[bs..bs+3] = o (+ src[ps..ps+3] when ps >= 0: the TW result),
 // 16-bit or fp32, tail-masked by n.
 __device__ __forceinline__ void residual_store4(const ResidualArgs& args, int64_t bs, int n,
@@ -136,20 +147,29 @@ __device__ __forceinline__ void residual_store4(const ResidualArgs& args, int64_
   }
 }
 
-// One CTA of K2: token block bx, column split by.
-template <int T, bool kBf>
+// One CTA of K2: token block bx, column split by.  TPL tokens per lane: 8
+// (one 16-byte chunk of a staged row per entry) or 16 (two chunks, T = 64:
+// half the lanes per column, so the per-column work around the FMAs --
+// metadata, entry broadcast, the output read-modify-write -- is spread over
+// twice the products; odd columns of a warp step read their second chunk
+// first, so each of the two loads of a warp covers all 32 banks).
+template <int T, bool kBf, int TPL = 8, int NT = kResThreads>
 __device__ __forceinline__ void residual_body(const ResidualArgs& args, const int bx,
                                               const int by) {
   extern __shared__ __align__(16) uint8_t res_smem[];
   uint16_t* sA = reinterpret_cast<uint16_t*>(res_smem);  // [K][T]
-  constexpr int L = T / 8;        // lanes per column (8 tokens each)
+  constexpr int kH = TPL / 8;     // 16-byte chunks per lane and entry
+  constexpr int L = T / TPL;      // lanes per column
   constexpr int kCols = 32 / L;   // columns per warp step
+  static_assert(kH == 1 || kH == 2, "8 or 16 tokens per lane");
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint16_t* at = static_cast<const uint16_t*>(args.at);
   const int K = args.K;
   const int sub = lane / L;
   const int tl = lane - sub * L;
-  const int tok = tl * 8;
+  const int swp = kH == 2 ? (sub & 1) : 0;
+  // tokens of the first (and second) chunk this lane reads
+  const int tokA = tl * TPL + 8 * swp, tokB = tl * TPL + 8 * (1 - swp);
   const int64_t t0 = static_cast<int64_t>(bx) * T;
   const int64_t rem = args.M - t0;
   const int ntok = rem < T ? static_cast<int>(rem) : T;
@@ -161,7 +181,7 @@ __device__ __forceinline__ void residual_body(const ResidualArgs& args, const in
   {
     constexpr int per_row = T / 8;
     // row K stays zero: padding entries (row K, value 0) add exactly 0
-    for (int i = threadIdx.x; i < (K + 1) * per_row; i += kResThreads) {
+    for (int i = threadIdx.x; i < (K + 1) * per_row; i += NT) {
       const int r = i / per_row, j = (i - r * per_row) * 8;
       const int valid = r < K ? ntok - j : 0;
       const uint32_t bytes = valid >= 8 ? 16u : (valid > 0 ? static_cast<uint32_t>(valid) * 2 : 0u);
@@ -173,57 +193,66 @@ __device__ __forceinline__ void residual_body(const ResidualArgs& args, const in
   }
   // the next kernel may launch; it waits for this grid before touching data
   grid_launch_dependents();
-  const uint16_t* sAt = sA + tok;
-  // One column per lane group per step; the next step's metadata is
-  // prefetched one step ahead.
-  constexpr int kStep = kCols * kResWarps;
+  constexpr int kStep = kCols * (NT / 32);
   constexpr int G = L;  // entries per group (1 per lane, one 4-byte load)
-  // entries: 16-bit value << 16 | row offset in 16-byte units (row * L)
-  const uint32_t zrow = static_cast<uint32_t>(K) * L;
-  const uint8_t* sAb = reinterpret_cast<const uint8_t*>(sAt);
-  const bool fast = args.vec_ok && args.out_dtype != kF32 && args.ld_out % 8 == 0;
+  // entries: 16-bit value << 16 | row offset in 16-byte units (row * T / 8)
+  const uint32_t zrow = static_cast<uint32_t>(K) * (T / 8);
+  const uint8_t* sAa = reinterpret_cast<const uint8_t*>(sA + tokA);
+  const uint8_t* sAb = reinterpret_cast<const uint8_t*>(sA + tokB);
+  // whole blocks with 16-bit outputs of the input type and 16-byte aligned
+  // rows (t0 is a multiple of T, pitches of 8 elements): one 16-byte
+  // read-modify-write per chunk, the TW result added with FHFMA (x * 1 + acc:
+  // exact product, one rounding, as widening and adding)
+  const bool fast = args.vec_ok && args.out_dtype == (kBf ? kBF16 : kF16) && ntok == T &&
+                    args.ld_out % 8 == 0 && (!args.src || args.ld_src % 8 == 0);
+  const uint16_t one = kBf ? 0x3f80u : 0x3c00u;
+  uint16_t* out16 = static_cast<uint16_t*>(args.out);
+  const void* src = args.src ? args.src : args.out;
+  const uint16_t* src16 = static_cast<const uint16_t*>(src);
   int cs = c0 + warp * kCols;
   // columns past c1 read the (zero-row) padding at the start of the lists
   int4 m = cs + sub < c1 ? __ldg(args.meta + cs + sub) : make_int4(0, 0, 0, 0);
+  // first two entry groups of the current column; for later columns they are
+  // loaded at the end of the previous step, so their latency overlaps that
+  // step's stores and this step's setup
+  uint32_t c = __ldg(args.rv + m.x + tl), n1 = __ldg(args.rv + m.x + tl + L);
   for (; cs < c1; cs += kStep) {
     const int col = cs + sub;
+    // the next step's metadata, one step ahead
     const int4 mn = col + kStep < c1 ? __ldg(args.meta + col + kStep) : make_int4(0, 0, 0, 0);
-    const bool live = col < c1 && tok < ntok;
-    const int64_t bs = static_cast<int64_t>(m.z) * args.ld_out + t0 + tok;
+    const bool incol = col < c1;
+    const int64_t bs0 = static_cast<int64_t>(m.z) * args.ld_out + t0;
     // the TW result of a kept column (workspace row m.w - 1, else the out row
-    // itself), read now and consumed after the sum
-    const void* src = args.src ? args.src : args.out;
-    const int64_t ps = args.acc_all ? bs
-                       : m.w == 0 ? -1
-                       : args.src ? static_cast<int64_t>(m.w - 1) * args.ld_src + t0 + tok
-                                  : bs;
-    uint4 prev = make_uint4(0u, 0u, 0u, 0u);
-    const bool vec = fast && ntok - tok >= 8 && (ps < 0 || ps % 8 == 0);
-    if (live && vec && ps >= 0)
-      prev = *reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(src) + ps);
+    // itself); -1: residual-only column
+    const int64_t ps0 = args.acc_all ? bs0
+                        : m.w == 0 ? -1
+                        : args.src ? static_cast<int64_t>(m.w - 1) * args.ld_src + t0
+                                   : bs0;
     const int maxlen = __reduce_max_sync(0xffffffffu, m.y);
-    float ac[8];
+    float aa[8], ab[8];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) ac[i] = 0.f;
+    for (int i = 0; i < 8; ++i) aa[i] = ab[i] = 0.f;
+    // one entry: its staged row (one or two chunks) times its value
+    auto entry = [&](uint32_t q) {
+      // PRMT (zero-extended low half) + IMAD: the chunk address
+      const uint32_t off = __byte_perm(q, 0u, 0x4410) * 16u;
+      const uint16_t v = static_cast<uint16_t>(q >> 16);
+      fma8<kBf>(aa, *reinterpret_cast<const uint4*>(sAa + off), v);
+      if constexpr (kH == 2) fma8<kBf>(ab, *reinterpret_cast<const uint4*>(sAb + off), v);
+    };
     // entry groups: lane tl holds entry tl of a group;
     // groups gi + 1, gi + 2 are in flight while gi is consumed.  Lists are
     // padded to whole groups with zero-row entries (row K of the block is
     // zero) and a lane group past its list substitutes them, so the entry
     // loop has no branches.
     const uint32_t* lp = args.rv + m.x + tl;
-    uint32_t c = __ldg(lp), n1 = __ldg(lp + L);
     int eo = 0;
     for (; eo + G <= maxlen; eo += G) {
       const uint32_t f = __ldg(lp + 2 * L);
       lp += L;
       if (eo >= m.y) c = zrow;
 #pragma unroll
-      for (int j = 0; j < G; ++j) {
-        const uint32_t q = L == 1 ? c : __shfl_sync(0xffffffffu, c, j, L);  // lane j of the group (immediate)
-        // PRMT (zero-extended low half) + LEA: two instructions per address
-        fma8<kBf>(ac, *reinterpret_cast<const uint4*>(sAb + __byte_perm(q, 0u, 0x4410) * 16u),
-                  static_cast<uint16_t>(q >> 16));
-      }
+      for (int j = 0; j < G; ++j) entry(L == 1 ? c : __shfl_sync(0xffffffffu, c, j, L));
       c = n1;
       n1 = f;
     }
@@ -233,48 +262,47 @@ __device__ __forceinline__ void residual_body(const ResidualArgs& args, const in
       if (eo >= m.y) c = zrow;
       const int cnt = maxlen - eo;
       int j = 0;
-      if (L >= 4 && cnt >= 4) {
+      if (L >= 8 && cnt >= 4) {
         // four entries unrolled (their shared loads in flight together), the
         // rest one by one
 #pragma unroll
-        for (int jj = 0; jj < 4; ++jj) {
-          const uint32_t q = __shfl_sync(0xffffffffu, c, jj, L);
-          fma8<kBf>(ac, *reinterpret_cast<const uint4*>(sAb + __byte_perm(q, 0u, 0x4410) * 16u),
-                    static_cast<uint16_t>(q >> 16));
-        }
+        for (int jj = 0; jj < 4; ++jj) entry(__shfl_sync(0xffffffffu, c, jj, L));
         j = 4;
       }
 #pragma unroll 1
-      for (; j < cnt; ++j) {
-        const uint32_t q = L == 1 ? c : __shfl_sync(0xffffffffu, c, j, L);  // lane j of the group
-        // PRMT (zero-extended low half) + LEA: two instructions per address
-        fma8<kBf>(ac, *reinterpret_cast<const uint4*>(sAb + __byte_perm(q, 0u, 0x4410) * 16u),
-                  static_cast<uint16_t>(q >> 16));
-      }
+      for (; j < cnt; ++j) entry(L == 1 ? c : __shfl_sync(0xffffffffu, c, j, L));
     }
-    if (live) {
-      if (vec) {
-        // 16-byte read-modify-write of 8 16-bit outputs
-        const bool obf = args.out_dtype == kBF16;
-        const uint32_t pw[4] = {prev.x, prev.y, prev.z, prev.w};
-        uint32_t o[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const float2 fp = h2_to_f2(pw[i], obf);
-          const float f0 = fp.x + ac[2 * i], f1 = fp.y + ac[2 * i + 1];
-          if (!obf) {
-            const __half2 h = __floats2half2_rn(f0, f1);
-            o[i] = *reinterpret_cast<const uint32_t*>(&h);
-          } else {
-            const __nv_bfloat162 h = __floats2bfloat162_rn(f0, f1);
-            o[i] = *reinterpret_cast<const uint32_t*>(&h);
-          }
+    // the next column's first two entry groups, in flight during the stores
+    c = __ldg(args.rv + mn.x + tl);
+    n1 = __ldg(args.rv + mn.x + tl + L);
+    if (fast) {
+      if (incol) {
+        // the TW result is read here, not before the entry loop: holding it
+        // across the loop costs registers the loop's loads in flight need
+        if (ps0 >= 0) {
+          fma8<kBf>(aa, *reinterpret_cast<const uint4*>(src16 + ps0 + tokA), one);
+          if constexpr (kH == 2) fma8<kBf>(ab, *reinterpret_cast<const uint4*>(src16 + ps0 + tokB), one);
         }
-        *reinterpret_cast<uint4*>(static_cast<uint16_t*>(args.out) + bs) = make_uint4(o[0], o[1], o[2], o[3]);
-      } else {
-        residual_store4(args, bs, ntok - tok, src, ps, ac[0], ac[1], ac[2], ac[3]);
-        if (tok + 4 < ntok)
-          residual_store4(args, bs + 4, ntok - tok - 4, src, ps < 0 ? -1 : ps + 4, ac[4], ac[5],
+        uint16_t* orow = out16 + bs0;
+        *reinterpret_cast<uint4*>(orow + tokA) =
+            make_uint4(pack2<kBf>(aa[0], aa[1]), pack2<kBf>(aa[2], aa[3]),
+                       pack2<kBf>(aa[4], aa[5]), pack2<kBf>(aa[6], aa[7]));
+        if constexpr (kH == 2)
+          *reinterpret_cast<uint4*>(orow + tokB) =
+              make_uint4(pack2<kBf>(ab[0], ab[1]), pack2<kBf>(ab[2], ab[3]),
+                         pack2<kBf>(ab[4], ab[5]), pack2<kBf>(ab[6], ab[7]));
+      }
+    } else {
+#pragma unroll
+      for (int h = 0; h < kH; ++h) {
+        const int tk = h ? tokB : tokA;
+        const float* ac = h ? ab : aa;
+        if (!incol || tk >= ntok) continue;
+        const int64_t bs = bs0 + tk;
+        const int64_t ps = ps0 < 0 ? -1 : ps0 + tk;
+        residual_store4(args, bs, ntok - tk, src, ps, ac[0], ac[1], ac[2], ac[3]);
+        if (tk + 4 < ntok)
+          residual_store4(args, bs + 4, ntok - tk - 4, src, ps < 0 ? -1 : ps + 4, ac[4], ac[5],
                           ac[6], ac[7]);
       }
     }
@@ -282,10 +310,10 @@ __device__ __forceinline__ void residual_body(const ResidualArgs& args, const in
   }
 }
 
-template <int T, bool kBf>
-__global__ void __launch_bounds__(kResThreads, 1)
+template <int T, bool kBf, int TPL, int NT = kResThreads>
+__global__ void __launch_bounds__(NT, 1)
     tw_residual_kernel(const __grid_constant__ ResidualArgs args) {
-  residual_body<T, kBf>(args, blockIdx.x, blockIdx.y);
+  residual_body<T, kBf, TPL, NT>(args, blockIdx.x, blockIdx.y);
 }
 
 // K2 of several layers in one launch (the TEW grouped step): layer p owns
@@ -299,6 +327,10 @@ __global__ void __launch_bounds__(kResThreads, 1)
   const ResidualArgs& a = g.args[p];
   const int local = static_cast<int>(blockIdx.x) - g.cta0[p];
   const int bx = local % a.n_blocks, by = local / a.n_blocks;
+  if (a.tokens_per_lane == 16) {
+    residual_body<64, kBf, 16>(a, bx, by);
+    return;
+  }
   switch (a.block_tokens) {
     case 64: residual_body<64, kBf>(a, bx, by); break;
     case 32: residual_body<32, kBf>(a, bx, by); break;
@@ -477,7 +509,7 @@ int residual_block_tokens(int32_t K, int* ctas_per_sm) {
   return 0;
 }
 
-template <int T, bool kBf>
+template <int T, bool kBf, int TPL, int NT = kResThreads>
 static cudaError_t launch_res_t(const ResidualArgs& args, cudaStream_t stream) {
   const size_t smem = static_cast<size_t>(args.K + 1) * T * 2;
   // the dynamic shared-memory limit is raised once per device (to the
@@ -487,14 +519,14 @@ static cudaError_t launch_res_t(const ResidualArgs& args, cudaStream_t stream) {
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
   if (dev >= 64 || !(configured >> dev & 1u)) {
-    e = cudaFuncSetAttribute(tw_residual_kernel<T, kBf>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    e = cudaFuncSetAttribute(tw_residual_kernel<T, kBf, TPL, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(200 * 1024 + 2 * T));
     if (e != cudaSuccess) return e;
     if (dev < 64) configured |= uint64_t{1} << dev;
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(static_cast<unsigned>(args.n_blocks), static_cast<unsigned>(args.n_groups));
-  cfg.blockDim = dim3(kResThreads);
+  cfg.blockDim = dim3(NT);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
   // programmatic dependent launch: K2's CTAs start as K1's leave (the
@@ -504,13 +536,13 @@ static cudaError_t launch_res_t(const ResidualArgs& args, cudaStream_t stream) {
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, tw_residual_kernel<T, kBf>, args);
+  return cudaLaunchKernelEx(&cfg, tw_residual_kernel<T, kBf, TPL, NT>, args);
 }
 
-template <int T>
+template <int T, int TPL = 8, int NT = kResThreads>
 static cudaError_t launch_res(const ResidualArgs& args, cudaStream_t stream) {
-  return args.in_dtype == kBF16 ? launch_res_t<T, true>(args, stream)
-                                : launch_res_t<T, false>(args, stream);
+  return args.in_dtype == kBF16 ? launch_res_t<T, true, TPL, NT>(args, stream)
+                                : launch_res_t<T, false, TPL, NT>(args, stream);
 }
 
 cudaError_t launch_tw_residual_group(const ResidualGroupArgs& g, cudaStream_t stream) {
@@ -554,7 +586,9 @@ cudaError_t launch_tw_residual_group(const ResidualGroupArgs& g, cudaStream_t st
 cudaError_t launch_tw_residual(const ResidualArgs& args, cudaStream_t stream) {
   if (args.n_cols <= 0 || args.M <= 0) return cudaSuccess;
   switch (args.rv ? args.block_tokens : 0) {
-    case 64: return launch_res<64>(args, stream);
+    case 64:
+      return args.tokens_per_lane == 16 ? launch_res<64, 16>(args, stream)
+                                        : launch_res<64>(args, stream);
     case 32: return launch_res<32>(args, stream);
     case 16: return launch_res<16>(args, stream);
     default: break;

@@ -229,7 +229,7 @@ struct tw_plan {
       *this = OvDev{};
     }
   } ov;
-  int32_t ov_block_tokens = 0, ov_ctas_per_sm = 0;
+  int32_t ov_block_tokens = 0, ov_ctas_per_sm = 0, ov_tpl = 8;
   std::vector<int32_t> ov_start;       // host copy of the K2 column pointers
 
   ~tw_plan() {
@@ -1162,7 +1162,7 @@ int tw_plan_attach_overlay(tw_plan* p, int32_t k, int32_t n, int64_t nnz, const 
   // (L = T / 8 lanes per column), so every lane fetches its next entry with
   // one 4-byte load (1 instead of 2 per lane: less padding, 11.5 entries per
   // column on BERT).
-  int32_t new_block_tokens = 0, new_ctas_per_sm = 0;
+  int32_t new_block_tokens = 0, new_ctas_per_sm = 0, new_tpl = 8;
   const int32_t kr = p->k_rows();  // rows of the kernels' A^T (2k for fp32 plans)
   if (kr < 65535 && !ov_cols.empty() && !env_int("TW_RESIDUAL_DIRECT", 0)) {
     int cps = 0;
@@ -1170,7 +1170,11 @@ int tw_plan_attach_overlay(tw_plan* p, int32_t k, int32_t n, int64_t nnz, const 
     if (T > 0) {
       new_block_tokens = T;
       new_ctas_per_sm = cps;
-      const int G = T / 8;
+      // entries per group = lanes per column: T / 8 (8 tokens per lane), or
+      // T / 16 with 16 tokens per lane (T = 64)
+      new_tpl = (T == 64 && env_int("TW_K2_TPL", 16) == 16) ? 16 : 8;
+      const int G = T / new_tpl;
+      const int row16 = T / 8;  // staged row length in 16-byte units
       std::vector<uint32_t> rv;
       std::vector<int4> meta(ov_cols.size());
       // Shared-memory bank classes: a staged row is T * 2 bytes, so
@@ -1183,7 +1187,7 @@ int tw_plan_attach_overlay(tw_plan* p, int32_t k, int32_t n, int64_t nnz, const 
       // then covers the classes evenly.  Classes follow the row the kernel
       // reads (layout position on row-run plans); the natural-order list uses
       // the same entry order, so both paths stay bit-identical.
-      const int C = std::max(1, 64 / T), kCols = 256 / T;
+      const int C = std::max(1, 64 / T), kCols = 32 / G;
       std::vector<int32_t> order;
       std::vector<std::vector<int32_t>> cls(C);
       for (size_t i = 0; i < ov_cols.size(); ++i) {
@@ -1198,7 +1202,9 @@ int tw_plan_attach_overlay(tw_plan* p, int32_t k, int32_t n, int64_t nnz, const 
             cls[r % C].push_back(e);
           }
           std::vector<size_t> head(C, 0);
-          int c = (int)(i % (size_t)kCols) % C;
+          // 16 tokens per lane: odd columns read their chunks in the other
+          // order, so the class alternates per column pair
+          int c = (int)((i % (size_t)kCols) / (new_tpl == 16 ? 2 : 1)) % C;
           for (int32_t t = 0; t < n; ++t) {
             while (head[c] >= cls[c].size()) c = (c + 1) % C;
             order.push_back(cls[c][head[c]++]);
@@ -1219,10 +1225,10 @@ int tw_plan_attach_overlay(tw_plan* p, int32_t k, int32_t n, int64_t nnz, const 
       for (size_t i = 0; i < ov_cols.size(); ++i) max_len = std::max(max_len, start[i + 1] - start[i]);
       rv.resize(rv.size() + ((size_t)(max_len + G - 1) / G + 2) * G, (uint32_t)kr << 16);
       // device form: value << 16 | row offset in 16-byte units of the staged
-      // block (row * T * 2 / 16 = row * G < 2^16 since the block is <= 200 KB),
-      // so K2 forms the shared-memory address with one mask and one shift-add
-      auto device_form = [G](std::vector<uint32_t> v) {
-        for (uint32_t& x : v) x = ((x & 0xffffu) << 16) | ((x >> 16) * (uint32_t)G);
+      // block (row * T * 2 / 16 < 2^16 since the block is <= 200 KB), so K2
+      // forms the shared-memory address with one mask and one shift-add
+      auto device_form = [row16](std::vector<uint32_t> v) {
+        for (uint32_t& x : v) x = ((x & 0xffffu) << 16) | ((x >> 16) * (uint32_t)row16);
         return v;
       };
       if (int st = upload(&nd.rv, device_form(rv), s)) return st;
@@ -1239,6 +1245,7 @@ int tw_plan_attach_overlay(tw_plan* p, int32_t k, int32_t n, int64_t nnz, const 
   p->ov = nd;
   ng.keep = true;
   p->ov_block_tokens = new_block_tokens;
+  p->ov_tpl = new_tpl;
   p->ov_ctas_per_sm = new_ctas_per_sm;
   p->ov_start = start;
   p->union_cols = uni;
@@ -1869,6 +1876,7 @@ static void build_k2_args(const tw_plan* p, const void* x, int64_t m, int64_t ld
   r.vec_ok = al16(ct, ld_ct, esz) && (!src || al16(src, ld_src, esz)) ? 1 : 0;
   r.rv = plan_layout ? p->ov.rv_pos : p->ov.rv;
   r.block_tokens = p->ov_block_tokens;
+  r.tokens_per_lane = p->ov_tpl;
   if (r.block_tokens > 0) {
     // grid = token blocks x column splits; splits (nnz-balanced runs of the
     // descending-nnz column order) are added only to round the number of

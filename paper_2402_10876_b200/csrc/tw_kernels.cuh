@@ -149,6 +149,7 @@ struct ResidualArgs {
   int32_t n_cols;
   int32_t K;                // rows of A^T
   int32_t block_tokens;     // T: tokens of the staged A^T block (0 = direct kernel)
+  int32_t tokens_per_lane;  // 8, or 16 (T = 64 only): lists grouped by T / tokens_per_lane
   int32_t n_blocks;         // ceil(M / T): grid.x
   int32_t n_groups;         // nnz-balanced column splits: grid.y
   int32_t vec_ok;           // out (and src) bases and pitches 16-byte aligned: vector I/O allowed

@@ -339,6 +339,31 @@ def test_tew_workspace_path_bit_identical(out_dtype):
     assert torch.equal(o_ws, o_sc)
 
 
+@pytest.mark.parametrize("compute,m,out_dtype", [
+    ("fp16", 8192, "fp16"), ("bf16", 4096, "bf16"), ("fp16", 1000, "fp16"), ("fp16", 640, "fp32"),
+])
+def test_tew_k2_16_tokens_per_lane_bit_identical(compute, m, out_dtype, monkeypatch):
+    """K2 with 16 tokens per lane (the default for 64-token blocks) against
+    the 8-token kernel (TW_K2_TPL=8 at plan creation): same entry order, same
+    fp32 sums, so bit-identical outputs -- whole blocks (the 16-byte
+    read-modify-write with the FHFMA add), a ragged last block and fp32
+    outputs (the general store)."""
+    k, n = 768, 3072
+    w = tw.round_to(tw.synthetic_matrix(0, k, n, tw.STREAM_WEIGHTS), compute)
+    a = tw.round_to(tw.synthetic_matrix(0, m, k, tw.STREAM_INPUT), compute)
+    _, tsm, ov = tw.prune_tew(w, 0.75, 0.015, 128)
+    enc = tw.encode_cto(tsm)
+    p16 = tw.TwPlan(enc, ov, compute_dtype=compute)
+    monkeypatch.setenv("TW_K2_TPL", "8")
+    p8 = tw.TwPlan(enc, ov, compute_dtype=compute)
+    x = p16.prepare(a)
+    assert torch_equal(p16.run_tew(x, out_dtype=out_dtype), p8.run_tew(x, out_dtype=out_dtype))
+    idx = np.arange(0, m, max(1, m // 64))
+    ref, _ = orc.tew_reference(a[idx], enc, ov.col_ptr, ov.row_idx, ov.values, n)
+    o32 = p16.run_tew(x, out_dtype="fp32").t().cpu().numpy()[idx]
+    assert tw.relative_error(o32, ref) <= TOL["fp32"]
+
+
 @pytest.mark.parametrize("k,n,m,out_dtype,env", [
     (768, 768, 700, "fp32", {}),
     (3072, 768, 500, "fp16", {}),
