@@ -215,7 +215,22 @@ __device__ __forceinline__ void residual_body(const ResidualArgs& args, const in
   // first two entry groups of the current column; for later columns they are
   // loaded at the end of the previous step, so their latency overlaps that
   // step's stores and this step's setup
-  uint32_t c = __ldg(args.rv + m.x + tl), n1 = __ldg(args.rv + m.x + tl + L);
+  // 32-token blocks (4 lanes per column): every lane loads its column's whole
+  // entry group with one 16-byte load instead of one entry plus 4 shuffles
+  // (the shuffles share the MIO queue with the shared-memory loads: 41.3 ->
+  // 39.3 us on 3072 x 768).  With 16 tokens per lane the extra registers
+  // cost more than the shuffles.
+  constexpr bool kGL = G == 4 && TPL == 8;
+  uint32_t c = 0, n1 = 0;
+  uint4 c4 = make_uint4(0u, 0u, 0u, 0u), n4 = c4;
+  const uint4 z4 = make_uint4(zrow, zrow, zrow, zrow);
+  if constexpr (kGL) {
+    c4 = __ldg(reinterpret_cast<const uint4*>(args.rv + m.x));
+    n4 = __ldg(reinterpret_cast<const uint4*>(args.rv + m.x + G));
+  } else {
+    c = __ldg(args.rv + m.x + tl);
+    n1 = __ldg(args.rv + m.x + tl + L);
+  }
   for (; cs < c1; cs += kStep) {
     const int col = cs + sub;
     // the next step's metadata, one step ahead
@@ -245,8 +260,32 @@ __device__ __forceinline__ void residual_body(const ResidualArgs& args, const in
     // padded to whole groups with zero-row entries (row K of the block is
     // zero) and a lane group past its list substitutes them, so the entry
     // loop has no branches.
-    const uint32_t* lp = args.rv + m.x + tl;
     int eo = 0;
+    if constexpr (kGL) {
+      // the column's lanes share the address of each group load
+      const uint4* lq = reinterpret_cast<const uint4*>(args.rv + m.x);
+      for (; eo + G <= maxlen; eo += G) {
+        const uint4 f4 = __ldg(lq + 2);
+        ++lq;
+        if (eo >= m.y) c4 = z4;
+        entry(c4.x);
+        entry(c4.y);
+        entry(c4.z);
+        entry(c4.w);
+        c4 = n4;
+        n4 = f4;
+      }
+      if (eo < maxlen) {
+        if (eo >= m.y) c4 = z4;
+        const int cnt = maxlen - eo;
+        entry(c4.x);
+        if (cnt > 1) entry(c4.y);
+        if (cnt > 2) entry(c4.z);
+      }
+      c4 = __ldg(reinterpret_cast<const uint4*>(args.rv + mn.x));
+      n4 = __ldg(reinterpret_cast<const uint4*>(args.rv + mn.x + G));
+    } else {
+    const uint32_t* lp = args.rv + m.x + tl;
     for (; eo + G <= maxlen; eo += G) {
       const uint32_t f = __ldg(lp + 2 * L);
       lp += L;
@@ -275,6 +314,7 @@ __device__ __forceinline__ void residual_body(const ResidualArgs& args, const in
     // the next column's first two entry groups, in flight during the stores
     c = __ldg(args.rv + mn.x + tl);
     n1 = __ldg(args.rv + mn.x + tl + L);
+    }
     if (fast) {
       if (incol) {
         // the TW result is read here, not before the entry loop: holding it

@@ -29,7 +29,8 @@ def main():
         a = tw.round_to(tw.synthetic_matrix(0, m, k, tw.STREAM_INPUT), "fp16")
         _, tsm, ov = tw.prune_tew(w, 0.75, 0.015, 128)
         enc = tw.encode_cto(tsm)
-        plan = tw.TwPlan(enc, ov)
+        layout = "runs" if os.environ.get("RUNS") == "1" else "natural"
+        plan = tw.TwPlan(enc, ov, row_layout=layout)
         x = plan.prepare(a)
         o = plan.run_tew(x, out_dtype="fp16")
         torch.cuda.synchronize()
@@ -37,12 +38,20 @@ def main():
         both = graph_us(lambda i: plan.run_tew(x, out=o, out_dtype="fp16"), 32)
         os.environ["TW_TEW_PARTS"] = "2"
         alone = graph_us(lambda i: plan.run_tew(x, out=o, out_dtype="fp16"), 32)
+        os.environ["TW_TEW_PARTS"] = "1"
+        k1 = graph_us(lambda i: plan.run_tew(x, out=o, out_dtype="fp16"), 32)
         del os.environ["TW_TEW_PARTS"]
+        tw_plan = tw.TwPlan(enc, row_layout=layout)
+        xt = tw_plan.prepare(a)
+        ot = tw_plan.run(xt, out_dtype="fp16")
+        k1_tw = graph_us(lambda i: tw_plan.run(xt, out=ot, out_dtype="fp16"), 32)
         o32 = plan.run_tew(x, out_dtype="fp32")
         idx = np.arange(0, m, max(1, m // 256))
         ref, _ = orc.tew_reference(a[idx], enc, ov.col_ptr, ov.row_idx, ov.values, n)
         err = tw.relative_error(o32.t()[torch.as_tensor(idx, device=o32.device)].cpu().numpy(), ref)
-        line.append(f"{k}x{n}: K2 {alone:.2f} us, K1+K2 {both:.2f} us, rel err {err:.2e}")
+        line.append(f"{k}x{n} runs={int(plan.uses_row_runs)}/{int(tw_plan.uses_row_runs)}: "
+                    f"K1 {k1:.2f} (TW plan {k1_tw:.2f}) us, K2 {alone:.2f} us, "
+                    f"K1+K2 {both:.2f} us, rel err {err:.2e}")
         plans.append(plan)
         xs.append(x)
         outs.append(o)
