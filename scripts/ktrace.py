@@ -23,10 +23,11 @@ def main():
     ap.add_argument("--mode", default="1")
     ap.add_argument("--flags", default="0")
     ap.add_argument("--m", type=int, default=8192)
+    ap.add_argument("--shape", default="", help="KxN instead of a BERT layer (e.g. 1024x1024)")
     args = ap.parse_args()
     os.environ["TW_GATHER"] = args.mode
     os.environ["TW_DEBUG_FLAGS"] = args.flags
-    k, n = LAYERS[args.layer]
+    k, n = (tuple(int(v) for v in args.shape.split("x")) if args.shape else LAYERS[args.layer])
     w = tw.round_to(tw.synthetic_matrix(0, k, n, 0), "fp16")
     _, tsm = tw.prune_tw(w, 0.75, 128)
     plan = tw.TwPlan(tw.encode_cto(tsm), row_layout=os.environ.get('TW_ROW_LAYOUT', 'runs'))
@@ -46,6 +47,7 @@ def main():
     print(f"layer {k}x{n} mode={args.mode} flags={args.flags}")
     full_ts, epi = [], []
     ends = []
+    first_active = int(np.argmax(t[:, 1024] != 0))
     for c in range(148):
         t0 = t[c, 3072]
         if t0 == 0:
@@ -59,10 +61,10 @@ def main():
         if len(e):
             ends.append(e[-1, 1] - t0)
             epi.extend((e[:, 1] - e[:, 0]).tolist())
-        if c == 0:
+        if c == first_active:
             iss = np.where(t[c, 0:ns] > 0, t[c, 0:ns] - t0, 0)
             f = ful[:ns] - t0
-            print("  cta0 issue/full/lat: " + " ".join(f"{int(a)}/{int(b)}/{int(b - a)}" for a, b in zip(iss[:16], f[:16])))
+            print(f"  cta {c} issue/full/lat: " + " ".join(f"{int(a)}/{int(b)}/{int(b - a)}" for a, b in zip(iss[:16], f[:16])))
         if c < 4 or c in (74, 147):
             f = ful[:ns] - t0
             print(f" cta {c}: stages {ns}, full at {f[:3].tolist()}..{f[-2:].tolist()}, "
