@@ -174,7 +174,12 @@ TW_API int tw_plan_union_columns(const tw_plan* plan, int32_t* out_cols);
 /* TW product, condensed: ct[N' x m] = (A . W_tw)^T from at = A^T [k x m].
  * Replaces: executor.gemm_cto (executor.py:149-177), gemm_tile_sparse
  * (executor.py:135-146) and execute_batched (executor.py:230-265); all three
- * are bit-identical on the GPU as in the reference. */
+ * are bit-identical on the GPU as in the reference.
+ * Small m (<= 128 tokens) on plans with long tiles (>= 16 64-row stages) runs
+ * split-K: the stages over several CTAs, fp32 partials in a workspace the
+ * plan owns, summed by a second kernel.  Like a cuBLAS handle's workspace,
+ * that workspace serves one launch at a time, so calls on one plan must be
+ * ordered (one stream, or events between streams); TW_SPLITK=0 turns it off. */
 TW_API int tw_gemm(const tw_plan* plan, const void* at, int64_t m, int64_t ld_at, void* ct,
                    int64_t ld_ct, int32_t out_dtype, void* stream);
 

@@ -638,6 +638,44 @@ cudaError_t launch_tw_residual(const ResidualArgs& args, cudaStream_t stream) {
   return cudaGetLastError();
 }
 
+// Split-K reduction (tw_capi.cu, kSplitKMaxTokens): one thread per 4 tokens
+// of a row, the partials summed in split order, launched with programmatic
+// dependent launch after K1 (waits before reading the partials).
+__global__ void __launch_bounds__(256) splitk_reduce_kernel(const __grid_constant__ SplitKArgs a) {
+  grid_dependency_wait();
+  const int r = blockIdx.y;
+  const int t = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  if (r >= a.rows || t >= a.M) return;
+  const float* src = a.ws + static_cast<int64_t>(r) * a.ld_ws + t;
+  float4 acc = *reinterpret_cast<const float4*>(src);
+  for (int j = 1; j < a.splits; ++j) {
+    const float4 v = *reinterpret_cast<const float4*>(src + j * a.split_stride);
+    acc.x += v.x;
+    acc.y += v.y;
+    acc.z += v.z;
+    acc.w += v.w;
+  }
+  const int64_t orow = a.rowmap ? __ldg(a.rowmap + r) : r;
+  const int64_t o = orow * a.ld_out + t;
+  const float f[4] = {acc.x, acc.y, acc.z, acc.w};
+  const int n = a.M - t < 4 ? a.M - t : 4;
+  for (int i = 0; i < n; ++i) store_from_float(a.out, a.out_dtype, o + i, f[i]);
+}
+
+cudaError_t launch_splitk_reduce(const SplitKArgs& a, cudaStream_t stream) {
+  if (a.rows <= 0 || a.M <= 0) return cudaSuccess;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>((a.M + 1023) / 1024), static_cast<unsigned>(a.rows));
+  cfg.blockDim = dim3(256);
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, splitk_reduce_kernel, a);
+}
+
 cudaError_t launch_transpose_cast(const void* a, int32_t a_dtype, int64_t M, int64_t K,
                                   int64_t lda, void* at, int32_t at_dtype, int64_t ld_at,
                                   const int32_t* out_row, cudaStream_t stream) {

@@ -141,6 +141,10 @@ struct TwLaunch {  // everything a K1 launch needs besides the plan constants
   bool resident = false;
   bool sparse = false;  // tcgen05.mma.sp on the compressed payload
   bool sparse_resident = false;
+  // split-K (small M): K1 wrote S fp32 partial products into the plan's
+  // workspace; splitk_reduce sums them into the caller's output
+  int splitk = 0;
+  SplitKArgs red{};
 };
 
 struct tw_plan;
@@ -170,7 +174,7 @@ struct tw_plan {
     const void* x; int64_t m, ld_x; void* ct; int64_t ld_ct; int32_t out_dtype;
     const int32_t* rowmap; int64_t out_rows; bool plan_layout; int32_t budget;
     int flags, no_tma_store, strided, force_owner, gran, split1, run_max_units, no_sparse,
-        sparse_resident;
+        sparse_resident, splitk;
     long long* trace;
     bool operator==(const Key& o) const { return std::memcmp(this, &o, sizeof(Key)) == 0; }
   };
@@ -230,12 +234,16 @@ struct tw_plan {
     }
   } ov;
   int32_t ov_block_tokens = 0, ov_ctas_per_sm = 0, ov_tpl = 8;
+  // split-K workspace for small M: up to splitk_max partial products of
+  // n_cond rows x kSplitKMaxTokens fp32 (allocated at plan creation)
+  float* d_splitws = nullptr;
+  int32_t splitk_max = 0;
   std::vector<int32_t> ov_start;       // host copy of the K2 column pointers
 
   ~tw_plan() {
     for (void* p : {(void*)d_subtiles, (void*)d_gidx, d_payload, (void*)d_perm, (void*)d_inv,
                     (void*)d_box_first, (void*)d_boxes, (void*)d_gidx_pos, d_payload_sp,
-                    (void*)d_meta})
+                    (void*)d_meta, (void*)d_splitws})
       if (p) cudaFree(p);
     ov.release();
   }
@@ -286,6 +294,36 @@ struct Reader {
 }  // namespace
 
 static std::vector<int32_t> split_counts(const tw_plan* plan, int G);
+
+// Split-K for small M (tokens <= kSplitKMaxTokens): one CTA per sub-tile would
+// leave most SMs idle while each active CTA streams every stage of its
+// sub-tile at one SM's ingress rate (profiles/r2_k1_stage_ingress.txt), so the
+// stages of every sub-tile are spread over S CTAs instead, each writing an
+// fp32 partial product, and a second kernel sums the S partials in order.
+// Measured (scripts/splitk_probe.py): 3072 x 768 (43 k-steps) at M = 1 / 128:
+// 13.3 -> 8.0 / 14.5 -> 11.1 us; on 9-step sub-tiles (1024^2, 768 x 3072) it
+// only pays below ~20 tokens, and at M = 256 it loses everywhere.
+constexpr int64_t kSplitKMaxTokens = 128;
+constexpr int kSplitKMinSteps = 16;
+constexpr int kSplitKMaxSplits = 16;
+constexpr int64_t kSplitKMaxWsBytes = 64ll << 20;
+
+static int splitk_splits(const tw_plan* p, int budget) {
+  if (p->n_sub < 1 || p->subtiles.empty()) return 0;
+  int min_steps = 1 << 30;
+  for (const SubTile& st : p->subtiles) min_steps = std::min(min_steps, (int)st.kp_steps);
+  return std::min({min_steps, budget / p->n_sub, kSplitKMaxSplits});
+}
+
+static int alloc_splitk_ws(tw_plan* plan) {
+  const int S = splitk_splits(plan, plan->sm_count);
+  if (S < 2) return TW_OK;
+  const int64_t bytes = (int64_t)S * plan->n_cond * kSplitKMaxTokens * 4;
+  if (bytes > kSplitKMaxWsBytes) return TW_OK;
+  TW_CUDA(cudaMalloc(&plan->d_splitws, (size_t)bytes));
+  plan->splitk_max = S;
+  return TW_OK;
+}
 
 static void owner_split(tw_plan* plan) {
   const int G = plan->sm_budget;
@@ -798,6 +836,7 @@ int tw_plan_create_cto_ex(tw_plan** out, int32_t k, int32_t n, int32_t g, int32_
   plan->tile_cost = tile_cost;
   plan->sm_budget = plan->sm_count;
   owner_split(plan);
+  if (int st = alloc_splitk_ws(plan)) return st;
 
   plan->h_gidx = gidx;
   if (int st = upload(&plan->d_subtiles, plan->subtiles, s)) return st;
@@ -1035,6 +1074,7 @@ int tw_plan_load(tw_plan** out, const void* buf, uint64_t len, void* stream) {
   if (int st = sm_count_of_current_device(&plan->sm_count)) return st;
   TW_CUDA(configure_gemm_kernels());
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  for (SubTile& st : plan->subtiles) st.k0 = 0;  // written per launch (split-K) only
   if (int st = upload(&plan->d_subtiles, plan->subtiles, s)) return st;
   if (int st = upload(&plan->d_gidx, plan->h_gidx, s)) return st;
   if (plan->runs) {
@@ -1053,6 +1093,7 @@ int tw_plan_load(tw_plan** out, const void* buf, uint64_t len, void* stream) {
   plan->sm_budget = plan->sm_count;
   if (plan->tile_cost.size() < (size_t)nt) plan->tile_cost.resize(nt, 0.0);
   owner_split(plan);
+  if (int st = alloc_splitk_ws(plan)) return st;
   plan->union_cols = plan->cond_cols;
   *out = guard.release();
   return TW_OK;
@@ -1366,13 +1407,13 @@ static int check_io(const tw_plan* p, const void* x, int64_t m, int64_t ld_x, co
 // read on every call (getenv is cheap) so tests can flip them per call.
 struct LaunchEnv {
   int flags, no_tma_store, strided, force_owner, gran, split1, run_max_units, no_sparse,
-      sparse_resident;
+      sparse_resident, splitk;
   long long* trace;
   bool operator==(const LaunchEnv& o) const {
     return flags == o.flags && no_tma_store == o.no_tma_store && strided == o.strided &&
            force_owner == o.force_owner && gran == o.gran && split1 == o.split1 &&
            run_max_units == o.run_max_units && no_sparse == o.no_sparse &&
-           sparse_resident == o.sparse_resident && trace == o.trace;
+           sparse_resident == o.sparse_resident && splitk == o.splitk && trace == o.trace;
   }
 };
 
@@ -1388,6 +1429,8 @@ static LaunchEnv read_launch_env() {
   // bit 0: TW_NO_SPARSE; bit 1: TW_SPARSE_SW128 (diagnostic payload variant)
   e.no_sparse = (env_int("TW_NO_SPARSE", 0) ? 1 : 0) | (env_int("TW_SPARSE_SW128", 0) ? 2 : 0);
   e.sparse_resident = env_int("TW_SPARSE_RESIDENT", 0);
+  // split-K for small M: -1 = when M <= kSplitKMaxTokens, 0 = never, 1 = forced
+  e.splitk = env_int("TW_SPLITK", -1);
   e.trace = g_trace;
   return e;
 }
@@ -1429,6 +1472,7 @@ static int build_tw_launch(const tw_plan* p, const void* x, int64_t m, int64_t l
   // on the SMs; otherwise 256-token units strided over the CTAs.
   int& grid = L.grid;
   WorkTable& work = L.work;
+  std::memset(&work, 0, sizeof(work));  // the cached launch is rebuilt in place
   bool owner = p->owner && !env.strided;
   // sparse tensor-core path: owner mode with the compressed payload resident
   int max_steps_all = 0;
@@ -1454,7 +1498,56 @@ static int build_tw_launch(const tw_plan* p, const void* x, int64_t m, int64_t l
     const int64_t strided = (units + p->sm_budget - 1) / p->sm_budget * kTN * max_steps;
     if (strided < own) owner = false;
   }
-  if (owner) {
+  // split-K for small M (see kSplitKMaxTokens): S CTAs per sub-tile, each a
+  // contiguous range of its k-steps, one unit of all M tokens, fp32 partial
+  // products into the plan's workspace (partial j of condensed row r at row
+  // j * n_cond + r); splitk_reduce then writes the caller's output
+  L.splitk = 0;
+  int S = 0;
+  if (p->d_splitws && !sparse && m <= kSplitKMaxTokens &&
+      (env.splitk > 0 || (env.splitk < 0 && max_steps_all >= kSplitKMinSteps)))
+    S = std::min(splitk_splits(p, p->sm_budget), (int)p->splitk_max);
+  if (S >= 2) {
+    a.owner = 1;
+    grid = p->n_sub * S;
+    const int64_t ldw = (m + 15) / 16 * 16;
+    const int32_t usz = (int32_t)std::min<int64_t>(kTN, (m + 63) / 64 * 64);
+    for (int sidx = 0; sidx < p->n_sub; ++sidx) {
+      const SubTile& st = p->subtiles[sidx];
+      for (int j = 0; j < S; ++j) {
+        CtaWork& w = work.w[sidx * S + j];
+        const int k0 = st.kp_steps * j / S, k1 = st.kp_steps * (j + 1) / S;
+        w.kp_steps = k1 - k0;
+        w.k0 = k0;
+        w.idx_row = st.idx_row;
+        w.pay_row = st.pay_row;
+        w.width = st.width;
+        w.out_row = j * p->n_cond + st.out_row;
+        w.b = 0;
+        w.e = (int32_t)m;
+        w.usz = usz;
+      }
+    }
+    a.out = p->d_splitws;
+    a.ld_out = ldw;
+    a.out_dtype = kF32;
+    a.rowmap = nullptr;
+    a.vec_ok = 1;
+    a.vec32_ok = 1;
+    a.use_tma_store = 0;
+    L.splitk = S;
+    SplitKArgs& r = L.red;
+    r.ws = p->d_splitws;
+    r.splits = S;
+    r.split_stride = (int64_t)p->n_cond * ldw;
+    r.ld_ws = ldw;
+    r.rows = p->n_cond;
+    r.M = (int32_t)m;
+    r.out = ct;
+    r.ld_out = ld_ct;
+    r.out_dtype = out_dtype;
+    r.rowmap = rowmap;
+  } else if (owner) {
     a.owner = 1;
     int gran = env.gran;
     if (gran != 16 && gran != 32 && gran != 64) gran = 64;
@@ -1588,7 +1681,7 @@ static int get_launch(const tw_plan* p, const void* x, int64_t m, int64_t ld_x, 
   key.flags = env.flags; key.no_tma_store = env.no_tma_store; key.strided = env.strided;
   key.force_owner = env.force_owner; key.gran = env.gran; key.split1 = env.split1;
   key.run_max_units = env.run_max_units; key.no_sparse = env.no_sparse;
-  key.sparse_resident = env.sparse_resident; key.trace = env.trace;
+  key.sparse_resident = env.sparse_resident; key.splitk = env.splitk; key.trace = env.trace;
   if (!(p->cache_valid && p->cache_key == key)) {
     p->cache_valid = false;
     if (int st = build_tw_launch(p, x, m, ld_x, ct, ld_ct, out_dtype, rowmap, out_rows,
@@ -1621,6 +1714,7 @@ static int run_tw(const tw_plan* p, const void* x, int64_t m, int64_t ld_x, void
   if (env.flags & 64) return TW_OK;  // diagnostics: host work only, no launch
   TW_CUDA(launch_tw_gemm(launch_payload_map(p, L), L.map_out, L.maps, L.a, L.work, L.resident,
                          L.grid, s));
+  if (L.splitk) TW_CUDA(launch_splitk_reduce(L.red, s));
   return TW_OK;
 }
 
@@ -1642,7 +1736,8 @@ static int group_k1(const tw_plan* const* plans, int32_t n, const void* const* x
   if (!plans || !xs || !ld_xs || !outs || !ld_outs || n < 1)
     return fail(TW_ERR_INVALID_INPUT, "null argument");
   if (n > kMaxGroup) return fail(TW_ERR_INVALID_INPUT, "at most %d plans per group launch", kMaxGroup);
-  const LaunchEnv env = read_launch_env();
+  LaunchEnv env = read_launch_env();
+  env.splitk = 0;  // one launch for every plan: no second (reduce) kernel per plan
   GroupArgs g;
   std::memset(&g, 0, sizeof(g));
   WorkTable work;

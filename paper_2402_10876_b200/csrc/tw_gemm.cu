@@ -117,6 +117,7 @@ struct Walker {
     if (a.owner) {
       const CtaWork& w = *mine;
       d.kp_steps = w.kp_steps;
+      d.k0 = w.k0;
       d.idx_row = w.idx_row;
       d.pay_row = w.pay_row;
       d.width = w.width;
@@ -414,7 +415,7 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& map_pay, const CUte
             continue;
           }
           mbar_arrive_expect_tx(&pfull[ks], kPBytes);
-          tma_load_2d(sP + ks * kPBytes, &map_pay, &pfull[ks], ks * kBK, s0.d.pay_row);
+          tma_load_2d(sP + ks * kPBytes, &map_pay, &pfull[ks], (s0.d.k0 + ks) * kBK, s0.d.pay_row);
         }
       }
     }
@@ -427,7 +428,8 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& map_pay, const CUte
       while (walk.next(args, sg)) {
         const int n = (sg.ue - sg.ub + 15) & ~15;
         const int chunks = (n + 63) >> 6;
-        const int32_t* bf = args.box_first + static_cast<int64_t>(sg.d.idx_row) * args.box_stride;
+        const int32_t* bf =
+            args.box_first + static_cast<int64_t>(sg.d.idx_row) * args.box_stride + sg.d.k0;
         int b0 = __ldg(bf), b1 = __ldg(bf + 1);
         for (int ks = 0; ks < sg.d.kp_steps; ++ks, ++gs) {
           const int stage = gs % kStages;
@@ -445,7 +447,8 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& map_pay, const CUte
             mbar_arrive_expect_tx(&full[stage], (skip_p ? 0u : static_cast<uint32_t>(kPBytes)) +
                                                     (skip_a ? 0u : static_cast<uint32_t>(chunks * kBK * 128)));
             if (!skip_p)
-              tma_load_2d(sP + stage * kPBytes, &map_pay, &full[stage], ks * kBK, sg.d.pay_row);
+              tma_load_2d(sP + stage * kPBytes, &map_pay, &full[stage], (sg.d.k0 + ks) * kBK,
+                          sg.d.pay_row);
           }
           __syncwarp();
           for (int j = b0 + lane, jj = 0; j < b1 && !skip_a; j += 32, jj += 32) {
@@ -479,7 +482,8 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& map_pay, const CUte
             tma_load_2d(sP + stage * kPBytes, &map_pay, &full[stage], (ks >> 1) * kBK, sg.d.pay_row);
           } else {
             mbar_arrive_expect_tx(&full[stage], kPBytes);
-            tma_load_2d(sP + stage * kPBytes, &map_pay, &full[stage], ks * kBK, sg.d.pay_row);
+            tma_load_2d(sP + stage * kPBytes, &map_pay, &full[stage], (sg.d.k0 + ks) * kBK,
+                        sg.d.pay_row);
           }
         }
       }
@@ -528,7 +532,7 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& map_pay, const CUte
     auto stage_chunk = [&](const Seg& g, int c) {  // stages [c * kChunkSt, ...) -> buffer c & 1
       const int first = c * kChunkSt * kBK;
       const int n = min(kChunkSt, g.d.kp_steps - c * kChunkSt) * kBK;
-      const int32_t* src = args.gidx + static_cast<int64_t>(g.d.idx_row) * args.kp + first;
+      const int32_t* src = args.gidx + static_cast<int64_t>(g.d.idx_row) * args.kp + g.d.k0 * kBK + first;
       int32_t* dst = sIdx + (c & 1) * kChunkSt * kBK;
       for (int i = gt; i < n; i += kGatherThreads) dst[i] = __ldg(src + i);
     };
@@ -540,7 +544,7 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& map_pay, const CUte
       named_bar_sync(1, kGatherThreads);
     };
     if (whole) {
-      const int32_t* src = args.gidx + static_cast<int64_t>(sg.d.idx_row) * args.kp;
+      const int32_t* src = args.gidx + static_cast<int64_t>(sg.d.idx_row) * args.kp + sg.d.k0 * kBK;
       for (int i = gt; i < sg.d.kp_steps * kBK; i += kGatherThreads) sIdx[i] = __ldg(src + i);
       named_bar_sync(1, kGatherThreads);
     }

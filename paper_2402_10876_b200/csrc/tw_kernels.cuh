@@ -24,7 +24,8 @@ struct SubTile {
   int32_t out_row;    // first condensed output column == row of C'^T
   int32_t kept;       // K'_i (kept rows), for accounting and LPT ordering
   int32_t stage_off;  // first stage of this sub-tile inside one token block
-  int32_t pad0, pad1, pad2, pad3, pad4;
+  int32_t k0;         // first k-step (split-K: a CTA owns stages [k0, k0 + kp_steps))
+  int32_t pad1, pad2, pad3, pad4;
 };
 
 // Resident-payload kernel: a sub-tile's whole payload (<= kResSteps k-steps,
@@ -39,6 +40,7 @@ struct CtaWork {
   int32_t kp_steps, idx_row, pay_row, width, out_row;  // the owned sub-tile
   int32_t b, e;                                        // token range [b, e)
   int32_t usz;                                         // tokens per unit (0 = idle CTA)
+  int32_t k0;                                          // first k-step (split-K), else 0
 };
 struct WorkTable {
   CtaWork w[kMaxCtas];
@@ -168,6 +170,23 @@ struct ResidualGroupArgs {
   int32_t n;
 };
 cudaError_t launch_tw_residual_group(const ResidualGroupArgs& g, cudaStream_t stream);
+
+// Split-K (small M): out[rowmap ? rowmap[r] : r][t] = sum over j < splits of
+// ws[j * split_stride + r * ld_ws + t] (fp32, in order j = 0, 1, ...), for
+// rows r < rows and tokens t < M, converted to out_dtype.
+struct SplitKArgs {
+  const float* ws;
+  int32_t splits;
+  int64_t split_stride;
+  int64_t ld_ws;
+  int32_t rows;
+  int32_t M;
+  void* out;
+  int64_t ld_out;
+  int32_t out_dtype;
+  const int32_t* rowmap;
+};
+cudaError_t launch_splitk_reduce(const SplitKArgs& a, cudaStream_t stream);
 
 // ct[u] = src[src_row[u]] (or 0 where src_row[u] < 0) for u < n_rows, M tokens,
 // element size esz (the caller's tile product scattered to the union rows).
