@@ -629,7 +629,8 @@ def run_ours(args, cfg, rank: int, world: int) -> None:
             torch.cuda.synchronize()
             ms = e0.elapsed_time(e1) / 5
             return reduce_max(ms, world) if world > 1 else ms
-        tuned = tw.tune_budgets(groups, rotation_ms)
+        moves = tuple(int(v) for v in os.environ.get("TW_TUNE_MOVES", "8,4,2").split(","))
+        tuned = tw.tune_budgets(groups, rotation_ms, moves=moves)
 
     # one CUDA graph per rotating set: a step is one graph replay (3 launches)
     graphs = [capture_graph(lambda r=r: run_set(r)) for r in range(N_ROTATE)]
