@@ -1860,19 +1860,35 @@ int tw_gemm_tew_group(const tw_plan* const* plans, int32_t n, const void* const*
   ResidualGroupArgs rg;
   std::memset(&rg, 0, sizeof(rg));
   bool grouped = n <= kMaxResGroup && !env_int("TW_K2_PER_LAYER", 0);
+  // Layers enter the launch heaviest CTA first (CTAs are dispatched in index
+  // order as SMs free up, so the long ones must not come last: BERT TEW,
+  // 768x3072 / 3072x768 / 768^2 CTAs of ~34 / ~20 / ~11 us, packs 84 -> 75 us
+  // in a list-scheduling model); each CTA's work ~ its entries x tokens.
+  std::vector<int> order(n);
+  std::vector<double> cta_work(n, 0.0);
   for (int i = 0; i < n; ++i) {
+    order[i] = i;
+    const tw_plan* p = plans[i];
+    if (p && p->ov_block_tokens > 0 && !p->ov_start.empty())
+      cta_work[i] = (double)p->ov_start.back() * p->ov_block_tokens;
+  }
+  if (!env_int("TW_GROUP_PLAN_ORDER", 0))
+    std::stable_sort(order.begin(), order.end(),
+                     [&](int x, int y) { return cta_work[x] > cta_work[y]; });
+  for (int j = 0; j < n; ++j) {
+    const int i = order[j];
     const tw_plan* p = plans[i];
     if (int st = check_io(p, xs[i], m, ld_xs[i], cts[i], ld_cts[i], out_dtype)) return st;
     const bool plan_layout = x_layouts && x_layouts[i] == TW_LAYOUT_PLAN;
     const bool ws = !scatter[i];
     build_k2_args(p, xs[i], m, ld_xs[i], cts[i], ld_cts[i], out_dtype, ws ? k1_out[i] : nullptr,
                   ws ? k1_ld[i] : 0, ws ? p->n_ov_cols_all : p->n_ov_cols, nullptr, false,
-                  plan_layout, rg.args[i]);
-    const ResidualArgs& a = rg.args[i];
+                  plan_layout, rg.args[j]);
+    const ResidualArgs& a = rg.args[j];
     if (!a.rv || a.block_tokens <= 0 || a.n_cols <= 0 ||
         (a.in_dtype == kBF16) != (rg.args[0].in_dtype == kBF16))
       grouped = false;
-    rg.cta0[i + 1] = rg.cta0[i] + (a.n_cols > 0 ? a.n_blocks * a.n_groups : 0);
+    rg.cta0[j + 1] = rg.cta0[j] + (a.n_cols > 0 ? a.n_blocks * a.n_groups : 0);
   }
   rg.n = n;
   if (grouped) {
