@@ -101,13 +101,18 @@ def test_plan_from_cto1_file(tmp_path):
 
 
 @pytest.mark.gpu
-def test_chain_plans_write_next_layers_run_layout():
+@pytest.mark.parametrize("m,splitk", [(1000, None), (64, "1")])
+def test_chain_plans_write_next_layers_run_layout(m, splitk, monkeypatch):
     """chain_plans (BERT FFN shapes): layer l's epilogue writes C'^T directly
     in layer l+1's row-run order (payload rows permuted inside sub-tiles), and
     layer l+1 reads it with dense TMA boxes -- no prepare pass in between.
-    Both products match the oracle on the same (fp16-rounded) values."""
+    Both products match the oracle on the same (fp16-rounded) values.  At
+    m = 64 with TW_SPLITK=1 both layers run split-K (splitk_reduce writes
+    the permuted order)."""
     import torch
 
+    if splitk:
+        monkeypatch.setenv("TW_SPLITK", splitk)
     rng = np.random.default_rng(5)
     w1 = tw.round_to(rng.normal(size=(768, 3072)).astype(np.float32), "fp16")
     w2 = tw.round_to(rng.normal(size=(3072, 768)).astype(np.float32), "fp16")
@@ -124,7 +129,7 @@ def test_chain_plans_write_next_layers_run_layout():
     kept = np.asarray(t1.column_mask.kept)
     for lo, hi in zip(b[:-1], b[1:]):
         assert sorted(cols[lo:hi].tolist()) == kept[lo:hi].tolist()
-    a = tw.round_to(rng.normal(size=(1000, 768)).astype(np.float32), "fp16")
+    a = tw.round_to(rng.normal(size=(m, 768)).astype(np.float32), "fp16")
     h = prev.run(prev.prepare(a), out_dtype="fp16")             # N1' x M, next's layout
     ref1 = orc.c_gemm_cto_enc(a, e1)                            # M x N1', condensed order
     pos = {int(c): i for i, c in enumerate(kept)}
