@@ -315,12 +315,18 @@ static int splitk_splits(const tw_plan* p, int budget) {
   return std::min({min_steps, budget / p->n_sub, kSplitKMaxSplits});
 }
 
+// Optional: without the workspace (too large, or the allocation fails) the
+// plan simply never splits.
 static int alloc_splitk_ws(tw_plan* plan) {
   const int S = splitk_splits(plan, plan->sm_count);
-  if (S < 2) return TW_OK;
+  if (S < 2 || plan->n_cond > 65535) return TW_OK;  // reduce grid: one row per grid.y
   const int64_t bytes = (int64_t)S * plan->n_cond * kSplitKMaxTokens * 4;
   if (bytes > kSplitKMaxWsBytes) return TW_OK;
-  TW_CUDA(cudaMalloc(&plan->d_splitws, (size_t)bytes));
+  if (cudaMalloc(&plan->d_splitws, (size_t)bytes) != cudaSuccess) {
+    (void)cudaGetLastError();
+    plan->d_splitws = nullptr;
+    return TW_OK;
+  }
   plan->splitk_max = S;
   return TW_OK;
 }
