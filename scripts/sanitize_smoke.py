@@ -20,8 +20,11 @@ import paper_2402_10876_b200 as tw  # noqa: E402
 
 
 def main():
-    only = sys.argv[1] if len(sys.argv) > 1 else "all"   # all | small | runs | gather
+    only = sys.argv[1] if len(sys.argv) > 1 else "all"   # all | small | runs | gather | k2
     rng = np.random.default_rng(0)
+    if only == "k2":
+        k2_and_splitk(rng)
+        return
     for (k, n, m, s, g) in ([] if only in ("runs", "gather") else [(256, 384, 300, 0.75, 128), (1024, 512, 200, 0.5, 128),
                             (96, 80, 37, 0.3, 16)]):
         w = tw.round_to(rng.standard_normal((k, n)).astype(np.float32), "fp16")
@@ -55,6 +58,41 @@ def main():
             del os.environ[key]
     torch.cuda.synchronize()
     print("sanitize smoke done")
+
+
+def k2_and_splitk(rng):
+    """K2 with 16 tokens per lane (T = 64) and the 16-byte group loads (T =
+    32), whole and ragged blocks, 16-bit and fp32 outputs, the grouped K2
+    launch; split-K K1 + splitk_reduce for TW (both layouts) and TEW."""
+    plans, xs = [], []
+    for (k, n, m, dt) in [(768, 512, 200, "fp16"), (3072, 384, 96, "bf16"), (768, 640, 128, "fp16")]:
+        w = tw.round_to(rng.standard_normal((k, n)).astype(np.float32), dt)
+        a = tw.round_to(rng.standard_normal((m, k)).astype(np.float32), dt)
+        _, tsm, ov = tw.prune_tew(w, 0.75, 0.015, 128)
+        plan = tw.TwPlan(tw.encode_cto(tsm), ov, compute_dtype=dt, row_layout="runs")
+        x = plan.prepare(a)
+        for od in ("fp32", dt):
+            plan.run_tew(x, out_dtype=od)
+        if m == 128:
+            plans.append(plan)
+            xs.append(x)
+    w = tw.round_to(rng.standard_normal((3072, 768)).astype(np.float32), "fp16")
+    _, tsm, ov = tw.prune_tew(w, 0.75, 0.015, 128)
+    p3 = tw.TwPlan(tw.encode_cto(tsm), ov, row_layout="runs")
+    x3 = p3.prepare(tw.round_to(rng.standard_normal((128, 3072)).astype(np.float32), "fp16"))
+    tw.TwPlanGroup(plans + [p3], 128).run_tew(xs + [x3], out_dtype="fp16")
+    # split-K: 3072-row tiles (>= 16 stages), M <= 128
+    _, tsm = tw.prune_tw(w, 0.75, 128)
+    for layout in ("natural", "runs"):
+        plan = tw.TwPlan(tw.encode_cto(tsm), row_layout=layout)
+        for m in (1, 77):
+            a = tw.round_to(rng.standard_normal((m, 3072)).astype(np.float32), "fp16")
+            x = plan.prepare(a)
+            plan.run(x, out_dtype="fp16")
+            plan.run(x, out_dtype="fp32")
+    p3.run_tew(x3, out_dtype="fp16")
+    torch.cuda.synchronize()
+    print("sanitize k2 / split-K done")
 
 
 if __name__ == "__main__":
