@@ -858,6 +858,13 @@ def run_ours(args, cfg, rank: int, world: int) -> None:
 
     pk = peaks()
     tot_bytes = sum(p["bytes"] for p in per_layer)
+
+    def splitk_layer(plan) -> bool:
+        # a lone launch of this plan at m tokens runs split-K (tw_gemm)
+        info = plan.info
+        return (info.splitk_max >= 2 and m <= info.splitk_max_tokens
+                and os.environ.get("TW_SPLITK", "-1") != "0"
+                and (info.kp // 64 >= info.splitk_min_steps or os.environ.get("TW_SPLITK") == "1"))
     tot_us = sum(p["us"] for p in per_layer)
     # the dominant kernel of the timed region: with the grouped TW schedule
     # that is the one tw_gemm_group_kernel launch per step (its average
@@ -945,10 +952,13 @@ def run_ours(args, cfg, rank: int, world: int) -> None:
                          "port_matches_reference": port_ok},
         **extra,
         # K1 launches per step: one for the whole grouped step (tw_gemm_group),
-        # one per layer sequentially; TEW adds as many K2 launches (grouped:
-        # one tw_residual_group_kernel)
-        "gpu_launches": args.steps * (1 if schedule == "grouped" and groups_fused else len(layers))
-                        * (2 if tew else 1),
+        # one per layer sequentially (+ its splitk_reduce when a layer runs
+        # split-K, tw_plan_info.splitk_*); TEW adds as many K2 launches
+        # (grouped: one tw_residual_group_kernel)
+        "gpu_launches": args.steps * (
+            (1 if schedule == "grouped" and groups_fused
+             else sum(2 if splitk_layer(p) else 1 for p, _, _ in sets[0]))
+            * (2 if tew else 1)),
         "launch": "CUDA graph per step (one graph per rotating buffer set)",
         "clocks": clocks,
     }

@@ -86,6 +86,11 @@ typedef struct tw_plan_info {
                                  (TVW, patterns.py:645-717) and K1 runs it on
                                  tcgen05.mma.sp from a compressed resident
                                  copy (TW_NO_SPARSE=1: dense tensor cores)  */
+  int32_t splitk_max;         /* split-K for small m: most CTAs per sub-tile
+                                 (0: never; see tw_gemm)                     */
+  int32_t splitk_max_tokens;  /* ... used when m <= this on tiles of at least
+                                 splitk_min_steps 64-row stages             */
+  int32_t splitk_min_steps;
 } tw_plan_info;
 
 /* Build a device plan from a CTO encoding held in host memory.

@@ -36,7 +36,8 @@ class PlanInfo(ctypes.Structure):
                 ("compute_dtype", _i32), ("nnz", _i64), ("kept_macs_per_token", _i64),
                 ("sm_count", _i32), ("has_overlay", _i32), ("row_runs", _i32),
                 ("row_copies", _i32), ("sm_budget", _i32), ("stage_work", _i64),
-                ("sparse_payload", _i32)]
+                ("sparse_payload", _i32), ("splitk_max", _i32),
+                ("splitk_max_tokens", _i32), ("splitk_min_steps", _i32)]
 
 
 # name -> (restype, argtypes); must match include/tw_gemm.h exactly

@@ -386,7 +386,7 @@ extern "C" {
 
 const char* tw_last_error(void) { return g_last_error.c_str(); }
 
-int32_t tw_abi_version(void) { return 420; }
+int32_t tw_abi_version(void) { return 421; }
 
 int tw_plan_create_cto(tw_plan** out, int32_t k, int32_t n, int32_t g, int32_t n_tiles,
                        const uint32_t* row_counts, const uint32_t* col_counts,
@@ -1362,6 +1362,9 @@ int tw_plan_get_info(const tw_plan* p, tw_plan_info* info) {
   info->row_copies = p->runs ? p->row_copies : p->split ? 2 : 1;
   info->sm_budget = p->sm_budget;
   info->sparse_payload = p->sparse ? 1 : 0;
+  info->splitk_max = p->d_splitws ? p->splitk_max : 0;
+  info->splitk_max_tokens = (int32_t)kSplitKMaxTokens;
+  info->splitk_min_steps = kSplitKMinSteps;
   int64_t steps = 0;
   for (const SubTile& st : p->subtiles) steps += st.kp_steps;
   info->stage_work = steps;

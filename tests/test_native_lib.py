@@ -44,7 +44,7 @@ def test_library_exports_every_declared_symbol(lib):
 
 
 def test_abi_version(lib):
-    assert lib.tw_abi_version() == 420
+    assert lib.tw_abi_version() == 421
 
 
 def test_sass_is_blackwell_native():
