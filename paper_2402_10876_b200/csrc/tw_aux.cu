@@ -45,18 +45,18 @@ __device__ __forceinline__ void store_from_float(void* p, int32_t dtype, int64_t
 //
 // Grid = (token blocks, column splits), one 32-warp CTA per SM; T is as
 // large as shared memory allows so the column lists (re-read per block) are
-// amortised.  After one barrier the warps walk
-// their columns independently: a lane group of L = T / 8 lanes per column
-// (8 tokens per lane, one 16-byte shared load per entry), 32 / L columns per
-// warp step, columns in descending-nnz order (host) so the groups of a warp
-// finish together.  Each lane group fetches L packed entries (16-bit value,
-// rounded like the TW payload, << 16 | the row's offset in the staged block in
-// 16-byte units) per 4-byte load per lane, two groups
-// ahead, and broadcasts them with shuffles; one fma.rn.f32.f16 (FHFMA: 16-bit
-// operands, fp32 accumulator, no conversions) per token, fp32 accumulation in
-// the list order (the CSC rows of patterns.py:145-214, interleaved by bank
-// class on the host, tw_capi.cu), then one read-modify-write of the TW result
-// (accumulate = 1) or a plain store (residual-only column).
+// amortised.  After one barrier the warps walk their columns independently:
+// a lane group of L lanes per column (8 tokens per lane and one 16-byte
+// shared load per entry; 16 tokens and two loads for T = 64), 32 / L columns
+// per warp step, columns in descending-nnz order (host) so the groups of a
+// warp finish together.  Each lane group fetches its column's packed entries
+// (16-bit value, rounded like the TW payload, << 16 | the row's offset in the
+// staged block in 16-byte units) in groups of L, two groups ahead; one
+// fma.rn.f32.f16 (FHFMA: 16-bit operands, fp32 accumulator, no conversions)
+// per token, fp32 accumulation in the list order (the CSC rows of
+// patterns.py:145-214, interleaved by bank class on the host, tw_capi.cu),
+// then one read-modify-write of the TW result (accumulate = 1) or a plain
+// store (residual-only column).
 constexpr int kResThreads = 1024;  // 32 warps: one CTA per SM, 64 registers per thread
 constexpr int kResWarps = kResThreads / 32;
 
@@ -194,7 +194,7 @@ __device__ __forceinline__ void residual_body(const ResidualArgs& args, const in
   // the next kernel may launch; it waits for this grid before touching data
   grid_launch_dependents();
   constexpr int kStep = kCols * (NT / 32);
-  constexpr int G = L;  // entries per group (1 per lane, one 4-byte load)
+  constexpr int G = L;  // entries per group (one per lane of the column)
   // entries: 16-bit value << 16 | row offset in 16-byte units (row * T / 8)
   const uint32_t zrow = static_cast<uint32_t>(K) * (T / 8);
   const uint8_t* sAa = reinterpret_cast<const uint8_t*>(sA + tokA);
@@ -212,14 +212,15 @@ __device__ __forceinline__ void residual_body(const ResidualArgs& args, const in
   int cs = c0 + warp * kCols;
   // columns past c1 read the (zero-row) padding at the start of the lists
   int4 m = cs + sub < c1 ? __ldg(args.meta + cs + sub) : make_int4(0, 0, 0, 0);
-  // first two entry groups of the current column; for later columns they are
-  // loaded at the end of the previous step, so their latency overlaps that
-  // step's stores and this step's setup
-  // 32-token blocks (4 lanes per column): every lane loads its column's whole
-  // entry group with one 16-byte load instead of one entry plus 4 shuffles
-  // (the shuffles share the MIO queue with the shared-memory loads: 41.3 ->
-  // 39.3 us on 3072 x 768).  With 16 tokens per lane the extra registers
-  // cost more than the shuffles.
+  // Entry groups: lane tl of a column holds entry tl of each group and the
+  // group is broadcast with shuffles -- except for 32-token blocks (4 lanes
+  // per column, 8 tokens each), where every lane loads its column's whole
+  // group with one 16-byte load (the shuffles share the MIO queue with the
+  // shared-memory loads: 41.3 -> 39.3 us on 3072 x 768; with 16 tokens per
+  // lane the extra registers cost more than the shuffles).  The current
+  // column's first two groups are loaded here; later columns' at the end of
+  // the previous step, so their latency overlaps its stores and the next
+  // step's setup.
   constexpr bool kGL = G == 4 && TPL == 8;
   uint32_t c = 0, n1 = 0;
   uint4 c4 = make_uint4(0u, 0u, 0u, 0u), n4 = c4;
