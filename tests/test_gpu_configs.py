@@ -68,6 +68,8 @@ def test_configs0_full_size():
     (768, 768, 500, 0.75, 128, 0.0),
     (1000, 700, 333, 0.6, 64, 0.02),    # ragged + TEW through K2 (2K-row staged block)
     (3072, 768, 256, 0.75, 128, 0.015),
+    (3072, 768, 40, 0.75, 128, 0.0),     # small M on long tiles: split-K
+    (3072, 768, 64, 0.75, 128, 0.015),   # split-K K1 under TEW
 ])
 def test_fp32_compute_on_unrounded_inputs(k, n, m, s, g, delta):
     """compute_dtype='fp32' on fp32 data that is NOT fp16-representable:
