@@ -52,6 +52,26 @@ def main():
         s, e = s[live], e[live & (e > 0)]
         print(f"{k}x{n}: CTAs {int(live.sum())}: start {(int(s.min()) - t0) / 1e3:6.2f}..{(int(s.max()) - t0) / 1e3:6.2f} us, "
               f"done {(int(e.min()) - t0) / 1e3:6.2f}..{(int(e.max()) - t0) / 1e3:6.2f} us", flush=True)
+        # clock64 phases per CTA (cycles from the CTA's prologue end)
+        ph = []
+        for c in range(c0, c0 + b):
+            tc = t[c]
+            if tc[3072] == 0:
+                continue
+            ful = tc[1024:2048]
+            ns = int((ful != 0).sum())
+            ep = tc[2048:2560].view(-1, 2)
+            ep = ep[ep[:, 0] > 0]
+            if ns < 2 or len(ep) == 0:
+                continue
+            first, last = int(ful[0] - tc[3072]), int(ful[ns - 1] - tc[3072])
+            endc = int(ep[-1, 1] - tc[3072])
+            ph.append((first, (last - first) / (ns - 1), endc - last, ns, len(ep)))
+        if ph:
+            import statistics as st
+            cols = list(zip(*ph))
+            print("    first-full {:.0f} | cycles/stage {:.0f} | last-full->end {:.0f} | stages {:.0f} | units {:.1f}"
+                  .format(*(st.median(v) for v in cols)), flush=True)
         c0 += b
 
 
