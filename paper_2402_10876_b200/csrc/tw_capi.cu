@@ -174,7 +174,7 @@ struct tw_plan {
     const void* x; int64_t m, ld_x; void* ct; int64_t ld_ct; int32_t out_dtype;
     const int32_t* rowmap; int64_t out_rows; bool plan_layout; int32_t budget;
     int flags, no_tma_store, strided, force_owner, gran, split1, run_max_units, no_sparse,
-        sparse_resident, splitk;
+        sparse_resident, splitk, pair;
     long long* trace;
     bool operator==(const Key& o) const { return std::memcmp(this, &o, sizeof(Key)) == 0; }
   };
@@ -1416,13 +1416,14 @@ static int check_io(const tw_plan* p, const void* x, int64_t m, int64_t ld_x, co
 // read on every call (getenv is cheap) so tests can flip them per call.
 struct LaunchEnv {
   int flags, no_tma_store, strided, force_owner, gran, split1, run_max_units, no_sparse,
-      sparse_resident, splitk;
+      sparse_resident, splitk, pair;
   long long* trace;
   bool operator==(const LaunchEnv& o) const {
     return flags == o.flags && no_tma_store == o.no_tma_store && strided == o.strided &&
            force_owner == o.force_owner && gran == o.gran && split1 == o.split1 &&
            run_max_units == o.run_max_units && no_sparse == o.no_sparse &&
-           sparse_resident == o.sparse_resident && splitk == o.splitk && trace == o.trace;
+           sparse_resident == o.sparse_resident && splitk == o.splitk && pair == o.pair &&
+           trace == o.trace;
   }
 };
 
@@ -1440,6 +1441,8 @@ static LaunchEnv read_launch_env() {
   e.sparse_resident = env_int("TW_SPARSE_RESIDENT", 0);
   // split-K for small M: -1 = when M <= kSplitKMaxTokens, 0 = never, 1 = forced
   e.splitk = env_int("TW_SPLITK", -1);
+  // paired units on streamed run-path plans (two units share each payload stage)
+  e.pair = env_int("TW_PAIR", 0);
   e.trace = g_trace;
   return e;
 }
@@ -1642,13 +1645,18 @@ static int build_tw_launch(const tw_plan* p, const void* x, int64_t m, int64_t l
   // stream the payload: the TMA boxes need the deeper 4 x 48 KB ring more
   // than the payload needs residency (768^2: 9.3 -> 8.7 us).
   bool use_runs = false;
+  int64_t min_units = 0;  // owner mode: fewest units of an active CTA
   if (plan_layout && p->runs) {
     int64_t max_units = 0;
     if (a.owner) {
+      min_units = INT64_MAX;
       for (int i = 0; i < grid; ++i)
-        if (work.w[i].usz > 0)
-          max_units = std::max<int64_t>(
-              max_units, (work.w[i].e - work.w[i].b + work.w[i].usz - 1) / work.w[i].usz);
+        if (work.w[i].usz > 0) {
+          const int64_t u = (work.w[i].e - work.w[i].b + work.w[i].usz - 1) / work.w[i].usz;
+          max_units = std::max<int64_t>(max_units, u);
+          min_units = std::min<int64_t>(min_units, u);
+        }
+      if (min_units == INT64_MAX) min_units = 0;
     } else {
       max_units = (a.n_units + grid - 1) / grid;
     }
@@ -1670,6 +1678,11 @@ static int build_tw_launch(const tw_plan* p, const void* x, int64_t m, int64_t l
                       (uint64_t)p->k * p->row_copies, (uint64_t)ld_x, 64, 1u << c, 128) != TW_OK)
         return TW_ERR_INVALID_INPUT;
   }
+  // paired units: owner CTAs (one sub-tile each) on the streamed run path
+  // (every active CTA has two units or more: a single unit gains nothing and
+  // would only run on the shallower 2-slot ring)
+  a.pair = (env.pair && a.owner && !resident && a.runs && !sparse && !L.splitk && min_units >= 2)
+               ? 1 : 0;
   return TW_OK;
 }
 
@@ -1690,7 +1703,8 @@ static int get_launch(const tw_plan* p, const void* x, int64_t m, int64_t ld_x, 
   key.flags = env.flags; key.no_tma_store = env.no_tma_store; key.strided = env.strided;
   key.force_owner = env.force_owner; key.gran = env.gran; key.split1 = env.split1;
   key.run_max_units = env.run_max_units; key.no_sparse = env.no_sparse;
-  key.sparse_resident = env.sparse_resident; key.splitk = env.splitk; key.trace = env.trace;
+  key.sparse_resident = env.sparse_resident; key.splitk = env.splitk; key.pair = env.pair;
+  key.trace = env.trace;
   if (!(p->cache_valid && p->cache_key == key)) {
     p->cache_valid = false;
     if (int st = build_tw_launch(p, x, m, ld_x, ct, ld_ct, out_dtype, rowmap, out_rows,

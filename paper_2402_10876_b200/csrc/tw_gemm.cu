@@ -288,7 +288,7 @@ __device__ __forceinline__ void epilogue_unit(const GemmArgs& args, const CUtens
 // owner-mode work entry at `work` (this CTA's own).  Called by tw_gemm_kernel (one layer per
 // launch) and tw_gemm_group_kernel (several independent layers in one
 // launch); the tensor maps and args live in kernel parameter space.
-template <bool kRes>
+template <bool kRes, bool kPair>
 __device__ __forceinline__ void gemm_body(const CUtensorMap& map_pay, const CUtensorMap& map_out,
                                           const RunMaps& run_maps, const GemmArgs& args,
                                           const CtaWork* work, const int cta, const int ncta,
@@ -299,8 +299,15 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& map_pay, const CUte
   // 1024-byte aligned base derived by offset so the compiler keeps the shared
   // address space (plain LDS/STS instead of generic loads)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint8_t* sX = smem;                                    // [kStages][kXBytes]
-  uint8_t* sP = smem + kStages * kXBytes;                // streamed: [kStages][kPBytes]
+  // paired units (kPair: streamed run path, args.pair set by the host): 2
+  // ring slots of [2 units][kXBytes] A^T + the payload
+  constexpr bool pair = !kRes && kPair;
+  constexpr int nst = pair ? 2 : kStages;                // ring slots in use
+  constexpr int xstride = pair ? 2 * kXBytes : kXBytes;  // A^T bytes per slot
+  static_assert(kRes || 2 * (2 * kXBytes + kPBytes) <= kStages * (kXBytes + kPBytes),
+                "paired ring fits the streamed ring");
+  uint8_t* sX = smem;                                    // [nst][xstride]
+  uint8_t* sP = smem + nst * xstride;                    // streamed: [nst][kPBytes]
                                                          // resident: [kResSteps][kPBytes]
   uint8_t* sStg = smem + kStages * C::kStageBytes + C::kPayloadRegion;
   uint8_t* bar_region = sStg + kEpilogueWarps * kStgBytes;
@@ -428,15 +435,26 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& map_pay, const CUte
       while (walk.next(args, sg)) {
         const int n = (sg.ue - sg.ub + 15) & ~15;
         const int chunks = (n + 63) >> 6;
+        // paired units: the next unit (same sub-tile, same stages) rides along
+        int ub2 = 0, chunks2 = 0;
+        if (pair) {
+          Walker w2 = walk;
+          Seg s2;
+          if (w2.next(args, s2)) {
+            walk = w2;
+            ub2 = s2.ub;
+            chunks2 = (((s2.ue - s2.ub + 15) & ~15) + 63) >> 6;
+          }
+        }
         const int32_t* bf =
             args.box_first + static_cast<int64_t>(sg.d.idx_row) * args.box_stride + sg.d.k0;
         int b0 = __ldg(bf), b1 = __ldg(bf + 1);
         for (int ks = 0; ks < sg.d.kp_steps; ++ks, ++gs) {
-          const int stage = gs % kStages;
+          const int stage = gs % nst;
           const int nb0 = ks + 1 < sg.d.kp_steps ? __ldg(bf + ks + 1) : 0;
           const int nb1 = ks + 1 < sg.d.kp_steps ? __ldg(bf + ks + 2) : 0;
           const uint32_t e = b0 + lane < b1 ? __ldg(args.boxes + b0 + lane) : 0u;
-          mbar_wait(&empty[stage], ((gs / kStages) & 1) ^ 1u);
+          mbar_wait(&empty[stage], ((gs / nst) & 1) ^ 1u);
           if (trace && lane == 0 && gs < 1024) {
             trace[gs] = clock64();
             trace[3076] += b1 - b0;
@@ -444,8 +462,9 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& map_pay, const CUte
           const bool skip_p = kRes || (flags & kFlagSkipP);
           const bool skip_a = flags & kFlagSkipA;
           if (lane == 0) {
-            mbar_arrive_expect_tx(&full[stage], (skip_p ? 0u : static_cast<uint32_t>(kPBytes)) +
-                                                    (skip_a ? 0u : static_cast<uint32_t>(chunks * kBK * 128)));
+            mbar_arrive_expect_tx(&full[stage],
+                                  (skip_p ? 0u : static_cast<uint32_t>(kPBytes)) +
+                                      (skip_a ? 0u : static_cast<uint32_t>((chunks + chunks2) * kBK * 128)));
             if (!skip_p)
               tma_load_2d(sP + stage * kPBytes, &map_pay, &full[stage], (sg.d.k0 + ks) * kBK,
                           sg.d.pay_row);
@@ -455,9 +474,12 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& map_pay, const CUte
             const uint32_t ej = jj == 0 ? e : __ldg(args.boxes + j);
             const int slot = static_cast<int>(ej & 63u), code = static_cast<int>((ej >> 6) & 7u);
             const int32_t pos = static_cast<int32_t>(ej >> 9);
-            uint8_t* dst = sX + stage * kXBytes + slot * 128;
+            uint8_t* dst = sX + stage * xstride + slot * 128;
             for (int c = 0; c < chunks; ++c)
               tma_load_2d(dst + c * kChunkBytes, &run_maps.m[code], &full[stage], sg.ub + c * 64, pos);
+            for (int c = 0; c < chunks2; ++c)
+              tma_load_2d(dst + kXBytes + c * kChunkBytes, &run_maps.m[code], &full[stage],
+                          ub2 + c * 64, pos);
           }
           b0 = nb0;
           b1 = nb1;
@@ -659,17 +681,31 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& map_pay, const CUte
         const uint32_t idesc = umma_idesc_f16(kBN, (sg.ue - sg.ub + 15) & ~15, in_fmt,
                                               /*a (payload) K-major*/ 0u, /*b (A^T) MN-major*/ 1u) |
                                (sparse ? 4u : 0u);
+        // paired units: the next unit's MMAs follow each stage's into the
+        // other accumulator (j is even here, so that is accumulator 1)
+        bool two = false;
+        uint32_t idesc2 = 0;
+        if (pair) {
+          Walker w2 = walk;
+          Seg s2;
+          if (w2.next(args, s2)) {
+            walk = w2;
+            two = true;
+            idesc2 = umma_idesc_f16(kBN, (s2.ue - s2.ub + 15) & ~15, in_fmt, 0u, 1u);
+          }
+        }
         mbar_wait(&tempty[acc], ((j >> 1) & 1) ^ 1u);
+        if (two) mbar_wait(&tempty[acc ^ 1], (((j + 1) >> 1) & 1) ^ 1u);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * kTileN;
         for (int ks = 0; ks < sg.d.kp_steps; ++ks, ++gs) {
-          const int stage = gs % kStages;
+          const int stage = gs % nst;
           if (kRes) mbar_wait(&pfull[sparse ? ks >> 1 : ks], 0);
-          mbar_wait(&full[stage], (gs / kStages) & 1);
+          mbar_wait(&full[stage], (gs / nst) & 1);
           if (trace && gs < 1024) trace[1024 + gs] = clock64();
           tc_fence_after();
           if (!args.runs) fence_proxy_async_smem();  // cp.async (generic proxy) writes -> tcgen05 reads
-          const uint32_t x0 = smem_u32(sX + stage * kXBytes);
+          const uint32_t x0 = smem_u32(sX + stage * xstride);
           if (sparse && !(flags & kFlagSkipMma)) {
             // two tcgen05.mma.sp of K = 32 logical rows: A = this stage's 32
             // compressed columns (64 B of the 128-B SW128 row of box ks / 2,
@@ -700,11 +736,21 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& map_pay, const CUte
               const uint64_t bdesc = umma_desc_sw128(x0 + kk * 2048, kChunkBytes, 1024);
               umma_f16(d_tmem, adesc, bdesc, idesc, (ks != 0) || (kk != 0));
             }
+            if (two) {
+              const uint32_t d2 = tmem_base + (acc ^ 1) * kTileN;
+#pragma unroll
+              for (int kk = 0; kk < kBK / 16; ++kk) {
+                const uint64_t adesc = umma_desc_sw128(p0 + kk * 32, 16, 1024);
+                const uint64_t bdesc = umma_desc_sw128(x0 + kXBytes + kk * 2048, kChunkBytes, 1024);
+                umma_f16(d2, adesc, bdesc, idesc2, (ks != 0) || (kk != 0));
+              }
+            }
           }
           umma_commit(&empty[stage]);
         }
         umma_commit(&tfull[acc]);
-        ++j;
+        if (two) umma_commit(&tfull[acc ^ 1]);
+        j += two ? 2 : 1;
       }
     }
   } else if (warp >= kEpilogueWarp0 || (wide_epi && warp >= kGatherWarp0)) {
@@ -773,14 +819,14 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& map_pay, const CUte
   }
 }
 
-template <bool kRes>
+template <bool kRes, bool kPair>
 __global__ void __launch_bounds__(kThreads, 1)
     tw_gemm_kernel(const __grid_constant__ CUtensorMap map_pay,
                    const __grid_constant__ CUtensorMap map_out,
                    const __grid_constant__ RunMaps run_maps, const __grid_constant__ GemmArgs args,
                    const __grid_constant__ WorkTable work) {
-  gemm_body<kRes>(map_pay, map_out, run_maps, args, work.w + blockIdx.x, blockIdx.x, gridDim.x,
-                  blockIdx.x);
+  gemm_body<kRes, kPair>(map_pay, map_out, run_maps, args, work.w + blockIdx.x, blockIdx.x,
+                         gridDim.x, blockIdx.x);
 }
 
 // Several independent layers in ONE launch (TwPlanGroup): layer p owns CTAs
@@ -797,9 +843,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int cta = g.cta_local[b];
   const int ncta = g.plan_ctas[p];
   if (g.resident[p])
-    gemm_body<true>(g.map_pay[p], g.map_out[p], g.run_maps[p], g.args[p], work.w + b, cta, ncta, b);
+    gemm_body<true, false>(g.map_pay[p], g.map_out[p], g.run_maps[p], g.args[p], work.w + b, cta,
+                           ncta, b);
+  else if (g.args[p].pair)
+    gemm_body<false, true>(g.map_pay[p], g.map_out[p], g.run_maps[p], g.args[p], work.w + b, cta,
+                           ncta, b);
   else
-    gemm_body<false>(g.map_pay[p], g.map_out[p], g.run_maps[p], g.args[p], work.w + b, cta, ncta, b);
+    gemm_body<false, false>(g.map_pay[p], g.map_out[p], g.run_maps[p], g.args[p], work.w + b, cta,
+                            ncta, b);
 }
 
 }  // namespace
@@ -808,11 +859,14 @@ constexpr int kGroupSmemBytes =
     Cfg<true>::kSmemBytes > Cfg<false>::kSmemBytes ? Cfg<true>::kSmemBytes : Cfg<false>::kSmemBytes;
 
 cudaError_t configure_gemm_kernels() {
-  cudaError_t e = cudaFuncSetAttribute(tw_gemm_kernel<true>,
+  cudaError_t e = cudaFuncSetAttribute(tw_gemm_kernel<true, false>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        Cfg<true>::kSmemBytes);
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(tw_gemm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  e = cudaFuncSetAttribute(tw_gemm_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           Cfg<false>::kSmemBytes);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(tw_gemm_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            Cfg<false>::kSmemBytes);
   if (e != cudaSuccess) return e;
   return cudaFuncSetAttribute(tw_gemm_group_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -855,8 +909,13 @@ cudaError_t launch_tw_gemm(const CUtensorMap& map_pay, const CUtensorMap& map_ou
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   if (resident)
-    return cudaLaunchKernelEx(&cfg, tw_gemm_kernel<true>, map_pay, map_out, run_maps, args, work);
-  return cudaLaunchKernelEx(&cfg, tw_gemm_kernel<false>, map_pay, map_out, run_maps, args, work);
+    return cudaLaunchKernelEx(&cfg, tw_gemm_kernel<true, false>, map_pay, map_out, run_maps, args,
+                              work);
+  if (args.pair)
+    return cudaLaunchKernelEx(&cfg, tw_gemm_kernel<false, true>, map_pay, map_out, run_maps, args,
+                              work);
+  return cudaLaunchKernelEx(&cfg, tw_gemm_kernel<false, false>, map_pay, map_out, run_maps, args,
+                            work);
 }
 
 }  // namespace tw

@@ -80,6 +80,10 @@ struct GemmArgs {
   int32_t sparse;
   const uint32_t* meta;     // [n_sub][meta_cols][128] u32, TMEM lane order (tw_capi.cu)
   int32_t meta_cols;        // sparse MMAs per sub-tile (2 per 64-row stage)
+  // paired units (owner mode, streamed payload, run path): two consecutive
+  // units of the CTA's sub-tile share every payload stage (2 ring slots of
+  // payload + both units' A^T boxes; accumulators 0 and 1)
+  int32_t pair;
 };
 constexpr int kSparseMaxTokens = 224;  // sparse units: accumulators at 0 / 256, metadata at 480
 constexpr int kMetaCol0 = 480;         // 4-aligned; 32 columns = 16 stages (K' <= 1024)

@@ -339,6 +339,28 @@ def test_tew_workspace_path_bit_identical(out_dtype):
     assert torch.equal(o_ws, o_sc)
 
 
+@pytest.mark.parametrize("sms,m", [(50, 8192), (24, 3001), (24, 8192)])
+def test_paired_units_bit_identical(sms, m, monkeypatch):
+    """TW_PAIR=1 (two units of a CTA's sub-tile share every streamed payload
+    stage, accumulators 0 and 1) gives exactly the regular ring's output on a
+    streamed row-run plan with several units per CTA, including a CTA with an
+    odd unit count (its last unit runs alone)."""
+    k, n = 3072, 768
+    w = tw.round_to(tw.synthetic_matrix(0, k, n, tw.STREAM_WEIGHTS), "fp16")
+    _, tsm = tw.prune_tw(w, 0.75, 128)
+    plan = tw.TwPlan(tw.encode_cto(tsm), row_layout="runs")
+    plan.set_sm_budget(sms)
+    a = tw.round_to(tw.synthetic_matrix(0, m, k, tw.STREAM_INPUT), "fp16")
+    x = plan.prepare(a)
+    regular = plan.run(x, out_dtype="fp16")
+    monkeypatch.setenv("TW_PAIR", "1")
+    paired = plan.run(x, out_dtype="fp16")
+    assert torch_equal(regular, paired)
+    idx = np.arange(0, m, max(1, m // 64))
+    ref = orc.c_gemm_cto_enc(a[idx], tw.encode_cto(tsm))
+    assert tw.relative_error(paired.float().t().cpu().numpy()[idx], ref) <= TOL["fp16"]
+
+
 @pytest.mark.parametrize("compute,m,out_dtype", [
     ("fp16", 8192, "fp16"), ("bf16", 4096, "bf16"), ("fp16", 1000, "fp16"), ("fp16", 640, "fp32"),
 ])
